@@ -1,0 +1,215 @@
+/*
+ * qcs_abi.h -- C ABI of the B200 state-vector engine (libqcs_b200.so).
+ *
+ * The reference (arXiv 2411.15332, /root/reference/proj) has no FFI: its hot path is a set of
+ * free C++ functions in namespace qcsim.  Each entry point below replaces one of them; the
+ * comment names the reference declaration (path:line under proj/).  Plain pointers and sizes
+ * only: no torch or C++ types cross this boundary.
+ *
+ * Conventions
+ *  - Complex numbers are interleaved (re, im) doubles, the byte layout of
+ *    std::complex<double>; a state of n qubits is 2*2^n doubles (core.hpp:66-76).
+ *  - Qubit q is bit (n-1-q) of the basis index: qubit 0 is the most significant bit
+ *    (core.hpp:64-66).
+ *  - A placement lists its qubits in gate-local order: local index bit (arity-1-i) is
+ *    qubits[i].  Contiguous ascending lists are the reference's own placements
+ *    (circuit.hpp:10-15); any other distinct list is accepted as well (a superset).
+ *  - Every function returns QCS_OK or an error code mirroring the reference's exception
+ *    hierarchy (core.hpp:13-36); qcs_last_error() gives the message (thread-local).  The
+ *    library never falls back to the CPU: without a CUDA device calls fail with QCS_ERR_CUDA.
+ *  - Calls on one state are asynchronous on that state's stream unless they return host data;
+ *    qcs_state_sync surfaces deferred CUDA errors.  One state must not be used from two threads
+ *    at once; distinct states may (the reference is reentrant).
+ */
+#ifndef QCS_ABI_H
+#define QCS_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QCS_MAX_ARITY 3 /* largest catalog gate (CCX, CSwap), gates.cpp:193-194 */
+
+/* status codes -- SimError (core.hpp:13-16) and its subclasses (core.hpp:18-36) */
+enum {
+    QCS_OK = 0,
+    QCS_ERR_CAPACITY = 1,  /* CapacityError  (core.hpp:18-21) */
+    QCS_ERR_DIMENSION = 2, /* DimensionError (core.hpp:23-26) */
+    QCS_ERR_ENCODING = 3,  /* EncodingError  (core.hpp:28-31) */
+    QCS_ERR_PARSE = 4,     /* ParseError     (core.hpp:33-36) */
+    QCS_ERR_SIM = 5,       /* SimError       (core.hpp:13-16) */
+    QCS_ERR_CUDA = 6,      /* device failure or no device */
+    QCS_ERR_NCCL = 7,      /* collective failure */
+    QCS_ERR_ARG = 8        /* null pointer / malformed argument */
+};
+
+/* engines and sign methods -- engine.hpp:10, rh.hpp:22 */
+enum { QCS_ENGINE_DENSE = 0, QCS_ENGINE_DAX = 1, QCS_ENGINE_DAS = 2, QCS_ENGINE_RH_DAX = 3 };
+enum { QCS_SIGN_NONOPT = 0, QCS_SIGN_QUARTER = 1, QCS_SIGN_BLOCK = 2, QCS_SIGN_LOGARITHM = 3 };
+enum { QCS_STEP_GATES = 0, QCS_STEP_DIAG = 1 };               /* CircuitStep::Kind, circuit.hpp:30 */
+enum { QCS_STRUCT_DENSE = 0, QCS_STRUCT_DAX = 1, QCS_STRUCT_DAS = 2, QCS_STRUCT_RH = 3 };
+enum { QCS_MEM_HOST = 0, QCS_MEM_DEVICE = 1 };
+
+const char* qcs_last_error(void);
+const char* qcs_version(void);
+int qcs_device_count(int* count);
+
+/* dense_cap / set_dense_cap (core.hpp:38-43): element cap of the Matrix (dense) engine,
+ * default 2^26; QCS_ENGINE_DENSE raises QCS_ERR_CAPACITY where the reference would. */
+int qcs_set_dense_cap(uint64_t cap);
+uint64_t qcs_dense_cap(void);
+
+/* ------------------------------------------------------------------ gate catalog
+ * gates.hpp:29 gate_catalog, :31 gate_known, :36 gate_catalog_lookup, :41 canonical_params.
+ * Matrices are computed on the host exactly as the reference computes them, so the device
+ * receives identical bytes. */
+int qcs_gate_catalog_size(void);
+int qcs_gate_catalog_entry(int index, const char** name, int* arity, int* param_count,
+                           double* zero_ratio);
+int qcs_gate_lookup(const char* name, const double* params, int num_params,
+                    double* matrix_out /* 2*4^arity doubles, capacity 2*64 */, int* arity_out,
+                    const char** canonical_name);
+int qcs_canonical_params(const char* name, double* out /* capacity 4 */, int* count);
+
+/* ------------------------------------------------------------------ device state
+ * StateVector (core.hpp:64-76), held in HBM as 2^n x 16 B. */
+typedef struct qcs_state qcs_state;
+
+/* StateVector(n, basis_index), core.cpp:22-28: 1 <= n <= 62, basis_index < 2^n. */
+int qcs_state_create(int n, int device, uint64_t basis_index, qcs_state** out);
+/* Borrow caller-owned device memory (2^n x 16 B on `device`) and a CUDA stream (NULL = the
+ * legacy default stream).  The handle never frees borrowed memory. */
+int qcs_state_wrap(int n, int device, void* device_amps, void* cuda_stream, qcs_state** out);
+int qcs_state_destroy(qcs_state* s);
+int qcs_state_info(const qcs_state* s, int* n, int* device, void** device_amps, void** stream);
+int qcs_state_set_basis(qcs_state* s, uint64_t basis_index);
+/* Copy amplitudes [first, first+count) from / to host memory (pinned memory is fastest). */
+int qcs_state_upload(qcs_state* s, const double* host, uint64_t first, uint64_t count);
+int qcs_state_download(qcs_state* s, double* host, uint64_t first, uint64_t count);
+int qcs_state_copy(qcs_state* dst, const qcs_state* src);
+int qcs_state_sync(qcs_state* s);
+/* Seeded i.i.d. Gaussian re/im, L2-normalised (a synthetic-input generator on the device). */
+int qcs_state_random(qcs_state* s, uint64_t seed);
+
+/* Pinned host buffers for fast transfers (cudaHostAlloc / cudaFreeHost). */
+int qcs_host_alloc(size_t bytes, void** out);
+int qcs_host_free(void* p);
+
+/* ------------------------------------------------------------------ one step at a time */
+typedef struct {
+    int arity;            /* 1..QCS_MAX_ARITY */
+    const int* qubits;    /* arity distinct reference qubit indices, gate-local order */
+    const double* matrix; /* row-major 2^arity x 2^arity, interleaved (re, im) */
+    const char* name;     /* catalog name or NULL; used for the RH dispatch and reports */
+} qcs_placement;
+
+/* One gates step: s <- step_matrix(placements) * s, computed without materialising the
+ * operator.  Replaces step_matrix_dax (engine.hpp:38) + dax_mvm (dax.hpp:37) and
+ * step_matrix_das (engine.hpp:39) + das_mvm (das.hpp:39): the results are identical.
+ * Bit-exact with the reference for single-placement steps and for steps whose values
+ * are all in {0, +-1, +-i}; otherwise within 1e-12 per amplitude. */
+int qcs_apply_step(qcs_state* s, const qcs_placement* placements, int count);
+
+/* One diagonal sign step (circuit.hpp:20-25, engine.cpp:62-80): negate the amplitudes whose
+ * index is listed XOR flip_rest.  Bit-exact. */
+int qcs_apply_diag(qcs_state* s, const uint64_t* flipped, uint64_t count, int flip_rest);
+
+/* rh_mvm(rh_build(n), s) (rh.hpp:64-66): H^{(x)n} as a Walsh-Hadamard butterfly, scaled once
+ * by exp2(-n/2) (rh.cpp:20).  Within 1e-12 of the reference (whose own error is larger). */
+int qcs_apply_rh(qcs_state* s);
+
+/* ------------------------------------------------------------------ reductions
+ * StateVector::norm / probabilities (core.cpp:30-40). */
+int qcs_norm(qcs_state* s, double* out);
+/* probabilities into host memory (mem = QCS_MEM_HOST) or device memory (QCS_MEM_DEVICE),
+ * 2^n doubles, bit-exact (re*re + im*im). */
+int qcs_probabilities(qcs_state* s, double* out, int mem);
+/* argmax of the probabilities, first index on ties (std::max_element, circuit_io.cpp:111-112) */
+int qcs_argmax(qcs_state* s, uint64_t* index, double* probability);
+/* k largest probabilities, descending, ties to the lower index (circuit_io.cpp:140-147) */
+int qcs_topk(qcs_state* s, int k, uint64_t* indices, double* probabilities);
+/* amplitudes at arbitrary indices (host index list, host output 2*count doubles) */
+int qcs_gather(qcs_state* s, const uint64_t* indices, uint64_t count, double* out);
+
+/* ------------------------------------------------------------------ whole circuits */
+typedef struct {
+    int kind;  /* QCS_STEP_GATES or QCS_STEP_DIAG */
+    int stage; /* builder annotation, surfaces in reports (circuit.hpp:34) */
+    const qcs_placement* placements;
+    int num_placements;
+    const uint64_t* flipped; /* diag steps; sorted or not */
+    uint64_t num_flipped;
+    int flip_rest;
+} qcs_step;
+
+typedef struct {
+    int sign_method;     /* SimOptions::sign_method (engine.hpp:42); reports only */
+    uint64_t block_size; /* SimOptions::block_size (engine.hpp:43); 0 = optimal */
+    int fuse;            /* 0: one pass per step in circuit order (bit-exact per step);
+                            1: fuse consecutive operations into shared-memory passes
+                               (within 1e-12); default 1 */
+} qcs_sim_options;
+
+typedef struct {             /* StepReport, engine.hpp:16-24 */
+    int structure;           /* QCS_STRUCT_* */
+    int stage;
+    uint64_t matrix_bytes;   /* accounting bytes of the structure (24 B / entry, RH 16 B) */
+    uint64_t dense_bytes;    /* 2^{2n} * 16, saturating */
+    uint64_t entry_count;    /* stored nonzeros (0 for RH) */
+    uint64_t sign_count;
+    uint64_t madd_count;
+} qcs_step_report;
+
+/* simulate(Circuit, Engine, SimOptions) (engine.hpp:46, engine.cpp:153-210) applied to the
+ * state `s` in place.  The caller prepares s (normally qcs_state_set_basis(s, initial)).
+ * reports: num_steps entries or NULL.  Circuit::validate rules apply (circuit.cpp:41-62). */
+int qcs_simulate(qcs_state* s, const qcs_step* steps, int num_steps, int engine,
+                 const qcs_sim_options* opts, qcs_step_report* reports);
+
+/* memory_report (engine.hpp:49, engine.cpp:212-234): accounting without a state update. */
+int qcs_memory_report(int n, const qcs_step* steps, int num_steps, int engine,
+                      qcs_step_report* reports);
+
+/* ------------------------------------------------------------------ compressed structures
+ * The device gate encoder: materialise step_matrix_dax / step_matrix_das (engine.hpp:38-39)
+ * on the GPU, byte-identical to the reference, without ever forming dense operators.
+ * Output arrays are host (QCS_MEM_HOST) or device (QCS_MEM_DEVICE) memory of `capacity`
+ * entries; *count receives the entry count (also when capacity is too small, which returns
+ * QCS_ERR_CAPACITY).  Passing capacity 0 queries the count. */
+int qcs_step_dax(int n, const qcs_placement* placements, int num_placements, int device,
+                 uint64_t* rows, uint64_t* cols, double* values, uint64_t capacity, int mem,
+                 uint64_t* count);
+/* DasEntry stream (das.hpp:13-27): dis, last_in_row (0/1 bytes), value. */
+int qcs_step_das(int n, const qcs_placement* placements, int num_placements, int device,
+                 uint64_t* dis, uint8_t* last_in_row, double* values, uint64_t capacity, int mem,
+                 uint64_t* count);
+/* dax_mvm (dax.hpp:37, dax.cpp:96-103) on explicit entries, out-of-place: out = M * in.
+ * Entries must be sorted by row (the DaxMatrix invariant, dax.hpp:20-21). */
+int qcs_dax_mvm(const uint64_t* rows, const uint64_t* cols, const double* values, uint64_t count,
+                int mem, const qcs_state* in, qcs_state* out);
+/* das_mvm (das.hpp:39, das.cpp:131-150) on an explicit stream, out-of-place. */
+int qcs_das_mvm(const uint64_t* dis, const uint8_t* last_in_row, const double* values,
+                uint64_t count, int mem, const qcs_state* in, qcs_state* out);
+
+/* ------------------------------------------------------------------ profiling hooks */
+/* Number of kernels this library launched since load (process-wide). */
+uint64_t qcs_kernel_launches(void);
+/* Record / read CUDA events on the state's stream (for timing kernels on the launching stream). */
+int qcs_event_record(qcs_state* s, int slot);
+int qcs_event_elapsed_ms(qcs_state* s, int slot_begin, int slot_end, float* ms);
+/* Per-launch timing: when enabled, every kernel the library launches for this state is
+ * bracketed by CUDA events on the state's stream and attributed to its kernel class together
+ * with its algorithmic HBM bytes (32 B per touched amplitude, whole 32-byte sectors). */
+int qcs_timing_enable(qcs_state* s, int enable);
+int qcs_timing_reset(qcs_state* s);
+int qcs_timing_count(qcs_state* s, int* count); /* synchronises; number of kernel classes */
+int qcs_timing_entry(qcs_state* s, int index, const char** kernel_class, uint64_t* launches,
+                     double* total_ms, double* algorithmic_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QCS_ABI_H */

@@ -1,0 +1,131 @@
+// kernels.hpp -- POD descriptors shared by host planning code and the sm_100a kernels, and
+// the launch entry points of every kernel in this library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace qcs {
+
+// ---------------------------------------------------------------- single-placement gate pass
+// One canonical placement of arity k <= 3, reduced to the sub-cube of the state it touches.
+// "Members" are the 2^nfree amplitudes of one group; free bit i of the member index selects
+// free_bit[i] of the basis index.  Only `rows` (non-identity rows of the gate) are written;
+// each row accumulates its nonzeros in ascending global column order from (0,0) with
+// separately rounded multiply/add, i.e. exactly dax_mvm's per-row sum (dax.cpp:101).
+struct GateDesc {
+    int k;                    // gate bits (zero-inserted when enumerating groups)
+    int nfree;                // enumerated bits per group (0..3)
+    int nrows;                // rows written per group (<= 8)
+    int pos_asc[3];           // gate bit positions, ascending (zero insertion order)
+    std::uint64_t fixed_val;  // gate bits that are constant over the touched sub-cube
+    std::uint64_t free_bit[3];
+    std::uint64_t member_off[8];  // basis-index offset of each member (sum of its free bits)
+    std::uint32_t load_mask;  // members that must be loaded
+    std::uint8_t row_member[8];
+    std::uint8_t nnz[8];
+    std::uint8_t col_member[8][8];
+    double2 val[8][8];
+};
+
+// Kernel classes chosen by the host from the descriptor (for launch shape / specialisation).
+void launch_gate(double2* amps, int n, const GateDesc& d, cudaStream_t st);
+
+// ---------------------------------------------------------------- diagonal sign step
+// negate amplitudes whose index is (listed XOR flip_rest); `flipped` is a sorted device array.
+void launch_diag_sign(double2* amps, int n, const std::uint64_t* flipped_dev, std::uint64_t nflip,
+                      int flip_rest, cudaStream_t st);
+// few listed indices, flip_rest = 0: touch only those amplitudes
+void launch_negate_listed(double2* amps, const std::uint64_t* idx_dev, std::uint64_t count,
+                          cudaStream_t st);
+
+// ---------------------------------------------------------------- fused shared-memory passes
+// A pass loads the 2^m amplitudes whose basis indices differ only in the tile bits, applies a
+// list of tile operations in shared memory / registers, and writes them back: one HBM round
+// trip for many gates.
+enum TileOpKind : std::int32_t {
+    TOP_GATE = 0,    // dense/monomial k<=3 gate on local bits (GateDesc-like tables)
+    TOP_DIAG = 1,    // diagonal phase on up to 3 bits anywhere in the basis index
+    TOP_SIGN = 2,    // diag sign step: flipped list (global memory) XOR flip_rest
+    TOP_WHT = 3,     // unnormalised butterflies (a+b, a-b) over a mask of local bits
+    TOP_SCALE = 4,   // multiply by a real scalar (the RH magnitude, rh.cpp:99-100)
+};
+
+struct TileOp {
+    std::int32_t kind;
+    std::int32_t k;              // gate bits (TOP_GATE/TOP_DIAG)
+    std::int32_t nfree, nrows;   // TOP_GATE
+    std::int32_t lbit[3];        // TOP_GATE: local tile bit of each gate position, ascending
+    std::uint32_t lfixed_val;    // TOP_GATE: fixed gate bits (local mask form)
+    std::uint32_t lfree_bit[3];  // TOP_GATE: local masks of the free bits
+    std::uint32_t load_mask;
+    std::uint64_t gctrl_mask;    // controls outside the tile: required global bits
+    std::uint64_t gctrl_val;
+    std::uint32_t wht_mask;      // TOP_WHT: local bits to transform
+    std::int32_t dpos[3];        // TOP_DIAG: basis-bit positions (descending significance)
+    std::uint64_t flip_off;      // TOP_SIGN: offset into the pass's flipped array
+    std::uint64_t flip_cnt;
+    std::int32_t flip_rest;
+    double scale;                // TOP_SCALE
+    std::uint8_t row_member[8];
+    std::uint8_t nnz[8];
+    std::uint8_t col_member[8][8];
+    double2 val[8][8];           // TOP_GATE rows / TOP_DIAG: val[0][g] = diagonal entry g
+    std::uint8_t dskip[8];       // TOP_DIAG: entry g is exactly 1 (untouched)
+};
+
+struct TilePass {
+    int m;                    // tile bits
+    int bits[16];             // tile bit positions (ascending); local bit j <-> bits[j]
+    int op_begin, op_count;   // range in the op array
+};
+
+// ops_dev / flipped_dev: device arrays shared by all passes of a plan.
+void launch_tile_pass(double2* amps, int n, const TilePass& p, const TileOp* ops_dev,
+                      const std::uint64_t* flipped_dev, cudaStream_t st);
+int tile_max_bits();
+
+// ---------------------------------------------------------------- reductions
+double reduce_norm2(const double2* amps, int n, double* scratch_dev, cudaStream_t st);
+void probabilities(const double2* amps, std::uint64_t dim, double* out_dev, cudaStream_t st);
+void argmax(const double2* amps, std::uint64_t dim, std::uint64_t* idx, double* p, void* scratch_dev,
+            cudaStream_t st);
+void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st);
+void gather(const double2* amps, const std::uint64_t* idx_dev, std::uint64_t count, double2* out_dev,
+            cudaStream_t st);
+void scale(double2* amps, std::uint64_t dim, double s, cudaStream_t st);
+void fill_basis(double2* amps, std::uint64_t dim, std::uint64_t index, cudaStream_t st);
+void fill_random(double2* amps, std::uint64_t dim, std::uint64_t seed, cudaStream_t st);
+
+// ---------------------------------------------------------------- DAX / DAS encoder
+// One step in the reference's left-fold order (engine.cpp:31-52, dax.cpp:58-94).
+struct EncodePlacement {
+    int k;
+    int pos[3];               // basis-bit positions in gate-local order (local bit k-1-i <-> pos[i])
+    int nnz[8];
+    int col[8][8];            // nonzero local columns of each local row, ascending local column
+    double2 val[8][8];
+};
+struct EncodeStep {
+    int n;
+    int np;
+    int sorted;               // enumeration order yields ascending columns (no per-row sort)
+    int order[64];            // placements in enumeration order
+    int nfold;
+    int fold_gate[64];        // fold items in position order: placement index, or -1 = identity
+    std::uint64_t gate_mask;
+    EncodePlacement p[64];
+};
+// Materialise one step (DAX rows/cols/vals, or the DAS stream when das = true) on the device.
+// Returns the entry count; writes outputs only when it does not exceed capacity.
+std::uint64_t encode_step(const EncodeStep& st, bool das, std::uint64_t capacity, std::uint64_t* rows,
+                          std::uint64_t* cols, double2* vals, std::uint64_t* dis, std::uint8_t* last,
+                          bool out_on_device, cudaStream_t s);
+// dax_mvm from row-sorted entries
+void dax_mvm(const std::uint64_t* rows, const std::uint64_t* cols, const double2* vals, std::uint64_t count,
+             const double2* in, double2* out, std::uint64_t dim, int* err_dev, cudaStream_t s);
+void das_mvm(const std::uint64_t* dis, const std::uint8_t* last, const double2* vals, std::uint64_t count,
+             const double2* in, double2* out, std::uint64_t dim, int* err_dev, cudaStream_t s);
+
+}  // namespace qcs

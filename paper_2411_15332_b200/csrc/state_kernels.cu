@@ -1,0 +1,323 @@
+// state_kernels.cu -- diagonal sign steps, reductions and state initialisation (sm_100a).
+//
+// References: DiagSign steps (circuit.hpp:17-25, engine.cpp:62-80) and the StateVector
+// helpers (core.cpp:22-40).  All kernels are HBM streams; grids are sized in multiples of the
+// 148 SMs with grid-stride loops so reductions are deterministic for a given n.
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace qcs {
+namespace {
+
+using u64 = std::uint64_t;
+constexpr int kSMs = 148;
+
+__device__ __forceinline__ double2 neg_exact(double2 x) {
+    // 0 + (-1 + 0i) * x with dax_mvm's rounding: (-1*xr - 0*xi, -1*xi + 0*xr), then 0 + .
+    const double pr = __dsub_rn(__dmul_rn(-1.0, x.x), __dmul_rn(0.0, x.y));
+    const double pi = __dadd_rn(__dmul_rn(-1.0, x.y), __dmul_rn(0.0, x.x));
+    return make_double2(__dadd_rn(0.0, pr), __dadd_rn(0.0, pi));
+}
+
+__device__ __forceinline__ bool listed(const u64* f, u64 nf, u64 i) {
+    u64 lo = 0, hi = nf;
+    while (lo < hi) {
+        const u64 mid = (lo + hi) >> 1;
+        if (__ldg(f + mid) < i) lo = mid + 1; else hi = mid;
+    }
+    return lo < nf && __ldg(f + lo) == i;
+}
+
+__global__ void k_diag_sign(double2* __restrict__ a, u64 dim, const u64* __restrict__ f, u64 nf, int rest) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride) {
+        if (listed(f, nf, i) != (rest != 0)) a[i] = neg_exact(__ldcs(a + i));
+    }
+}
+
+__global__ void k_negate_listed(double2* __restrict__ a, const u64* __restrict__ idx, u64 count) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const u64 j = idx[i];
+        if (i > 0 && idx[i - 1] == j) continue;  // duplicates flip once (binary-search semantics)
+        a[j] = neg_exact(a[j]);
+    }
+}
+
+// ---- reductions: fixed grid, per-block partials in scratch, final pass by block 0 of a
+// second launch, so the summation order depends only on n.
+constexpr int kRedThreads = 512;
+constexpr int kRedBlocks = kSMs * 4;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    if (threadIdx.x < 32)
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void k_norm2_partial(const double2* __restrict__ a, u64 dim, double* part) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride) {
+        const double2 x = __ldcs(a + i);
+        acc += x.x * x.x + x.y * x.y;
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void k_sum_partials(double* part, int count) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) acc += part[i];
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[count] = acc;
+}
+
+__global__ void k_probabilities(const double2* __restrict__ a, u64 dim, double* __restrict__ p) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride) {
+        const double2 x = __ldcs(a + i);
+        p[i] = __dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y));  // std::norm, core.cpp:38
+    }
+}
+
+struct ArgMax {
+    double p;
+    u64 i;
+};
+__device__ __forceinline__ ArgMax better(ArgMax a, ArgMax b) {
+    // larger probability wins; equal -> smaller index (std::max_element keeps the first)
+    if (b.p > a.p || (b.p == a.p && b.i < a.i)) return b;
+    return a;
+}
+
+__global__ void k_argmax_partial(const double2* __restrict__ a, u64 dim, ArgMax* part) {
+    __shared__ ArgMax sh[32];
+    ArgMax best{-1.0, ~u64(0)};
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride) {
+        const double2 x = __ldcs(a + i);
+        best = better(best, ArgMax{__dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)), i});
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ArgMax other{__shfl_down_sync(0xffffffffu, best.p, o), __shfl_down_sync(0xffffffffu, best.i, o)};
+        best = better(best, other);
+    }
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) best = better(best, sh[w]);
+        part[blockIdx.x] = best;
+    }
+}
+
+__global__ void k_argmax_final(ArgMax* part, int count) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        ArgMax best = part[0];
+        for (int i = 1; i < count; ++i) best = better(best, part[i]);
+        part[count] = best;
+    }
+}
+
+__global__ void k_gather(const double2* __restrict__ a, const u64* __restrict__ idx, u64 count,
+                         double2* __restrict__ out) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) out[i] = a[idx[i]];
+}
+
+__global__ void k_scale(double2* __restrict__ a, u64 dim, double s) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride) {
+        const double2 x = __ldcs(a + i);
+        __stcs(a + i, make_double2(x.x * s, x.y * s));
+    }
+}
+
+__global__ void k_fill_basis(double2* __restrict__ a, u64 dim, u64 index) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride)
+        __stcs(a + i, make_double2(i == index ? 1.0 : 0.0, 0.0));
+}
+
+// splitmix64 counter hash -> two uniforms -> Box-Muller: i.i.d. N(0,1) re and im per index.
+__device__ __forceinline__ u64 mix64(u64 z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_fill_random(double2* __restrict__ a, u64 dim, u64 seed) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    const u64 key = mix64(seed);
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride) {
+        const u64 h1 = mix64(key ^ (2 * i)), h2 = mix64(key ^ (2 * i + 1));
+        const double u1 = (double(h1 >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
+        const double u2 = double(h2 >> 11) * 0x1.0p-53;          // [0, 1)
+        const double r = sqrt(-2.0 * log(u1));
+        double sn, cs;
+        sincospi(2.0 * u2, &sn, &cs);
+        __stcs(a + i, make_double2(r * cs, r * sn));
+    }
+}
+
+// ---- top-k (k <= 16): per-thread sorted lists in registers, K rounds of block argmax over
+// the list heads, K candidates per block; the host merges the block candidates.
+constexpr int kTopK = 16;
+
+__global__ void __launch_bounds__(256) k_topk_partial(const double2* __restrict__ a, u64 dim, int k,
+                                                      ArgMax* __restrict__ out) {
+    __shared__ ArgMax sh[8];
+    __shared__ ArgMax win;
+    ArgMax lst[kTopK];
+#pragma unroll
+    for (int j = 0; j < kTopK; ++j) lst[j] = ArgMax{-1.0, ~u64(0)};
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride) {
+        const double2 x = __ldcs(a + i);
+        ArgMax c{__dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)), i};
+        if (!(better(lst[kTopK - 1], c).i == c.i)) continue;
+#pragma unroll
+        for (int j = kTopK - 1; j >= 0; --j) {  // bubble c up the sorted list
+            const ArgMax cur = lst[j];
+            const bool take = better(cur, c).i == c.i;
+            if (take) {
+                if (j + 1 < kTopK) lst[j + 1] = cur;
+                lst[j] = c;
+            }
+        }
+    }
+    int head = 0;
+    for (int round = 0; round < k; ++round) {
+        ArgMax h{-1.0, ~u64(0)};
+#pragma unroll
+        for (int j = 0; j < kTopK; ++j)
+            if (j == head) h = lst[j];
+        ArgMax best = h;
+        for (int o = 16; o > 0; o >>= 1) {
+            ArgMax other{__shfl_down_sync(0xffffffffu, best.p, o), __shfl_down_sync(0xffffffffu, best.i, o)};
+            best = better(best, other);
+        }
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ArgMax b = sh[0];
+            for (int w = 1; w < int(blockDim.x >> 5); ++w) b = better(b, sh[w]);
+            win = b;
+            out[u64(blockIdx.x) * k + round] = b;
+        }
+        __syncthreads();
+        if (h.i == win.i && h.p == win.p && h.i != ~u64(0)) ++head;
+        __syncthreads();
+    }
+}
+
+inline unsigned grid_for(u64 work, int threads) {
+    const u64 want = (work + threads - 1) / threads;
+    const u64 cap = u64(kSMs) * 16;
+    return unsigned(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+}  // namespace
+
+void launch_diag_sign(double2* amps, int n, const std::uint64_t* f, std::uint64_t nf, int rest,
+                      cudaStream_t st) {
+    const u64 dim = u64(1) << n;
+    TimedLaunch tl("diag_sign", 32.0 * double(dim), st);
+    k_diag_sign<<<grid_for(dim, 256), 256, 0, st>>>(amps, dim, f, nf, rest);
+    check_launch("k_diag_sign");
+}
+
+void launch_negate_listed(double2* amps, const std::uint64_t* idx, std::uint64_t count, cudaStream_t st) {
+    if (!count) return;
+    TimedLaunch tl("negate_listed", 64.0 * double(count), st);
+    k_negate_listed<<<grid_for(count, 256), 256, 0, st>>>(amps, idx, count);
+    check_launch("k_negate_listed");
+}
+
+double reduce_norm2(const double2* amps, int n, double* scratch, cudaStream_t st) {
+    const u64 dim = u64(1) << n;
+    k_norm2_partial<<<kRedBlocks, kRedThreads, 0, st>>>(amps, dim, scratch);
+    check_launch("k_norm2_partial");
+    k_sum_partials<<<1, 1024, 0, st>>>(scratch, kRedBlocks);
+    check_launch("k_sum_partials");
+    double h = 0.0;
+    QCS_CUDA(cudaMemcpyAsync(&h, scratch + kRedBlocks, sizeof(double), cudaMemcpyDeviceToHost, st));
+    QCS_CUDA(cudaStreamSynchronize(st));
+    return h;
+}
+
+void probabilities(const double2* amps, std::uint64_t dim, double* out, cudaStream_t st) {
+    k_probabilities<<<grid_for(dim, 256), 256, 0, st>>>(amps, dim, out);
+    check_launch("k_probabilities");
+}
+
+void argmax(const double2* amps, std::uint64_t dim, std::uint64_t* idx, double* p, void* scratch,
+            cudaStream_t st) {
+    ArgMax* part = static_cast<ArgMax*>(scratch);
+    k_argmax_partial<<<kRedBlocks, kRedThreads, 0, st>>>(amps, dim, part);
+    check_launch("k_argmax_partial");
+    k_argmax_final<<<1, 32, 0, st>>>(part, kRedBlocks);
+    check_launch("k_argmax_final");
+    ArgMax h;
+    QCS_CUDA(cudaMemcpyAsync(&h, part + kRedBlocks, sizeof(ArgMax), cudaMemcpyDeviceToHost, st));
+    QCS_CUDA(cudaStreamSynchronize(st));
+    *idx = h.i;
+    *p = h.p;
+}
+
+void gather(const double2* amps, const std::uint64_t* idx, std::uint64_t count, double2* out, cudaStream_t st) {
+    if (!count) return;
+    k_gather<<<grid_for(count, 256), 256, 0, st>>>(amps, idx, count, out);
+    check_launch("k_gather");
+}
+
+void scale(double2* amps, std::uint64_t dim, double s, cudaStream_t st) {
+    k_scale<<<grid_for(dim, 256), 256, 0, st>>>(amps, dim, s);
+    check_launch("k_scale");
+}
+
+void fill_basis(double2* amps, std::uint64_t dim, std::uint64_t index, cudaStream_t st) {
+    k_fill_basis<<<grid_for(dim, 256), 256, 0, st>>>(amps, dim, index);
+    check_launch("k_fill_basis");
+}
+
+void fill_random(double2* amps, std::uint64_t dim, std::uint64_t seed, cudaStream_t st) {
+    k_fill_random<<<grid_for(dim, 256), 256, 0, st>>>(amps, dim, seed);
+    check_launch("k_fill_random");
+}
+
+void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st) {
+    if (k < 1 || k > kTopK) raise(QCS_ERR_ARG, "top-k supports 1 <= k <= 16");
+    const int blocks = kSMs * 2;
+    ArgMax* part = nullptr;
+    QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(ArgMax) * blocks * k, st));
+    k_topk_partial<<<blocks, 256, 0, st>>>(amps, dim, k, part);
+    check_launch("k_topk_partial");
+    std::vector<ArgMax> h(std::size_t(blocks) * k);
+    QCS_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(ArgMax) * h.size(), cudaMemcpyDeviceToHost, st));
+    QCS_CUDA(cudaFreeAsync(part, st));
+    QCS_CUDA(cudaStreamSynchronize(st));
+    std::vector<ArgMax> c;
+    for (const ArgMax& x : h)
+        if (x.i != ~u64(0)) c.push_back(x);
+    std::sort(c.begin(), c.end(), [](const ArgMax& x, const ArgMax& y) { return x.p != y.p ? x.p > y.p : x.i < y.i; });
+    for (int j = 0; j < k; ++j) {
+        idx[j] = j < int(c.size()) ? c[j].i : ~u64(0);
+        p[j] = j < int(c.size()) ? c[j].p : 0.0;
+    }
+}
+
+std::size_t reduce_scratch_bytes() { return sizeof(ArgMax) * (kRedBlocks + 1) + 64; }
+
+}  // namespace qcs
