@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC",
           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "--expt-relaxed-constexpr"]
 
-SOURCES = ["gates.cpp", "ops.cpp", "engine.cpp", "abi.cpp", "timing.cpp",
+SOURCES = ["gates.cpp", "ops.cpp", "planner.cpp", "engine.cpp", "abi.cpp", "timing.cpp",
            "gate_kernels.cu", "tile_kernels.cu", "state_kernels.cu", "encode_kernels.cu"]
 
 

@@ -6,6 +6,7 @@
 // (circuit.cpp:41-62).  What changes is where the work happens: operators are never built;
 // each step becomes one or a few HBM passes over the device-resident state.
 #include "engine.hpp"
+#include "planner.hpp"
 
 #include <algorithm>
 #include <atomic>
@@ -51,14 +52,6 @@ void ensure_flip(qcs_state* s, std::size_t count) {
     const std::size_t cap = std::max<std::size_t>(count, 64);
     QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s->flip_buf), cap * sizeof(u64), s->stream));
     s->flip_cap = cap;
-}
-
-void ensure_ops(qcs_state* s, std::size_t count) {
-    if (count <= s->ops_cap) return;
-    if (s->ops_buf) QCS_CUDA(cudaFreeAsync(s->ops_buf, s->stream));
-    const std::size_t cap = std::max<std::size_t>(count, 16);
-    QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s->ops_buf), cap * sizeof(TileOp), s->stream));
-    s->ops_cap = cap;
 }
 
 }  // namespace
@@ -118,7 +111,7 @@ qcs_state::~qcs_state() {
     if (stream) cudaStreamSynchronize(stream);
     if (timer) qcs::destroy_timer(timer);
     if (flip_buf) cudaFree(flip_buf);
-    if (ops_buf) cudaFree(ops_buf);
+    if (plan_buf) cudaFree(plan_buf);
     if (scratch) cudaFree(scratch);
     for (auto& e : events)
         if (e) cudaEventDestroy(e);
@@ -206,55 +199,124 @@ void apply_diag(qcs_state* s, const u64* flipped, u64 count, int flip_rest) {
 
 namespace {
 
-// Walsh-Hadamard plan: tiles of m bits; every tile after the first keeps the low `low` bits
-// for coalescing and transforms up to m - low fresh bits.
-void plan_rh(int n, std::vector<TilePass>& passes, std::vector<TileOp>& ops) {
-    const int m = std::min(n, tile_max_bits());
-    const int low = std::min(3, m);
-    const double value = std::exp2(-0.5 * n);  // rh_build, rh.cpp:20
-    int next = 0;
-    while (next < n) {
-        TilePass p{};
-        p.op_begin = int(ops.size());
-        int nb = 0;
-        unsigned wmask = 0;
-        if (next == 0) {
-            for (int b = 0; b < m; ++b) p.bits[nb++] = b;
-            wmask = (1u << m) - 1;
-            next = m;
-            TileOp sc{};
-            sc.kind = TOP_SCALE;
-            sc.scale = value;  // rh.cpp:99-100: scale first
-            ops.push_back(sc);
-        } else {
-            const int cnt = std::min(m - low, n - next);
-            for (int b = 0; b < low; ++b) p.bits[nb++] = b;
-            for (int b = 0; b < cnt; ++b) {
-                wmask |= 1u << nb;
-                p.bits[nb++] = next + b;
-            }
-            next += cnt;
+void ensure_plan(qcs_state* s, std::size_t bytes) {
+    if (bytes <= s->plan_cap) return;
+    if (s->plan_buf) QCS_CUDA(cudaFreeAsync(s->plan_buf, s->stream));
+    const std::size_t cap = std::max<std::size_t>(bytes, 1 << 16);
+    QCS_CUDA(cudaMallocAsync(&s->plan_buf, cap, s->stream));
+    s->plan_cap = cap;
+}
+
+// A single operation outside a tile pass: gates and diagonal gates run the gate kernel (it
+// touches only the amplitudes they change), sign steps the diag-sign kernels.
+void run_single(qcs_state* s, const FOp& f, const u64* flips_dev, u64 flip_cnt) {
+    switch (f.kind) {
+        case TOP_GATE:
+        case TOP_DIAG: {
+            GateDesc d;
+            if (build_gate_desc(f.src, d)) launch_gate(s->amps, s->n, d, s->stream);
+            return;
         }
-        p.m = nb;
-        TileOp w{};
-        w.kind = TOP_WHT;
-        w.wht_mask = wmask;
-        ops.push_back(w);
-        p.op_count = int(ops.size()) - p.op_begin;
-        passes.push_back(p);
+        case TOP_WHT: {  // unnormalised butterfly [[1, 1], [1, -1]]: exact a + b, a - b
+            GateOp op;
+            op.k = 1;
+            op.pos[0] = f.tpos[0];
+            op.m = {1.0, 1.0, 1.0, -1.0};
+            GateDesc d;
+            build_gate_desc(op, d);
+            launch_gate(s->amps, s->n, d, s->stream);
+            return;
+        }
+        case TOP_SCALE:
+            scale(s->amps, u64(1) << s->n, f.scale, s->stream);
+            return;
+        case TOP_SIGN:
+            if (!f.flip_rest) launch_negate_listed(s->amps, flips_dev, flip_cnt, s->stream);
+            else launch_diag_sign(s->amps, s->n, flips_dev, flip_cnt, 1, s->stream);
+            return;
+        default: return;
     }
 }
 
-void run_passes(qcs_state* s, const std::vector<TilePass>& passes, const std::vector<TileOp>& ops,
-                const std::vector<u64>& flips) {
-    ensure_ops(s, ops.size());
-    QCS_CUDA(cudaMemcpyAsync(s->ops_buf, ops.data(), ops.size() * sizeof(TileOp), cudaMemcpyHostToDevice, s->stream));
-    if (!flips.empty()) {
-        ensure_flip(s, flips.size());
-        QCS_CUDA(cudaMemcpyAsync(s->flip_buf, flips.data(), flips.size() * sizeof(u64), cudaMemcpyHostToDevice,
-                                 s->stream));
+// Plan, lower, upload and launch a list of operations on the state.
+void run_fused(qcs_state* s, const std::vector<FOp>& ops) {
+    if (ops.empty()) return;
+    const int n = s->n;
+    const int max_bits = n >= 3 ? tile_max_bits() : n;
+    Plan plan;
+    if (n >= 3) {
+        plan = plan_ops(n, ops, max_bits);
+    } else {  // no tile: one operation per pass
+        for (std::size_t i = 0; i < ops.size(); ++i) plan.passes.push_back(PlannedPass{0, {int(i)}});
     }
-    for (const TilePass& p : passes) launch_tile_pass(s->amps, s->n, p, s->ops_buf, s->flip_buf, s->stream);
+    Lowered low;
+    if (n >= 3) {
+        lower_plan(n, ops, plan, low);
+    } else {
+        for (const FOp& f : ops) {
+            low.pass_ops.push_back({int(&f - ops.data())});
+            TileOp o{};
+            o.kind = f.kind;
+            o.flip_off = low.flips.size();
+            o.flip_cnt = f.flips.size();
+            low.flips.insert(low.flips.end(), f.flips.begin(), f.flips.end());
+            low.ops.push_back(o);
+            TileRound r{};
+            r.op_begin = int(low.ops.size()) - 1;
+            r.op_count = 1;
+            low.rounds.push_back(r);
+            TilePass p{};
+            p.round_begin = int(low.rounds.size()) - 1;
+            p.round_count = 1;
+            low.passes.push_back(p);
+        }
+    }
+    const std::size_t rb = low.rounds.size() * sizeof(TileRound);
+    const std::size_t ob = low.ops.size() * sizeof(TileOp);
+    const std::size_t fb = low.flips.size() * sizeof(u64);
+    const std::size_t o_off = (rb + 255) & ~std::size_t(255), f_off = (o_off + ob + 255) & ~std::size_t(255);
+    ensure_plan(s, f_off + fb + 8);
+    auto* base = static_cast<unsigned char*>(s->plan_buf);
+    std::vector<unsigned char> host(f_off + fb);
+    if (rb) std::memcpy(host.data(), low.rounds.data(), rb);
+    if (ob) std::memcpy(host.data() + o_off, low.ops.data(), ob);
+    if (fb) std::memcpy(host.data() + f_off, low.flips.data(), fb);
+    QCS_CUDA(cudaMemcpyAsync(base, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
+    const auto* rounds_dev = reinterpret_cast<const TileRound*>(base);
+    const auto* ops_dev = reinterpret_cast<const TileOp*>(base + o_off);
+    const auto* flips_dev = reinterpret_cast<const u64*>(base + f_off);
+    for (std::size_t i = 0; i < low.passes.size(); ++i) {
+        const auto& po = low.pass_ops[i];
+        if (po.size() == 1) {
+            const TileOp& o = low.ops[std::size_t(low.rounds[std::size_t(low.passes[i].round_begin)].op_begin)];
+            run_single(s, ops[std::size_t(po[0])], flips_dev + o.flip_off, o.flip_cnt);
+        } else {
+            launch_tile_pass(s->amps, n, low.passes[i], rounds_dev, ops_dev, flips_dev, s->stream);
+        }
+    }
+    // pageable cudaMemcpyAsync staged `host` before returning; it may be freed now
+}
+
+std::vector<FOp> rh_ops(int n) {
+    std::vector<FOp> ops;
+    ops.push_back(make_scale(std::exp2(-0.5 * n)));  // rh_build (rh.cpp:20), scale first (rh.cpp:99-100)
+    for (int b = 0; b < n; ++b) ops.push_back(make_wht(b));
+    return ops;
+}
+
+void append_step_ops(int n, const qcs_step& st, bool rh, std::vector<FOp>& ops) {
+    if (rh) {
+        auto r = rh_ops(n);
+        ops.insert(ops.end(), r.begin(), r.end());
+    } else if (st.kind == QCS_STEP_DIAG) {
+        const bool any = st.flip_rest || st.num_flipped;
+        if (any) ops.push_back(make_sign(n, std::vector<u64>(st.flipped, st.flipped + st.num_flipped), st.flip_rest));
+    } else {
+        for (int j = 0; j < st.num_placements; ++j) {
+            FOp f;
+            if (make_fop(canonical_op(n, st.placements[j]), f)) ops.push_back(std::move(f));
+        }
+    }
 }
 
 }  // namespace
@@ -262,10 +324,7 @@ void run_passes(qcs_state* s, const std::vector<TilePass>& passes, const std::ve
 void apply_rh(qcs_state* s) {
     DeviceGuard g(s->device);
     TimerScope ts(s);
-    std::vector<TilePass> passes;
-    std::vector<TileOp> ops;
-    plan_rh(s->n, passes, ops);
-    run_passes(s, passes, ops, {});
+    run_fused(s, rh_ops(s->n));
 }
 
 // ------------------------------------------------------------------ simulate
@@ -358,19 +417,23 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
     qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1};
     if (opts) o = *opts;
     const u64 dim = u64(1) << n;
+    DeviceGuard g(s->device);
+    TimerScope ts(s);
+    std::vector<FOp> ops;  // fused mode: the whole circuit; stepwise: one step at a time
     for (int i = 0; i < nsteps; ++i) {
         const qcs_step& st = steps[i];
         qcs_step_report r{};
         r.stage = st.stage;
         r.dense_bytes = dense_step_bytes(n);
         const bool use_rh = engine == QCS_ENGINE_RH_DAX && is_hadamard_all(st, n);
+        if (!o.fuse) ops.clear();
+        append_step_ops(n, st, use_rh, ops);
         if (use_rh) {
             r.structure = QCS_STRUCT_RH;
             r.matrix_bytes = 16;  // engine.cpp:173
             r.sign_count = rh_sign_count(n, o.sign_method, o.block_size);
             const u64 half = u64(1) << (n - 1);
             r.madd_count = 4 * half * half;  // rh.cpp:153
-            apply_rh(s);
         } else {
             const u64 nnz = step_nnz(st, n);
             if (engine == QCS_ENGINE_DENSE) {
@@ -390,11 +453,11 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
                 r.matrix_bytes = 24 * nnz;  // dax.cpp:105, das.cpp:152
                 r.madd_count = nnz;         // engine.cpp:191, :199
             }
-            if (st.kind == QCS_STEP_DIAG) apply_diag(s, st.flipped, st.num_flipped, st.flip_rest);
-            else apply_step(s, st.placements, st.num_placements);
         }
+        if (!o.fuse) run_fused(s, ops);  // one step: fused only within the step
         if (reports) reports[i] = r;
     }
+    if (o.fuse) run_fused(s, ops);
 }
 
 void memory_report(int n, const qcs_step* steps, int nsteps, int engine, qcs_step_report* reports) {

@@ -19,8 +19,8 @@ struct qcs_state {
     void* scratch = nullptr;              // reduction scratch (device)
     std::uint64_t* flip_buf = nullptr;    // device copy of diag index lists
     std::size_t flip_cap = 0;
-    qcs::TileOp* ops_buf = nullptr;       // device op list of the current plan
-    std::size_t ops_cap = 0;
+    void* plan_buf = nullptr;             // device copy of the current plan (rounds, ops, flips)
+    std::size_t plan_cap = 0;
     cudaEvent_t events[8] = {};
     qcs::LaunchTimer* timer = nullptr;   // per-launch timing (qcs_timing_enable)
     ~qcs_state();

@@ -41,48 +41,54 @@ void launch_negate_listed(double2* amps, const std::uint64_t* idx_dev, std::uint
                           cudaStream_t st);
 
 // ---------------------------------------------------------------- fused shared-memory passes
-// A pass loads the 2^m amplitudes whose basis indices differ only in the tile bits, applies a
-// list of tile operations in shared memory / registers, and writes them back: one HBM round
-// trip for many gates.
+// A pass loads the 2^m amplitudes whose basis indices differ only in the tile bits, runs
+// rounds of operations on register-held groups of 8 amplitudes, and writes the tile back:
+// one HBM round trip for many gates (tile_kernels.cu).
 enum TileOpKind : std::int32_t {
-    TOP_GATE = 0,    // dense/monomial k<=3 gate on local bits (GateDesc-like tables)
-    TOP_DIAG = 1,    // diagonal phase on up to 3 bits anywhere in the basis index
+    TOP_GATE = 0,    // gate on <= 3 targets among the round bits (row tables as GateDesc)
+    TOP_DIAG = 1,    // diagonal phase on up to 3 basis bits anywhere
     TOP_SIGN = 2,    // diag sign step: flipped list (global memory) XOR flip_rest
-    TOP_WHT = 3,     // unnormalised butterflies (a+b, a-b) over a mask of local bits
+    TOP_WHT = 3,     // unnormalised butterflies (a+b, a-b) over round bits (wht_mask)
     TOP_SCALE = 4,   // multiply by a real scalar (the RH magnitude, rh.cpp:99-100)
 };
 
 struct TileOp {
     std::int32_t kind;
-    std::int32_t k;              // gate bits (TOP_GATE/TOP_DIAG)
-    std::int32_t nfree, nrows;   // TOP_GATE
-    std::int32_t lbit[3];        // TOP_GATE: local tile bit of each gate position, ascending
-    std::uint32_t lfixed_val;    // TOP_GATE: fixed gate bits (local mask form)
-    std::uint32_t lfree_bit[3];  // TOP_GATE: local masks of the free bits
-    std::uint32_t load_mask;
-    std::uint64_t gctrl_mask;    // controls outside the tile: required global bits
+    std::int32_t gcase;          // TOP_GATE: register round: target register bit (K = 1);
+                                 //           shared-memory round: K (2 or 3)
+    std::int32_t tl[3];          // TOP_GATE shared-memory round: target local bits, most significant first
+    std::int32_t nrows;          // TOP_GATE: touched rows
+    std::uint32_t lctrl_mask;    // controls on tile bits (local index mask / required value)
+    std::uint32_t lctrl_val;
+    std::uint32_t wht_mask;      // TOP_WHT: register bits 0..2 to transform
+    std::uint64_t gctrl_mask;    // controls outside the tile: required basis bits
     std::uint64_t gctrl_val;
-    std::uint32_t wht_mask;      // TOP_WHT: local bits to transform
-    std::int32_t dpos[3];        // TOP_DIAG: basis-bit positions (descending significance)
-    std::uint64_t flip_off;      // TOP_SIGN: offset into the pass's flipped array
+    std::int32_t dk;             // TOP_DIAG: number of phase bits
+    std::int32_t dpos[3];        // TOP_DIAG: basis-bit positions, most significant first
+    std::uint64_t flip_off;      // TOP_SIGN: offset into the plan's flipped array
     std::uint64_t flip_cnt;
     std::int32_t flip_rest;
     double scale;                // TOP_SCALE
-    std::uint8_t row_member[8];
+    std::uint8_t row_member[8];  // TOP_GATE: member index (gate-local) of each touched row
     std::uint8_t nnz[8];
     std::uint8_t col_member[8][8];
     double2 val[8][8];           // TOP_GATE rows / TOP_DIAG: val[0][g] = diagonal entry g
-    std::uint8_t dskip[8];       // TOP_DIAG: entry g is exactly 1 (untouched)
+    std::uint8_t dskip[8];       // TOP_DIAG: entry g is exactly 1 (left untouched)
+};
+
+struct TileRound {
+    int smem;                 // 1: ops run straight on shared memory (gates on 2-3 targets)
+    int rbits[3];             // local tile bits held in registers (ascending)
+    int op_begin, op_count;   // range in the plan's op array
 };
 
 struct TilePass {
-    int m;                    // tile bits
-    int bits[16];             // tile bit positions (ascending); local bit j <-> bits[j]
-    int op_begin, op_count;   // range in the op array
+    int m;                    // tile bits (3..12)
+    int bits[16];             // basis-bit positions, ascending; bits[0..2] = 0, 1, 2
+    int round_begin, round_count;
 };
 
-// ops_dev / flipped_dev: device arrays shared by all passes of a plan.
-void launch_tile_pass(double2* amps, int n, const TilePass& p, const TileOp* ops_dev,
+void launch_tile_pass(double2* amps, int n, const TilePass& p, const TileRound* rounds_dev, const TileOp* ops_dev,
                       const std::uint64_t* flipped_dev, cudaStream_t st);
 int tile_max_bits();
 

@@ -1,0 +1,326 @@
+// planner.cpp -- fusion planner: circuit operations -> HBM passes -> register rounds.
+//
+// The reference applies every step as its own full operator-vector product (engine.cpp:162-205).
+// On the GPU the cost of a step is one HBM round trip of the state, so consecutive operations
+// are grouped into passes whose target bits fit one shared-memory tile (tile_kernels.cu).
+// Operations may move earlier past unscheduled ones only when they commute: disjoint bit
+// supports, or both diagonal.  A pass keeps basis bits 0..2 in its tile for coalescing.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "engine.hpp"
+#include "planner.hpp"
+
+namespace qcs {
+
+namespace {
+inline bool is_zero(const cplx& v) { return v.real() == 0.0 && v.imag() == 0.0; }
+inline bool is_one(const cplx& v) { return v.real() == 1.0 && v.imag() == 0.0; }
+}  // namespace
+
+// One canonical placement -> one fused operation (nullopt-like: returns false for identity).
+bool make_fop(const GateOp& op, FOp& f) {
+    const int k = op.k, dim = 1 << k;
+    f = FOp{};
+    f.src = op;
+    bool any = false, diag = true;
+    for (int g = 0; g < dim; ++g)
+        for (int c = 0; c < dim; ++c) {
+            const cplx v = op.m[std::size_t(g) * dim + c];
+            if (is_zero(v)) continue;
+            if (c != g) diag = false;
+            if (!(c == g && is_one(v))) any = true;
+        }
+    if (!any) return false;
+    for (int i = 0; i < k; ++i) f.touch |= u64(1) << op.pos[i];
+    if (diag) {
+        f.kind = TOP_DIAG;
+        f.diagonal = true;
+        f.dk = k;
+        for (int i = 0; i < k; ++i) f.dpos[i] = op.pos[i];
+        for (int g = 0; g < dim; ++g) {
+            const cplx v = op.m[std::size_t(g) * dim + g];
+            f.dval[g] = make_double2(v.real(), v.imag());
+            f.dskip[g] = is_one(v);
+        }
+        return true;
+    }
+    // peel controls: local bit b is a control (on 1) when every row with b = 0 is an identity
+    // row and no row with b = 1 reads a column with b = 0
+    std::vector<int> bits;  // remaining local bits (of the canonical k-bit index), ascending
+    for (int b = 0; b < k; ++b) bits.push_back(b);
+    int cmask = 0;
+    for (int b = 0; b < k; ++b) {
+        bool ctrl = true;
+        for (int g = 0; g < dim && ctrl; ++g) {
+            if ((cmask & g) != cmask) continue;  // rows already excluded by earlier controls
+            for (int c = 0; c < dim; ++c) {
+                const cplx v = op.m[std::size_t(g) * dim + c];
+                if (is_zero(v)) continue;
+                if (!(g >> b & 1)) {
+                    if (!(c == g && is_one(v))) { ctrl = false; break; }
+                } else if (!(c >> b & 1)) { ctrl = false; break; }
+            }
+        }
+        if (ctrl && int(bits.size()) > 1) {
+            cmask |= 1 << b;
+            bits.erase(std::find(bits.begin(), bits.end(), b));
+        }
+    }
+    const int K = int(bits.size());
+    // targets, most significant first; local bit b <-> canonical slot k-1-b <-> op.pos[k-1-b]
+    f.kind = TOP_GATE;
+    f.K = K;
+    for (int i = 0; i < K; ++i) f.tpos[i] = op.pos[k - 1 - bits[K - 1 - i]];
+    for (int b = 0; b < k; ++b)
+        if (cmask >> b & 1) {
+            f.ctrl_mask |= u64(1) << op.pos[k - 1 - b];
+            f.ctrl_val |= u64(1) << op.pos[k - 1 - b];
+        }
+    auto full = [&](int mm) {  // K-bit member -> canonical k-bit index with controls set
+        int g = cmask;
+        for (int i = 0; i < K; ++i)
+            if (mm >> (K - 1 - i) & 1) g |= 1 << bits[K - 1 - i];
+        return g;
+    };
+    f.nrows = 0;
+    for (int r = 0; r < (1 << K); ++r) {
+        const int g = full(r);
+        int nz = 0, only = -1;
+        for (int c = 0; c < dim; ++c)
+            if (!is_zero(op.m[std::size_t(g) * dim + c])) { ++nz; only = c; }
+        if (nz == 1 && only == g && is_one(op.m[std::size_t(g) * dim + g])) continue;  // identity row
+        const int row = f.nrows++;
+        f.row_member[row] = std::uint8_t(r);
+        int z = 0;
+        for (int mm = 0; mm < (1 << K); ++mm) {  // ascending member == ascending global column
+            const cplx v = op.m[std::size_t(g) * dim + full(mm)];
+            if (is_zero(v)) continue;
+            f.col_member[row][z] = std::uint8_t(mm);
+            f.val[row][z] = make_double2(v.real(), v.imag());
+            ++z;
+        }
+        f.nnz[row] = std::uint8_t(z);
+    }
+    return true;
+}
+
+FOp make_sign(int n, std::vector<u64> flips, bool rest) {
+    FOp f{};
+    f.kind = TOP_SIGN;
+    f.diagonal = true;
+    f.touch = n >= 64 ? ~u64(0) : (u64(1) << n) - 1;
+    std::sort(flips.begin(), flips.end());
+    flips.erase(std::unique(flips.begin(), flips.end()), flips.end());
+    f.flips = std::move(flips);
+    f.flip_rest = rest;
+    return f;
+}
+
+FOp make_scale(double s) {
+    FOp f{};
+    f.kind = TOP_SCALE;
+    f.diagonal = true;
+    f.scale = s;
+    return f;
+}
+
+FOp make_wht(int bit) {
+    FOp f{};
+    f.kind = TOP_WHT;
+    f.K = 1;
+    f.tpos[0] = bit;
+    f.touch = u64(1) << bit;
+    return f;
+}
+
+namespace {
+
+bool elementwise(const FOp& f) { return f.kind == TOP_DIAG || f.kind == TOP_SIGN || f.kind == TOP_SCALE; }
+
+}  // namespace
+
+Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
+    Plan plan;
+    const int M = std::min(max_bits, n);
+    std::vector<int> remaining(ops.size());
+    for (std::size_t i = 0; i < ops.size(); ++i) remaining[i] = int(i);
+    while (!remaining.empty()) {
+        u64 S = 0;
+        for (int b = 0; b < std::min(3, n); ++b) S |= u64(1) << b;
+        int used = __builtin_popcountll(S);
+        std::vector<int> chosen, skipped;
+        u64 nd_block = 0, d_block = 0;  // supports of skipped non-diagonal / diagonal ops
+        for (int idx : remaining) {
+            const FOp& f = ops[std::size_t(idx)];
+            const bool conflict = (f.touch & nd_block) || (!f.diagonal && (f.touch & d_block));
+            bool take = false;
+            if (!conflict) {
+                if (elementwise(f)) {
+                    take = true;
+                } else {
+                    u64 need = 0;
+                    for (int i = 0; i < f.K; ++i) need |= u64(1) << f.tpos[i];
+                    need &= ~S;
+                    const int add = __builtin_popcountll(need);
+                    if (used + add <= M) {
+                        S |= need;
+                        used += add;
+                        take = true;
+                    }
+                }
+            }
+            if (take) {
+                chosen.push_back(idx);
+            } else {
+                skipped.push_back(idx);
+                (f.diagonal ? d_block : nd_block) |= f.touch;
+            }
+        }
+        // pad the tile to M bits with the lowest unused positions (bigger tiles, same cost)
+        for (int b = 0; b < n && used < M; ++b)
+            if (!(S >> b & 1)) {
+                S |= u64(1) << b;
+                ++used;
+            }
+        plan.passes.push_back(PlannedPass{S, chosen});
+        remaining.swap(skipped);
+    }
+    return plan;
+}
+
+// Lower planned passes to kernel descriptors (TilePass / TileRound / TileOp arrays).
+void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& out) {
+    out = Lowered{};
+    for (const PlannedPass& pp : plan.passes) {
+        TilePass tp{};
+        int loc[64];
+        std::fill(loc, loc + 64, -1);
+        for (int b = 0; b < n; ++b)
+            if (pp.tile >> b & 1) {
+                loc[b] = tp.m;
+                tp.bits[tp.m++] = b;
+            }
+        tp.round_begin = int(out.rounds.size());
+        // group the pass's ops into rounds of <= 3 register bits; gates on 2-3 targets get
+        // shared-memory rounds of their own
+        struct RoundPlan {
+            bool smem;
+            unsigned mask;
+            std::vector<int> ops;
+        };
+        std::vector<RoundPlan> rounds;
+        for (int idx : pp.ops) {
+            const FOp& f = ops[std::size_t(idx)];
+            const bool smem = f.kind == TOP_GATE && f.K >= 2;
+            unsigned t = 0;
+            if (!elementwise(f))
+                for (int i = 0; i < f.K; ++i) t |= 1u << loc[f.tpos[i]];
+            if (smem) {
+                if (!rounds.empty() && rounds.back().smem) rounds.back().ops.push_back(idx);
+                else rounds.push_back({true, 0u, {idx}});
+                continue;
+            }
+            if (rounds.empty() || rounds.back().smem) {
+                rounds.push_back({false, t, {idx}});
+                continue;
+            }
+            auto& cur = rounds.back();
+            if ((t & ~cur.mask) == 0) {
+                cur.ops.push_back(idx);
+            } else if (__builtin_popcount(cur.mask | t) <= 3) {
+                cur.mask |= t;
+                cur.ops.push_back(idx);
+            } else {
+                rounds.push_back({false, t, {idx}});
+            }
+        }
+        for (auto& r : rounds) {
+            unsigned mask = r.mask;
+            for (int b = 0; b < tp.m && __builtin_popcount(mask) < 3; ++b) mask |= 1u << b;
+            TileRound tr{};
+            tr.smem = r.smem ? 1 : 0;
+            int c = 0;
+            for (int b = 0; b < tp.m; ++b)
+                if (mask >> b & 1) tr.rbits[c++] = b;
+            auto reg = [&](int pos) {
+                const int l = loc[pos];
+                for (int i = 0; i < 3; ++i)
+                    if (tr.rbits[i] == l) return i;
+                return -1;
+            };
+            tr.op_begin = int(out.ops.size());
+            for (int idx : r.ops) {
+                const FOp& f = ops[std::size_t(idx)];
+                TileOp o{};
+                o.kind = f.kind;
+                // controls: inside the tile -> per element group; outside -> per tile
+                for (int b = 0; b < n; ++b) {
+                    if (!(f.ctrl_mask >> b & 1)) continue;
+                    const bool want = f.ctrl_val >> b & 1;
+                    if (loc[b] >= 0) {
+                        o.lctrl_mask |= 1u << loc[b];
+                        if (want) o.lctrl_val |= 1u << loc[b];
+                    } else {
+                        o.gctrl_mask |= u64(1) << b;
+                        if (want) o.gctrl_val |= u64(1) << b;
+                    }
+                }
+                switch (f.kind) {
+                    case TOP_GATE: {
+                        if (tr.smem) {
+                            o.gcase = f.K;
+                            for (int i = 0; i < f.K; ++i) o.tl[i] = loc[f.tpos[i]];
+                        } else {
+                            o.gcase = reg(f.tpos[0]);  // K = 1: the target's register bit
+                        }
+                        o.nrows = f.nrows;
+                        std::memcpy(o.row_member, f.row_member, sizeof(o.row_member));
+                        std::memcpy(o.nnz, f.nnz, sizeof(o.nnz));
+                        std::memcpy(o.col_member, f.col_member, sizeof(o.col_member));
+                        std::memcpy(o.val, f.val, sizeof(o.val));
+                        break;
+                    }
+                    case TOP_WHT: {
+                        // merge a run of single-bit butterflies into one masked op
+                        const unsigned bit = 1u << reg(f.tpos[0]);
+                        if (!out.ops.empty() && int(out.ops.size()) > tr.op_begin && out.ops.back().kind == TOP_WHT &&
+                            !(out.ops.back().wht_mask & bit)) {
+                            out.ops.back().wht_mask |= bit;
+                            continue;
+                        }
+                        o.wht_mask = bit;
+                        break;
+                    }
+                    case TOP_DIAG:
+                        o.dk = f.dk;
+                        for (int i = 0; i < f.dk; ++i) o.dpos[i] = f.dpos[i];
+                        for (int g = 0; g < 8; ++g) {
+                            o.val[0][g] = f.dval[g];
+                            o.dskip[g] = f.dskip[g];
+                        }
+                        break;
+                    case TOP_SIGN:
+                        o.flip_off = out.flips.size();
+                        o.flip_cnt = f.flips.size();
+                        o.flip_rest = f.flip_rest;
+                        out.flips.insert(out.flips.end(), f.flips.begin(), f.flips.end());
+                        break;
+                    case TOP_SCALE:
+                        o.scale = f.scale;
+                        break;
+                    default: break;
+                }
+                out.ops.push_back(o);
+            }
+            tr.op_count = int(out.ops.size()) - tr.op_begin;
+            out.rounds.push_back(tr);
+        }
+        tp.round_count = int(out.rounds.size()) - tp.round_begin;
+        out.passes.push_back(tp);
+        out.pass_ops.push_back(pp.ops);
+    }
+}
+
+}  // namespace qcs
