@@ -242,59 +242,37 @@ void run_single(qcs_state* s, const FOp& f, const u64* flips_dev, u64 flip_cnt) 
 void run_fused(qcs_state* s, const std::vector<FOp>& ops) {
     if (ops.empty()) return;
     const int n = s->n;
-    const int max_bits = n >= 3 ? tile_max_bits() : n;
-    Plan plan;
-    if (n >= 3) {
-        plan = plan_ops(n, ops, max_bits);
-    } else {  // no tile: one operation per pass
-        for (std::size_t i = 0; i < ops.size(); ++i) plan.passes.push_back(PlannedPass{0, {int(i)}});
-    }
     Lowered low;
     if (n >= 3) {
-        lower_plan(n, ops, plan, low);
-    } else {
-        for (const FOp& f : ops) {
-            low.pass_ops.push_back({int(&f - ops.data())});
-            TileOp o{};
-            o.kind = f.kind;
-            o.flip_off = low.flips.size();
-            o.flip_cnt = f.flips.size();
-            low.flips.insert(low.flips.end(), f.flips.begin(), f.flips.end());
-            low.ops.push_back(o);
-            TileRound r{};
-            r.op_begin = int(low.ops.size()) - 1;
-            r.op_count = 1;
-            low.rounds.push_back(r);
-            TilePass p{};
-            p.round_begin = int(low.rounds.size()) - 1;
-            p.round_count = 1;
-            low.passes.push_back(p);
+        lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
+    } else {  // no 3-bit tile: one operation per pass
+        for (std::size_t i = 0; i < ops.size(); ++i) {
+            low.pass_ops.push_back({int(i)});
+            low.single_flip_off.push_back(low.flips.size());
+            low.single_flip_cnt.push_back(ops[i].flips.size());
+            low.flips.insert(low.flips.end(), ops[i].flips.begin(), ops[i].flips.end());
+            low.passes.emplace_back();
         }
     }
-    const std::size_t rb = low.rounds.size() * sizeof(TileRound);
-    const std::size_t ob = low.ops.size() * sizeof(TileOp);
+    const std::size_t bb = low.big.size() * sizeof(TileOp);
     const std::size_t fb = low.flips.size() * sizeof(u64);
-    const std::size_t o_off = (rb + 255) & ~std::size_t(255), f_off = (o_off + ob + 255) & ~std::size_t(255);
-    ensure_plan(s, f_off + fb + 8);
+    const std::size_t f_off = (bb + 255) & ~std::size_t(255);
+    if (bb + fb) {
+        ensure_plan(s, f_off + fb + 8);
+        std::vector<unsigned char> host(f_off + fb);
+        if (bb) std::memcpy(host.data(), low.big.data(), bb);
+        if (fb) std::memcpy(host.data() + f_off, low.flips.data(), fb);
+        // pageable copy: staged before the call returns, so `host` may go out of scope
+        QCS_CUDA(cudaMemcpyAsync(s->plan_buf, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
+    }
     auto* base = static_cast<unsigned char*>(s->plan_buf);
-    std::vector<unsigned char> host(f_off + fb);
-    if (rb) std::memcpy(host.data(), low.rounds.data(), rb);
-    if (ob) std::memcpy(host.data() + o_off, low.ops.data(), ob);
-    if (fb) std::memcpy(host.data() + f_off, low.flips.data(), fb);
-    QCS_CUDA(cudaMemcpyAsync(base, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
-    const auto* rounds_dev = reinterpret_cast<const TileRound*>(base);
-    const auto* ops_dev = reinterpret_cast<const TileOp*>(base + o_off);
+    const auto* big_dev = reinterpret_cast<const TileOp*>(base);
     const auto* flips_dev = reinterpret_cast<const u64*>(base + f_off);
     for (std::size_t i = 0; i < low.passes.size(); ++i) {
         const auto& po = low.pass_ops[i];
-        if (po.size() == 1) {
-            const TileOp& o = low.ops[std::size_t(low.rounds[std::size_t(low.passes[i].round_begin)].op_begin)];
-            run_single(s, ops[std::size_t(po[0])], flips_dev + o.flip_off, o.flip_cnt);
-        } else {
-            launch_tile_pass(s->amps, n, low.passes[i], rounds_dev, ops_dev, flips_dev, s->stream);
-        }
+        if (po.size() == 1) run_single(s, ops[std::size_t(po[0])], flips_dev + low.single_flip_off[i], low.single_flip_cnt[i]);
+        else launch_tile_pass(s->amps, n, low.passes[i], big_dev, flips_dev, s->stream);
     }
-    // pageable cudaMemcpyAsync staged `host` before returning; it may be freed now
 }
 
 std::vector<FOp> rh_ops(int n) {

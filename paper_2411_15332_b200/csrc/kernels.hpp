@@ -76,19 +76,42 @@ struct TileOp {
     std::uint8_t dskip[8];       // TOP_DIAG: entry g is exactly 1 (left untouched)
 };
 
-struct TileRound {
-    int smem;                 // 1: ops run straight on shared memory (gates on 2-3 targets)
-    int rbits[3];             // local tile bits held in registers (ascending)
-    int op_begin, op_count;   // range in the plan's op array
+// Compact register-round operation; a pass's list travels in the kernel parameter space.
+struct RegOp {
+    std::uint8_t kind;        // TOP_GATE (one target), TOP_DIAG, TOP_SIGN, TOP_WHT, TOP_SCALE
+    std::uint8_t t;           // TOP_GATE: target register bit; TOP_WHT: register-bit mask
+    std::uint8_t rk0, rk1;    // TOP_GATE: row kind (0 untouched, 1 one product, 2 two products)
+    std::uint8_t rc0, rc1;    // TOP_GATE: column of a single-product row
+    std::uint8_t dk;          // TOP_DIAG: phase bits (<= 3)
+    std::uint8_t dskip;       // TOP_DIAG: bit g set = entry g is exactly 1 (untouched)
+    std::uint8_t dreg[3];     // TOP_DIAG: register bit of phase bit i, 0xff = constant over a group
+    std::uint8_t dpos[3];     // TOP_DIAG: basis-bit position of phase bit i (most significant first)
+    std::uint16_t ref;        // TOP_SIGN / shared-memory gates / 3-bit diagonals: index into the plan's TileOp array
+    std::uint32_t lctrl_mask; // controls on tile bits (local-index mask / required value)
+    std::uint32_t lctrl_val;
+    std::uint32_t pad0;
+    std::uint64_t gctrl_mask; // controls outside the tile (basis bits / required value)
+    std::uint64_t gctrl_val;
+    std::uint64_t pad1;
+    double2 c[4];             // TOP_GATE: a0, b0, a1, b1; TOP_DIAG: entries; TOP_SCALE: c[0].x
 };
 
-struct TilePass {
+struct RoundDesc {
+    std::uint8_t smem;        // 1: gates on 2-3 targets, run straight on shared memory
+    std::uint8_t r[3];        // local tile bits held in registers (ascending)
+    std::uint16_t op_begin, op_count;
+};
+
+constexpr int kPassMaxOps = 236;
+struct PassParams {           // <= 32 KB: the kernel parameter limit
     int m;                    // tile bits (3..12)
+    int nrounds;
     int bits[16];             // basis-bit positions, ascending; bits[0..2] = 0, 1, 2
-    int round_begin, round_count;
+    RoundDesc rounds[kPassMaxOps];
+    RegOp ops[kPassMaxOps];
 };
 
-void launch_tile_pass(double2* amps, int n, const TilePass& p, const TileRound* rounds_dev, const TileOp* ops_dev,
+void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* big_dev,
                       const std::uint64_t* flipped_dev, cudaStream_t st);
 int tile_max_bits();
 

@@ -171,6 +171,7 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
                     }
                 }
             }
+            if (take && int(chosen.size()) >= kPassMaxOps - 4) take = false;
             if (take) {
                 chosen.push_back(idx);
             } else {
@@ -190,21 +191,20 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
     return plan;
 }
 
-// Lower planned passes to kernel descriptors (TilePass / TileRound / TileOp arrays).
+// Lower planned passes to kernel descriptors: one PassParams (constant-bank operation list) per
+// pass, plus the plan-wide TileOp array (shared-memory gates, sign steps, 3-bit diagonals).
 void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& out) {
     out = Lowered{};
     for (const PlannedPass& pp : plan.passes) {
-        TilePass tp{};
+        PassParams P{};
         int loc[64];
         std::fill(loc, loc + 64, -1);
         for (int b = 0; b < n; ++b)
             if (pp.tile >> b & 1) {
-                loc[b] = tp.m;
-                tp.bits[tp.m++] = b;
+                loc[b] = P.m;
+                P.bits[P.m++] = b;
             }
-        tp.round_begin = int(out.rounds.size());
-        // group the pass's ops into rounds of <= 3 register bits; gates on 2-3 targets get
-        // shared-memory rounds of their own
+        // rounds of <= 3 register bits; gates on 2-3 targets get shared-memory rounds
         struct RoundPlan {
             bool smem;
             unsigned mask;
@@ -236,27 +236,30 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                 rounds.push_back({false, t, {idx}});
             }
         }
+        int nops = 0;
+        std::uint64_t flip_off = 0, flip_cnt = 0;
         for (auto& r : rounds) {
+            if (P.nrounds >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many rounds in a pass");
             unsigned mask = r.mask;
-            for (int b = 0; b < tp.m && __builtin_popcount(mask) < 3; ++b) mask |= 1u << b;
-            TileRound tr{};
-            tr.smem = r.smem ? 1 : 0;
+            for (int b = 0; b < P.m && __builtin_popcount(mask) < 3; ++b) mask |= 1u << b;
+            RoundDesc& rd = P.rounds[P.nrounds++];
+            rd.smem = r.smem ? 1 : 0;
             int c = 0;
-            for (int b = 0; b < tp.m; ++b)
-                if (mask >> b & 1) tr.rbits[c++] = b;
-            auto reg = [&](int pos) {
+            for (int b = 0; b < P.m; ++b)
+                if (mask >> b & 1) rd.r[c++] = std::uint8_t(b);
+            auto reg = [&](int pos) -> int {
                 const int l = loc[pos];
                 for (int i = 0; i < 3; ++i)
-                    if (tr.rbits[i] == l) return i;
+                    if (rd.r[i] == l) return i;
                 return -1;
             };
-            tr.op_begin = int(out.ops.size());
+            rd.op_begin = std::uint16_t(nops);
             for (int idx : r.ops) {
                 const FOp& f = ops[std::size_t(idx)];
-                TileOp o{};
-                o.kind = f.kind;
-                // controls: inside the tile -> per element group; outside -> per tile
-                for (int b = 0; b < n; ++b) {
+                if (nops >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many operations in a pass");
+                RegOp o{};
+                o.kind = std::uint8_t(f.kind);
+                for (int b = 0; b < n; ++b) {  // controls: in the tile per group, outside per tile
                     if (!(f.ctrl_mask >> b & 1)) continue;
                     const bool want = f.ctrl_val >> b & 1;
                     if (loc[b] >= 0) {
@@ -267,59 +270,92 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                         if (want) o.gctrl_val |= u64(1) << b;
                     }
                 }
+                TileOp big{};
+                bool use_big = false;
                 switch (f.kind) {
-                    case TOP_GATE: {
-                        if (tr.smem) {
-                            o.gcase = f.K;
-                            for (int i = 0; i < f.K; ++i) o.tl[i] = loc[f.tpos[i]];
+                    case TOP_GATE:
+                        if (rd.smem) {
+                            big.gcase = f.K;
+                            for (int i = 0; i < f.K; ++i) big.tl[i] = loc[f.tpos[i]];
+                            big.nrows = f.nrows;
+                            big.lctrl_mask = o.lctrl_mask;
+                            big.lctrl_val = o.lctrl_val;
+                            big.gctrl_mask = o.gctrl_mask;
+                            big.gctrl_val = o.gctrl_val;
+                            std::memcpy(big.row_member, f.row_member, sizeof(big.row_member));
+                            std::memcpy(big.nnz, f.nnz, sizeof(big.nnz));
+                            std::memcpy(big.col_member, f.col_member, sizeof(big.col_member));
+                            std::memcpy(big.val, f.val, sizeof(big.val));
+                            use_big = true;
                         } else {
-                            o.gcase = reg(f.tpos[0]);  // K = 1: the target's register bit
+                            o.t = std::uint8_t(reg(f.tpos[0]));
+                            for (int row = 0; row < f.nrows; ++row) {
+                                const double2 a = f.val[row][0];
+                                const double2 b2 = f.nnz[row] > 1 ? f.val[row][1] : make_double2(0.0, 0.0);
+                                if (f.row_member[row] == 0) {
+                                    o.rk0 = f.nnz[row];
+                                    o.rc0 = f.col_member[row][0];
+                                    o.c[0] = a;
+                                    o.c[1] = b2;
+                                } else {
+                                    o.rk1 = f.nnz[row];
+                                    o.rc1 = f.col_member[row][0];
+                                    o.c[2] = a;
+                                    o.c[3] = b2;
+                                }
+                            }
                         }
-                        o.nrows = f.nrows;
-                        std::memcpy(o.row_member, f.row_member, sizeof(o.row_member));
-                        std::memcpy(o.nnz, f.nnz, sizeof(o.nnz));
-                        std::memcpy(o.col_member, f.col_member, sizeof(o.col_member));
-                        std::memcpy(o.val, f.val, sizeof(o.val));
                         break;
-                    }
-                    case TOP_WHT: {
-                        // merge a run of single-bit butterflies into one masked op
+                    case TOP_WHT: {  // a run of single-bit butterflies becomes one masked op
                         const unsigned bit = 1u << reg(f.tpos[0]);
-                        if (!out.ops.empty() && int(out.ops.size()) > tr.op_begin && out.ops.back().kind == TOP_WHT &&
-                            !(out.ops.back().wht_mask & bit)) {
-                            out.ops.back().wht_mask |= bit;
+                        if (nops > rd.op_begin && P.ops[nops - 1].kind == TOP_WHT && !(P.ops[nops - 1].t & bit)) {
+                            P.ops[nops - 1].t = std::uint8_t(P.ops[nops - 1].t | bit);
                             continue;
                         }
-                        o.wht_mask = bit;
+                        o.t = std::uint8_t(bit);
                         break;
                     }
                     case TOP_DIAG:
-                        o.dk = f.dk;
-                        for (int i = 0; i < f.dk; ++i) o.dpos[i] = f.dpos[i];
-                        for (int g = 0; g < 8; ++g) {
-                            o.val[0][g] = f.dval[g];
-                            o.dskip[g] = f.dskip[g];
+                        o.dk = std::uint8_t(f.dk);
+                        for (int i = 0; i < f.dk; ++i) {
+                            o.dpos[i] = std::uint8_t(f.dpos[i]);
+                            const int rb = loc[f.dpos[i]] >= 0 ? reg(f.dpos[i]) : -1;
+                            o.dreg[i] = rb >= 0 ? std::uint8_t(rb) : 0xff;
                         }
+                        for (int g = 0; g < (1 << f.dk); ++g) {
+                            if (f.dskip[g]) o.dskip = std::uint8_t(o.dskip | (1u << g));
+                            if (g < 4) o.c[g] = f.dval[g];
+                            big.val[0][g] = f.dval[g];
+                        }
+                        use_big = f.dk == 3;
                         break;
                     case TOP_SIGN:
-                        o.flip_off = out.flips.size();
-                        o.flip_cnt = f.flips.size();
-                        o.flip_rest = f.flip_rest;
+                        big.flip_off = out.flips.size();
+                        big.flip_cnt = f.flips.size();
+                        big.flip_rest = f.flip_rest;
+                        flip_off = big.flip_off;
+                        flip_cnt = big.flip_cnt;
                         out.flips.insert(out.flips.end(), f.flips.begin(), f.flips.end());
+                        use_big = true;
                         break;
                     case TOP_SCALE:
-                        o.scale = f.scale;
+                        o.c[0] = make_double2(f.scale, 0.0);
                         break;
                     default: break;
                 }
-                out.ops.push_back(o);
+                if (use_big) {
+                    if (out.big.size() >= 0xffff) raise(QCS_ERR_SIM, "internal: plan too large");
+                    o.ref = std::uint16_t(out.big.size());
+                    out.big.push_back(big);
+                }
+                P.ops[nops++] = o;
             }
-            tr.op_count = int(out.ops.size()) - tr.op_begin;
-            out.rounds.push_back(tr);
+            rd.op_count = std::uint16_t(nops - rd.op_begin);
         }
-        tp.round_count = int(out.rounds.size()) - tp.round_begin;
-        out.passes.push_back(tp);
+        out.passes.push_back(P);
         out.pass_ops.push_back(pp.ops);
+        out.single_flip_off.push_back(flip_off);
+        out.single_flip_cnt.push_back(flip_cnt);
     }
 }
 

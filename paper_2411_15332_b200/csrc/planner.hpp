@@ -54,11 +54,11 @@ struct Plan {
 Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits);
 
 struct Lowered {
-    std::vector<TilePass> passes;
-    std::vector<TileRound> rounds;
-    std::vector<TileOp> ops;
+    std::vector<PassParams> passes;
+    std::vector<TileOp> big;                 // shared-memory gates, sign steps, 3-bit diagonals
     std::vector<u64> flips;
     std::vector<std::vector<int>> pass_ops;  // FOp indices per pass
+    std::vector<u64> single_flip_off, single_flip_cnt;  // sign step of a single-op pass
 };
 void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& out);
 

@@ -3,22 +3,26 @@
 // A pass owns a set S of m basis-bit positions, the tile bits (S always holds bits 0..2, so
 // warp accesses are 128-byte runs).  Each CTA copies the 2^m amplitudes of one tile -- the
 // indices that agree outside S -- from HBM into shared memory with cp.async (16 B per
-// request, every request of the tile in flight at once), runs the pass's operations, and
-// streams the tile back: one HBM round trip, 32 B per amplitude, for the whole operation list.
+// request, the whole tile in flight at once), runs the pass's operations, and streams the tile
+// back: one HBM round trip, 32 B per amplitude, for the whole operation list.
 //
-// Operations execute in "rounds": in a round every thread holds 8 amplitudes in registers
-// that differ exactly in three tile bits (the round bits) and applies every operation of the
-// round to them; rounds are separated by one shared-memory exchange and a barrier.  Shared
-// memory is XOR-swizzled (position = j ^ ((j >> 3) & 7)) so the 16-byte accesses of a round
-// are bank-conflict free whichever three bits it owns.
+// Operations execute in rounds: in a round each thread holds 8 amplitudes in registers that
+// differ exactly in three tile bits (the round bits) and applies every operation of the round
+// to them; rounds are separated by one shared-memory exchange and a barrier.  Shared memory is
+// XOR-swizzled (position = j ^ ((j >> 3) & 7)) so 16-byte accesses are bank-conflict free
+// whichever three bits a round owns.  The pass description -- rounds and compact operations --
+// travels in the kernel parameter space (<= 32 KB), i.e. the constant bank: every thread
+// reads the same operation at the same time, which the constant cache broadcasts.
 //
-// Operation kinds: a gate on up to 3 targets among the round bits (controls anywhere: on tile
-// bits they are tested per element group, outside the tile once per CTA); a diagonal phase
-// on up to 3 basis bits anywhere; a diagonal sign step (Grover oracle / Z0, engine.cpp:62-80);
-// unnormalised Walsh-Hadamard butterflies (the RH structure, rh.cpp:92-156: scale by
-// 2^{-n/2} first, then +-1 sums); a real scale.  Gate rows use dax_mvm's arithmetic
-// (acc = 0; acc += v * x in ascending column order, separately rounded), so a pass holding a
-// single gate reproduces the reference bit for bit.
+// Register operations: a one-target gate (controls anywhere; tile-bit controls are tested per
+// element group, controls outside the tile once per CTA), a diagonal phase on up to three
+// basis bits (bits outside the round are constant over a group: resolved once per group), a
+// diagonal sign step (Grover oracle / Z0, engine.cpp:62-80), unnormalised Walsh-Hadamard
+// butterflies (the RH structure, rh.cpp:92-156: scale by 2^{-n/2} first, then +-1 sums) and a
+// real scale.  Gates on 2-3 targets run straight on shared memory in rounds of their own.
+// Gate rows use dax_mvm's arithmetic (acc = 0; acc += v * x in ascending column order, each
+// operation separately rounded), so a single-gate pass reproduces the reference bit for bit.
+#include <algorithm>
 #include <cstdint>
 
 #include "common.hpp"
@@ -62,60 +66,29 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// Register index q (3 bits) <-> round bits: local index = lb | (q0 << r0) | (q1 << r1) | (q2 << r2).
-struct Round {
-    unsigned lb;       // this thread's local base (round bits zero)
-    unsigned ro[3];    // 1 << r_i
-    __device__ __forceinline__ unsigned local(int q) const {
-        return lb | ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u);
-    }
-};
-
-// One-target gate in register bit T.  The row tables are decoded once per operation into a
-// 2x2 recipe: row r is untouched (identity), one product (monomial), or two products in
-// ascending column order -- dax_mvm's accumulation for that row.
-struct Gate1 {
-    int kind[2];   // 0 untouched, 1 single product, 2 two products
-    int col[2];    // column of the single product
-    double2 a[2], b[2];
-};
-
-__device__ __forceinline__ Gate1 decode1(const TileOp& o) {
-    Gate1 g;
-    g.kind[0] = g.kind[1] = 0;
-    g.col[0] = g.col[1] = 0;
-    g.a[0] = g.a[1] = g.b[0] = g.b[1] = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {  // static indices only: keeps the recipe in registers
-        if (r >= o.nrows) break;
-        const bool hi = o.row_member[r] != 0;
-        const int kind = o.nnz[r], col = o.col_member[r][0];
-        const double2 a = o.val[r][0], b = kind > 1 ? o.val[r][1] : make_double2(0.0, 0.0);
-        if (hi) {
-            g.kind[1] = kind; g.col[1] = col; g.a[1] = a; g.b[1] = b;
-        } else {
-            g.kind[0] = kind; g.col[0] = col; g.a[0] = a; g.b[0] = b;
-        }
-    }
-    return g;
-}
-
-__device__ __forceinline__ double2 row1(const Gate1& g, int r, double2 x0, double2 x1, double2 self) {
-    if (g.kind[r] == 0) return self;
-    if (g.kind[r] == 1) return madd(make_double2(0.0, 0.0), g.a[r], g.col[r] ? x1 : x0);
-    return madd(madd(make_double2(0.0, 0.0), g.a[r], x0), g.b[r], x1);
+// Row recipe of a one-target gate: rk = 0 untouched, 1 one product (column rc), 2 two products.
+__device__ __forceinline__ double2 gate_row(int rk, int rc, double2 a, double2 b, double2 x0, double2 x1,
+                                            double2 self) {
+    if (rk == 0) return self;
+    if (rk == 1) return madd(make_double2(0.0, 0.0), a, rc ? x1 : x0);
+    return madd(madd(make_double2(0.0, 0.0), a, x0), b, x1);
 }
 
 template <int T>
-__device__ __forceinline__ void gate_op(double2 (&v)[8], const TileOp& o, const Round& rd) {
-    const Gate1 g = decode1(o);
+__device__ __forceinline__ void gate1(double2 (&v)[8], const RegOp& o, unsigned lb, const unsigned (&ro)[3]) {
+    const int rk0 = o.rk0, rk1 = o.rk1, rc0 = o.rc0, rc1 = o.rc1;
+    const double2 a0 = o.c[0], b0 = o.c[1], a1 = o.c[2], b1 = o.c[3];
+    const unsigned cm = o.lctrl_mask, cv = o.lctrl_val;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         if (q & (1 << T)) continue;
-        if (o.lctrl_mask && (rd.local(q) & o.lctrl_mask) != o.lctrl_val) continue;
+        if (cm) {
+            const unsigned l = lb | ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u);
+            if ((l & cm) != cv) continue;
+        }
         const double2 x0 = v[q], x1 = v[q | (1 << T)];
-        v[q] = row1(g, 0, x0, x1, x0);
-        v[q | (1 << T)] = row1(g, 1, x0, x1, x1);
+        v[q] = gate_row(rk0, rc0, a0, b0, x0, x1, x0);
+        v[q | (1 << T)] = gate_row(rk1, rc1, a1, b1, x0, x1, x1);
     }
 }
 
@@ -130,25 +103,41 @@ __device__ __forceinline__ void butterfly(double2 (&v)[8]) {
     }
 }
 
-__device__ __forceinline__ void dispatch_gate(double2 (&v)[8], const TileOp& o, const Round& rd) {
-    switch (o.gcase) {  // K and the register bits of the targets, see tile_gate_case()
-        case 0: gate_op<0>(v, o, rd); break;
-        case 1: gate_op<1>(v, o, rd); break;
-        case 2: gate_op<2>(v, o, rd); break;
-        default: break;
+// Diagonal phase: entry index g from up to three basis bits; bits held in registers vary with
+// q, the others are constant over the thread's group (taken from the group's first element).
+__device__ __forceinline__ void diag_op(double2 (&v)[8], const RegOp& o, const TileOp* big, u64 g0) {
+    const int dk = o.dk;
+    int cg = 0;
+    int regbit[3] = {-1, -1, -1};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        if (i >= dk) break;
+        const int sh = dk - 1 - i;
+        if (o.dreg[i] < 3) regbit[i] = o.dreg[i];
+        else cg |= int((g0 >> o.dpos[i]) & 1) << sh;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        int g = cg;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            if (i < dk && regbit[i] >= 0) g |= ((q >> regbit[i]) & 1) << (dk - 1 - i);
+        if (o.dskip >> g & 1) continue;
+        const double2 d = dk < 3 ? o.c[g & 3] : big[o.ref].val[0][g];
+        v[q] = madd(make_double2(0.0, 0.0), d, v[q]);
     }
 }
 
-// Gates on 2 or 3 targets run directly on shared memory in their own round (keeps the
-// register rounds small): each thread takes groups of 2^K amplitudes.
+// Gates on 2 or 3 targets, straight on shared memory (rare: after control peeling the catalog
+// leaves only Swap-like and 4x4/8x8 dense gates here).
 template <int K>
-__device__ __noinline__ void smem_gate(double2* sm, const TileOp& o, int m, unsigned nthreads) {
+__device__ __noinline__ void smem_gate(double2* sm, const TileOp& o, int m, unsigned stride) {
     constexpr int NM = 1 << K;
-    int asc[K];  // target local bits ascending (zero-insertion order)
+    int asc[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) asc[i] = o.tl[K - 1 - i];
     const unsigned ngroups = 1u << (m - K);
-    for (unsigned g = threadIdx.x; g < ngroups; g += nthreads) {
+    for (unsigned g = threadIdx.x; g < ngroups; g += stride) {
         unsigned lb = g;
 #pragma unroll
         for (int i = 0; i < K; ++i) lb = insert_zero(lb, asc[i]);
@@ -200,40 +189,35 @@ constexpr int kThreads = 256;
 constexpr int kMaxBits = 12;
 
 __global__ void __launch_bounds__(kThreads, 2)
-    k_tile(double2* __restrict__ a, const __grid_constant__ TilePass p, const TileRound* __restrict__ rounds,
-           const TileOp* __restrict__ ops, const u64* __restrict__ flipped) {
+    k_tile(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,
+           const u64* __restrict__ flipped) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int m = p.m;
+    const int m = P.m;
     const unsigned sz = 1u << m;
-    const unsigned nthreads = sz >> 3;  // 8 amplitudes per thread
+    const unsigned ngroups = sz >> 3;  // 8 amplitudes per group
     double2* sm = reinterpret_cast<double2*>(smem_raw);
-    u64* hi_tab = reinterpret_cast<u64*>(sm + sz);  // global offset of local bits 3..m-1
-    const unsigned t = threadIdx.x;
-    for (unsigned j = t; j < (sz >> 3); j += blockDim.x) {
+    u64* hi_tab = reinterpret_cast<u64*>(sm + sz);  // basis offset of local bits 3..m-1
+    const unsigned t = threadIdx.x, bt = blockDim.x;
+    for (unsigned j = t; j < ngroups; j += bt) {
         u64 v = 0;
         for (int b = 3; b < m; ++b)
-            if (j >> (b - 3) & 1) v |= u64(1) << p.bits[b];
+            if (j >> (b - 3) & 1) v |= u64(1) << P.bits[b];
         hi_tab[j] = v;
     }
     u64 base = blockIdx.x;
-    u64 tile_mask = 0;
-    for (int b = 0; b < m; ++b) {
-        const int pos = p.bits[b];
+    for (int b = 0; b < m; ++b) {  // bits[] ascending: insert zeros from the lowest position up
+        const int pos = P.bits[b];
         base = ((base >> pos) << (pos + 1)) | (base & ((u64(1) << pos) - 1));
-        tile_mask |= u64(1) << pos;
     }
-    (void)tile_mask;
     __syncthreads();
-    const unsigned bt = blockDim.x;
-    // load: consecutive threads take consecutive local indices (bits 0..2 are basis bits 0..2)
     for (unsigned j = t; j < sz; j += bt) cp_async16(sm + swz(j), a + (base | (j & 7u) | hi_tab[j >> 3]));
     cp_async_wait_all();
     __syncthreads();
-    for (int ri = 0; ri < p.round_count; ++ri) {
-        const TileRound& R = rounds[p.round_begin + ri];
-        if (R.smem) {  // gates on 2-3 targets, straight on shared memory
-            for (int oi = 0; oi < R.op_count; ++oi) {
-                const TileOp& o = ops[R.op_begin + oi];
+    for (int ri = 0; ri < P.nrounds; ++ri) {
+        const RoundDesc& R = P.rounds[ri];
+        if (R.smem) {
+            for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
+                const TileOp& o = big[P.ops[oi].ref];
                 if (!(o.gctrl_mask && (base & o.gctrl_mask) != o.gctrl_val)) {
                     if (o.gcase == 2) smem_gate<2>(sm, o, m, bt);
                     else smem_gate<3>(sm, o, m, bt);
@@ -242,50 +226,44 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             continue;
         }
-        for (unsigned g = t; g < nthreads; g += bt) {
-            Round rd;
-            unsigned lb = g;
-            lb = insert_zero(lb, R.rbits[0]);
-            lb = insert_zero(lb, R.rbits[1]);
-            lb = insert_zero(lb, R.rbits[2]);
-            rd.lb = lb;
-            rd.ro[0] = 1u << R.rbits[0];
-            rd.ro[1] = 1u << R.rbits[1];
-            rd.ro[2] = 1u << R.rbits[2];
+        const int r0 = R.r[0], r1 = R.r[1], r2 = R.r[2];
+        const unsigned ro[3] = {1u << r0, 1u << r1, 1u << r2};
+        const u64 go[3] = {u64(1) << P.bits[r0], u64(1) << P.bits[r1], u64(1) << P.bits[r2]};
+        for (unsigned g = t; g < ngroups; g += bt) {
+            const unsigned lb = insert_zero(insert_zero(insert_zero(g, r0), r1), r2);
             double2 v[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = sm[swz(rd.local(q))];
-            for (int oi = 0; oi < R.op_count; ++oi) {
-                const TileOp& o = ops[R.op_begin + oi];
+            for (int q = 0; q < 8; ++q)
+                v[q] = sm[swz(lb | ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u))];
+            const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];  // basis index of register 0
+            for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
+                const RegOp& o = P.ops[oi];
                 if (o.gctrl_mask && (base & o.gctrl_mask) != o.gctrl_val) continue;
                 switch (o.kind) {
-                    case TOP_GATE: dispatch_gate(v, o, rd); break;
+                    case TOP_GATE:
+                        if (o.t == 0) gate1<0>(v, o, lb, ro);
+                        else if (o.t == 1) gate1<1>(v, o, lb, ro);
+                        else gate1<2>(v, o, lb, ro);
+                        break;
                     case TOP_WHT:
-                        if (o.wht_mask & 1) butterfly<0>(v);
-                        if (o.wht_mask & 2) butterfly<1>(v);
-                        if (o.wht_mask & 4) butterfly<2>(v);
+                        if (o.t & 1) butterfly<0>(v);
+                        if (o.t & 2) butterfly<1>(v);
+                        if (o.t & 4) butterfly<2>(v);
                         break;
-                    case TOP_SCALE:
+                    case TOP_SCALE: {
+                        const double s = o.c[0].x;
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) v[q] = make_double2(v[q].x * o.scale, v[q].y * o.scale);
+                        for (int q = 0; q < 8; ++q) v[q] = make_double2(v[q].x * s, v[q].y * s);
                         break;
-                    case TOP_DIAG:
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const unsigned j = rd.local(q);
-                            const u64 gi = base | (j & 7u) | hi_tab[j >> 3];
-                            int gg = 0;
-                            for (int i = 0; i < o.dk; ++i) gg = (gg << 1) | int((gi >> o.dpos[i]) & 1);
-                            if (!o.dskip[gg]) v[q] = madd(make_double2(0.0, 0.0), o.val[0][gg], v[q]);
-                        }
-                        break;
+                    }
+                    case TOP_DIAG: diag_op(v, o, big, g0); break;
                     case TOP_SIGN: {
-                        const u64* f = flipped + o.flip_off;
+                        const TileOp& so = big[o.ref];
+                        const u64* f = flipped + so.flip_off;
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            const unsigned j = rd.local(q);
-                            const u64 gi = base | (j & 7u) | hi_tab[j >> 3];
-                            if (listed(f, o.flip_cnt, gi) != (o.flip_rest != 0)) v[q] = neg_exact(v[q]);
+                            const u64 gi = g0 | ((q & 1) ? go[0] : 0) | ((q & 2) ? go[1] : 0) | ((q & 4) ? go[2] : 0);
+                            if (listed(f, so.flip_cnt, gi) != (so.flip_rest != 0)) v[q] = neg_exact(v[q]);
                         }
                         break;
                     }
@@ -293,7 +271,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) sm[swz(rd.local(q))] = v[q];
+            for (int q = 0; q < 8; ++q)
+                sm[swz(lb | ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u))] = v[q];
         }
         __syncthreads();
     }
@@ -304,8 +283,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 int tile_max_bits() { return kMaxBits; }
 
-void launch_tile_pass(double2* amps, int n, const TilePass& p, const TileRound* rounds_dev, const TileOp* ops_dev,
-                      const std::uint64_t* flipped_dev, cudaStream_t st) {
+void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* big_dev, const std::uint64_t* flipped_dev,
+                      cudaStream_t st) {
     if (p.m < 3 || p.m > kMaxBits || p.m > n) raise(QCS_ERR_ARG, "tile bits out of range");
     const std::size_t smem = (std::size_t(1) << p.m) * sizeof(double2) + (std::size_t(1) << (p.m - 3)) * sizeof(u64);
     static bool attr_set[64] = {};  // per device
@@ -321,7 +300,7 @@ void launch_tile_pass(double2* amps, int n, const TilePass& p, const TileRound* 
     if (tiles > 0x7fffffffull) raise(QCS_ERR_CAPACITY, "too many tiles for one launch");
     const int threads = std::min(kThreads, std::max(32, 1 << (p.m - 3)));
     TimedLaunch tl("tile_pass", 32.0 * double(u64(1) << n), st);
-    k_tile<<<unsigned(tiles), threads, smem, st>>>(amps, p, rounds_dev, ops_dev, flipped_dev);
+    k_tile<<<unsigned(tiles), threads, smem, st>>>(amps, p, big_dev, flipped_dev);
     check_launch("k_tile");
 }
 
