@@ -26,6 +26,7 @@ struct GateDesc {
     std::uint8_t row_member[8];
     std::uint8_t nnz[8];
     std::uint8_t col_member[8][8];
+    std::uint8_t vkind[8][8];     // coefficient kind: 0 complex, 1 real, 2 imaginary
     double2 val[8][8];
 };
 

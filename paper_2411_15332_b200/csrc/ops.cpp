@@ -122,6 +122,7 @@ bool build_gate_desc(const GateOp& op, GateDesc& d) {
             if (is_zero(v)) continue;    // dax_encode skips exact zeros (dax.cpp:42)
             d.col_member[r][z] = std::uint8_t(member_of(c));
             d.val[r][z] = make_double2(v.real(), v.imag());
+            d.vkind[r][z] = std::uint8_t(v.imag() == 0.0 ? 1 : (v.real() == 0.0 ? 2 : 0));
             ++z;
         }
         d.nnz[r] = std::uint8_t(z);
