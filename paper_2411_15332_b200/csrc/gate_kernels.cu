@@ -12,6 +12,7 @@
 // keeps several independent groups in flight.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.hpp"
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(256) k_gate(double2* __restrict__ a, u64 ngrou
                 double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int z = 0; z < NNZ; ++z)
-                    if (z < d.nnz[r]) acc = madd_k(acc, d.val[r][z], d.vkind[r][z], pick<NF>(x[it], d.col_member[r][z]));
+                    if (z < d.nnz[r]) acc = madd(acc, d.val[r][z], pick<NF>(x[it], d.col_member[r][z]));
                 out[r] = acc;
             }
         }
@@ -148,15 +149,34 @@ int max_nnz(const GateDesc& d) {
 
 }  // namespace
 
+// Tuning hook (QCS_GATE_ITEMS=1|2|4 picks the groups per thread of the f0/f1 kernels).
+int items_override() {
+    static const int v = [] {
+        const char* e = std::getenv("QCS_GATE_ITEMS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 void launch_gate(double2* amps, int n, const GateDesc& d, cudaStream_t st) {
     const int z = max_nnz(d);
+    const int it = items_override();
     switch (d.nfree) {
         case 0:  // diagonal entry on a fixed sub-cube (Z, S, T, CZ)
-            launch<0, 1, 8>(amps, n, d, st, "gate_f0_diag");
+            if (it == 1) launch<0, 1, 1>(amps, n, d, st, "gate_f0_diag");
+            else if (it == 2) launch<0, 1, 2>(amps, n, d, st, "gate_f0_diag");
+            else launch<0, 1, 4>(amps, n, d, st, "gate_f0_diag");
             return;
         case 1:
-            if (z <= 1) launch<1, 1, 2>(amps, n, d, st, "gate_f1_monomial");  // X, Y, RZ, CNOT, CCX
-            else launch<1, 2, 2>(amps, n, d, st, "gate_f1_dense");             // H, RX, RY, U3, CH
+            if (z <= 1) {  // X, Y, RZ, CNOT, CCX
+                if (it == 1) launch<1, 1, 1>(amps, n, d, st, "gate_f1_monomial");
+                else if (it == 4) launch<1, 1, 4>(amps, n, d, st, "gate_f1_monomial");
+                else launch<1, 1, 2>(amps, n, d, st, "gate_f1_monomial");
+            } else {       // H, RX, RY, U3, CH
+                if (it == 1) launch<1, 2, 1>(amps, n, d, st, "gate_f1_dense");
+                else if (it == 4) launch<1, 2, 4>(amps, n, d, st, "gate_f1_dense");
+                else launch<1, 2, 2>(amps, n, d, st, "gate_f1_dense");
+            }
             return;
         case 2:
             if (z <= 1) launch<2, 1, 2>(amps, n, d, st, "gate_f2_monomial");  // SWAP, iSwap, RZZ, DCX
