@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(256) k_gate(double2* __restrict__ a, u64 ngrou
                                               const __grid_constant__ GateDesc d) {
     constexpr int NM = 1 << NF;
     const u64 stride = u64(gridDim.x) * blockDim.x;
-    const u64 t0 = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    // grid-stride over chunks of ITEMS * stride groups (one chunk when the grid covers all)
+    for (u64 t0 = u64(blockIdx.x) * blockDim.x + threadIdx.x; t0 < ngroups; t0 += stride * ITEMS) {
     double2 x[ITEMS][NM];
     u64 base[ITEMS];
 #pragma unroll
@@ -102,6 +103,16 @@ __global__ void __launch_bounds__(256) k_gate(double2* __restrict__ a, u64 ngrou
         for (int r = 0; r < 8; ++r)
             if (r < d.nrows) st_stream(a + (base[it] | d.member_off[d.row_member[r]]), out[r]);
     }
+    }
+}
+
+// Persistent grid (QCS_GATE_PERSIST=k: k resident waves) vs one thread per ITEMS groups.
+int persist_override() {
+    static const int v = [] {
+        const char* e = std::getenv("QCS_GATE_PERSIST");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
 }
 
 // Algorithmic HBM bytes of one pass: 16 B per member read and per row written, counted per
@@ -134,7 +145,13 @@ void launch(double2* a, int n, const GateDesc& d, cudaStream_t st, const char* c
     const u64 ngroups = u64(1) << (n - d.k);
     const int threads = 256;
     const u64 per_block = u64(threads) * ITEMS;
-    const u64 blocks = (ngroups + per_block - 1) / per_block;
+    u64 blocks = (ngroups + per_block - 1) / per_block;
+    if (const int waves = persist_override()) {
+        int occ = 0;
+        QCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gate<NF, NNZ, ITEMS>, threads, 0));
+        const u64 cap = u64(148) * u64(occ > 0 ? occ : 1) * u64(waves);
+        blocks = blocks < cap ? blocks : cap;
+    }
     if (blocks > 0x7fffffffull) raise(QCS_ERR_CAPACITY, "state too large for one launch");
     TimedLaunch tl(cls, algorithmic_bytes(n, d), st);
     k_gate<NF, NNZ, ITEMS><<<unsigned(blocks), threads, 0, st>>>(a, ngroups, d);
