@@ -10,6 +10,12 @@
 // reference's for single-placement steps.  The pass is HBM-bound: 16 B read + 16 B written
 // per touched amplitude, no reuse, so loads/stores carry evict-first hints and each thread
 // keeps several independent groups in flight.
+//
+// Three kernels by group shape, kept lean in registers (occupancy is what hides HBM latency):
+//   k_diag1  one member per group: a diagonal entry on a fixed sub-cube (Z, S, T, CZ, CCZ)
+//   k_pair   two members: any one-target gate, controls folded into the fixed bits
+//            (X, Y, H, RX, RY, U3, RZ, CNOT, CY, CH, Toffoli, ...)
+//   k_gate   2-3 free bits: the generic row-table kernel (Swap, iSwap, RXX, DCX, ...)
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -34,26 +40,15 @@ __device__ __forceinline__ double2 madd(double2 acc, double2 v, double2 x) {
 }
 
 // Insert zero bits at the k ascending positions: group index -> base basis index.
-__device__ __forceinline__ u64 insert_zeros(u64 t, const GateDesc& d) {
+__device__ __forceinline__ u64 insert_zeros(u64 t, int k, const int (&pos)[3]) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        if (i < d.k) {
-            const int p = d.pos_asc[i];
+        if (i < k) {
+            const int p = pos[i];
             t = ((t >> p) << (p + 1)) | (t & ((u64(1) << p) - 1));
         }
     }
     return t;
-}
-
-// acc + v * x, skipping the products by an exact-zero component of v (kind 1: real v, kind 2:
-// imaginary v).  Bit-identical to madd: a dropped product is +-0, and adding +-0 to an
-// accumulator that started at +0 changes neither its value nor, after the leading 0 + ..., its
-// sign (x + +-0 = x for x != 0; +0 + -0 = +0).  Inputs are finite.
-__device__ __forceinline__ double2 madd_k(double2 acc, double2 v, int kind, double2 x) {
-    if (kind == 1) return make_double2(__dadd_rn(acc.x, __dmul_rn(v.x, x.x)), __dadd_rn(acc.y, __dmul_rn(v.x, x.y)));
-    if (kind == 2)
-        return make_double2(__dadd_rn(acc.x, -__dmul_rn(v.y, x.y)), __dadd_rn(acc.y, __dmul_rn(v.y, x.x)));
-    return madd(acc, v, x);
 }
 
 template <int NF>
@@ -65,20 +60,83 @@ __device__ __forceinline__ double2 pick(const double2 (&x)[1 << NF], int m) {
     return v;
 }
 
+// ---------------------------------------------------------------- one member per group
+struct Diag1 {
+    int k;
+    int pos[3];
+    u64 fixed;
+    double2 d;
+};
+
+template <int ITEMS>
+__global__ void __launch_bounds__(256) k_diag1(double2* __restrict__ a, u64 ngroups, const __grid_constant__ Diag1 p) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    const u64 t0 = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    double2 x[ITEMS];
+    u64 idx[ITEMS];
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        idx[it] = insert_zeros(t0 + it * stride, p.k, p.pos) | p.fixed;
+        if (t0 + it * stride < ngroups) x[it] = ld_stream(a + idx[it]);
+    }
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it)
+        if (t0 + it * stride < ngroups) st_stream(a + idx[it], madd(make_double2(0.0, 0.0), p.d, x[it]));
+}
+
+// ---------------------------------------------------------------- two members per group
+struct Pair {
+    int k;
+    int pos[3];
+    u64 fixed;
+    u64 off1;        // basis offset of member 1
+    int load0, load1;
+    int rk[2];       // row kind: 0 untouched, 1 one product (column rc), 2 two products
+    int rc[2];
+    double2 a[2], b[2];
+};
+
+__device__ __forceinline__ double2 pair_row(int rk, int rc, double2 a, double2 b, double2 x0, double2 x1) {
+    if (rk == 1) return madd(make_double2(0.0, 0.0), a, rc ? x1 : x0);
+    return madd(madd(make_double2(0.0, 0.0), a, x0), b, x1);
+}
+
+template <int ITEMS>
+__global__ void __launch_bounds__(256) k_pair(double2* __restrict__ a, u64 ngroups, const __grid_constant__ Pair p) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    const u64 t0 = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    double2 x0[ITEMS], x1[ITEMS];
+    u64 idx[ITEMS];
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        idx[it] = insert_zeros(t0 + it * stride, p.k, p.pos) | p.fixed;
+        if (t0 + it * stride < ngroups) {
+            if (p.load0) x0[it] = ld_stream(a + idx[it]);
+            if (p.load1) x1[it] = ld_stream(a + (idx[it] | p.off1));
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        if (t0 + it * stride >= ngroups) continue;
+        if (p.rk[0]) st_stream(a + idx[it], pair_row(p.rk[0], p.rc[0], p.a[0], p.b[0], x0[it], x1[it]));
+        if (p.rk[1]) st_stream(a + (idx[it] | p.off1), pair_row(p.rk[1], p.rc[1], p.a[1], p.b[1], x0[it], x1[it]));
+    }
+}
+
+// ---------------------------------------------------------------- generic row tables
 // NF: free bits per group; NNZ: max nonzeros per touched row; ITEMS: groups per thread.
 template <int NF, int NNZ, int ITEMS>
 __global__ void __launch_bounds__(256) k_gate(double2* __restrict__ a, u64 ngroups,
                                               const __grid_constant__ GateDesc d) {
     constexpr int NM = 1 << NF;
     const u64 stride = u64(gridDim.x) * blockDim.x;
-    // grid-stride over chunks of ITEMS * stride groups (one chunk when the grid covers all)
-    for (u64 t0 = u64(blockIdx.x) * blockDim.x + threadIdx.x; t0 < ngroups; t0 += stride * ITEMS) {
+    const u64 t0 = u64(blockIdx.x) * blockDim.x + threadIdx.x;
     double2 x[ITEMS][NM];
     u64 base[ITEMS];
 #pragma unroll
     for (int it = 0; it < ITEMS; ++it) {
         const u64 g = t0 + it * stride;
-        base[it] = insert_zeros(g, d) | d.fixed_val;
+        base[it] = insert_zeros(g, d.k, d.pos_asc) | d.fixed_val;
         if (g < ngroups) {
 #pragma unroll
             for (int m = 0; m < NM; ++m)
@@ -103,16 +161,16 @@ __global__ void __launch_bounds__(256) k_gate(double2* __restrict__ a, u64 ngrou
         for (int r = 0; r < 8; ++r)
             if (r < d.nrows) st_stream(a + (base[it] | d.member_off[d.row_member[r]]), out[r]);
     }
-    }
 }
 
-// Persistent grid (QCS_GATE_PERSIST=k: k resident waves) vs one thread per ITEMS groups.
-int persist_override() {
-    static const int v = [] {
-        const char* e = std::getenv("QCS_GATE_PERSIST");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
+// role of basis bit 0 in a group: -2 fixed gate bit, >= 0 free member bit, -1 not a gate bit
+int bit0_role(const GateDesc& d) {
+    int b0 = -1;
+    for (int i = 0; i < d.k; ++i)
+        if (d.pos_asc[i] == 0) b0 = -2;
+    for (int i = 0; i < d.nfree; ++i)
+        if (d.free_bit[i] == 1) b0 = i;
+    return b0;
 }
 
 // Algorithmic HBM bytes of one pass: 16 B per member read and per row written, counted per
@@ -120,17 +178,13 @@ int persist_override() {
 // sector (SURVEY.md section 8d sector rounding).
 double algorithmic_bytes(int n, const GateDesc& d) {
     const double groups = double(u64(1) << (n - d.k));
-    int bit0 = -1;  // role of basis bit 0 in the group: -2 fixed, >= 0 free member bit, -1 not a gate bit
-    for (int i = 0; i < d.k; ++i)
-        if (d.pos_asc[i] == 0) bit0 = -2;  // fixed unless it is one of the free bits below
-    for (int i = 0; i < d.nfree; ++i)
-        if (d.free_bit[i] == 1) bit0 = i;
+    const int b0 = bit0_role(d);
     auto cost = [&](unsigned mask) {
         double c = 0;
         for (int m = 0; m < (1 << d.nfree); ++m) {
             if (!(mask >> m & 1)) continue;
-            if (bit0 == -2) c += 2;
-            else if (bit0 >= 0) c += (mask >> (m ^ (1 << bit0)) & 1) ? 1 : 2;
+            if (b0 == -2) c += 2;
+            else if (b0 >= 0) c += (mask >> (m ^ (1 << b0)) & 1) ? 1 : 2;
             else c += 1;
         }
         return c;
@@ -140,22 +194,17 @@ double algorithmic_bytes(int n, const GateDesc& d) {
     return groups * 16.0 * (cost(d.load_mask) + cost(rows));
 }
 
-template <int NF, int NNZ, int ITEMS>
-void launch(double2* a, int n, const GateDesc& d, cudaStream_t st, const char* cls) {
-    const u64 ngroups = u64(1) << (n - d.k);
+template <class K, class P>
+void launch_k(K kernel, double2* a, int n, int k, const GateDesc& d, const P& params, int items, cudaStream_t st,
+              const char* cls) {
+    const u64 ngroups = u64(1) << (n - k);
     const int threads = 256;
-    const u64 per_block = u64(threads) * ITEMS;
-    u64 blocks = (ngroups + per_block - 1) / per_block;
-    if (const int waves = persist_override()) {
-        int occ = 0;
-        QCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gate<NF, NNZ, ITEMS>, threads, 0));
-        const u64 cap = u64(148) * u64(occ > 0 ? occ : 1) * u64(waves);
-        blocks = blocks < cap ? blocks : cap;
-    }
+    const u64 per_block = u64(threads) * u64(items);
+    const u64 blocks = (ngroups + per_block - 1) / per_block;
     if (blocks > 0x7fffffffull) raise(QCS_ERR_CAPACITY, "state too large for one launch");
     TimedLaunch tl(cls, algorithmic_bytes(n, d), st);
-    k_gate<NF, NNZ, ITEMS><<<unsigned(blocks), threads, 0, st>>>(a, ngroups, d);
-    check_launch("k_gate");
+    kernel<<<unsigned(blocks), threads, 0, st>>>(a, ngroups, params);
+    check_launch(cls);
 }
 
 int max_nnz(const GateDesc& d) {
@@ -164,9 +213,7 @@ int max_nnz(const GateDesc& d) {
     return z;
 }
 
-}  // namespace
-
-// Tuning hook (QCS_GATE_ITEMS=1|2|4 picks the groups per thread of the f0/f1 kernels).
+// Tuning hook: QCS_GATE_ITEMS=1|2|4 overrides the groups per thread.
 int items_override() {
     static const int v = [] {
         const char* e = std::getenv("QCS_GATE_ITEMS");
@@ -175,35 +222,57 @@ int items_override() {
     return v;
 }
 
+}  // namespace
+
 void launch_gate(double2* amps, int n, const GateDesc& d, cudaStream_t st) {
-    const int z = max_nnz(d);
-    const int it = items_override();
-    switch (d.nfree) {
-        case 0:  // diagonal entry on a fixed sub-cube (Z, S, T, CZ)
-            if (it == 1) launch<0, 1, 1>(amps, n, d, st, "gate_f0_diag");
-            else if (it == 2) launch<0, 1, 2>(amps, n, d, st, "gate_f0_diag");
-            else launch<0, 1, 4>(amps, n, d, st, "gate_f0_diag");
-            return;
-        case 1:
-            if (z <= 1) {  // X, Y, RZ, CNOT, CCX
-                if (it == 1) launch<1, 1, 1>(amps, n, d, st, "gate_f1_monomial");
-                else if (it == 4) launch<1, 1, 4>(amps, n, d, st, "gate_f1_monomial");
-                else launch<1, 1, 2>(amps, n, d, st, "gate_f1_monomial");
-            } else {       // H, RX, RY, U3, CH
-                if (it == 1) launch<1, 2, 1>(amps, n, d, st, "gate_f1_dense");
-                else if (it == 4) launch<1, 2, 4>(amps, n, d, st, "gate_f1_dense");
-                else launch<1, 2, 2>(amps, n, d, st, "gate_f1_dense");
-            }
-            return;
-        case 2:
-            if (z <= 1) launch<2, 1, 2>(amps, n, d, st, "gate_f2_monomial");  // SWAP, iSwap, RZZ, DCX
-            else launch<2, 4, 1>(amps, n, d, st, "gate_f2_dense");             // RXX, ECR, CU
-            return;
-        default:
-            if (z <= 1) launch<3, 1, 1>(amps, n, d, st, "gate_f3_monomial");
-            else launch<3, 8, 1>(amps, n, d, st, "gate_f3_dense");
-            return;
+    const int b0 = bit0_role(d);
+    const int ov = items_override();
+    if (d.nfree == 0) {  // measured on B200: bit 0 fixed -> 1 group per thread, else 2
+        Diag1 p{};
+        p.k = d.k;
+        std::memcpy(p.pos, d.pos_asc, sizeof(p.pos));
+        p.fixed = d.fixed_val;
+        p.d = d.val[0][0];
+        const int items = ov ? ov : (b0 == -2 ? 1 : 2);
+        if (items == 1) launch_k(k_diag1<1>, amps, n, d.k, d, p, 1, st, "gate_diag1");
+        else if (items == 4) launch_k(k_diag1<4>, amps, n, d.k, d, p, 4, st, "gate_diag1");
+        else launch_k(k_diag1<2>, amps, n, d.k, d, p, 2, st, "gate_diag1");
+        return;
     }
+    if (d.nfree == 1) {  // bit 0 in the group -> 4 groups per thread, else 2
+        Pair p{};
+        p.k = d.k;
+        std::memcpy(p.pos, d.pos_asc, sizeof(p.pos));
+        p.fixed = d.fixed_val;
+        p.off1 = d.member_off[1];
+        p.load0 = d.load_mask & 1;
+        p.load1 = (d.load_mask >> 1) & 1;
+        bool dense = false;
+        for (int r = 0; r < d.nrows; ++r) {
+            const int m = d.row_member[r];
+            p.rk[m] = d.nnz[r];
+            p.rc[m] = d.col_member[r][0];
+            p.a[m] = d.val[r][0];
+            if (d.nnz[r] > 1) {
+                p.b[m] = d.val[r][1];
+                dense = true;
+            }
+        }
+        const char* cls = dense ? "gate_pair_dense" : "gate_pair_monomial";
+        const int items = ov ? ov : (b0 != -1 ? 4 : 2);
+        if (items == 1) launch_k(k_pair<1>, amps, n, d.k, d, p, 1, st, cls);
+        else if (items == 4) launch_k(k_pair<4>, amps, n, d.k, d, p, 4, st, cls);
+        else launch_k(k_pair<2>, amps, n, d.k, d, p, 2, st, cls);
+        return;
+    }
+    const int z = max_nnz(d);
+    if (d.nfree == 2) {
+        if (z <= 1) launch_k(k_gate<2, 1, 2>, amps, n, d.k, d, d, 2, st, "gate_f2_monomial");  // Swap, iSwap, DCX
+        else launch_k(k_gate<2, 4, 1>, amps, n, d.k, d, d, 1, st, "gate_f2_dense");           // RXX, ECR, CU
+        return;
+    }
+    if (z <= 1) launch_k(k_gate<3, 1, 1>, amps, n, d.k, d, d, 1, st, "gate_f3_monomial");
+    else launch_k(k_gate<3, 8, 1>, amps, n, d.k, d, d, 1, st, "gate_f3_dense");
 }
 
 }  // namespace qcs
