@@ -75,6 +75,17 @@ bool build_gate_desc(const GateOp& op, GateDesc& d) {
         }
     }
     if (nt == 0) return false;
+    // Sector completion: when basis bit 0 is a gate bit (canonical local bit 0), close the
+    // touched set under its flip, so every 32-byte sector (amplitudes 2u, 2u+1) is read and
+    // written whole instead of half.  An added row is an identity row, computed as
+    // 0 + (1+0i) * x -- exactly what dax_mvm writes for it (the DAX step holds that entry).
+    if (op.pos[k - 1] == 0) {
+        for (int g = 0; g < dim; ++g)
+            if (touched[g] && !touched[g ^ 1]) {
+                touched[g ^ 1] = needed[g ^ 1] = true;
+                ++nt;
+            }
+    }
     // local bits constant across the needed set are fixed: the kernel enumerates only the
     // sub-cube (e.g. a CNOT touches half the state, a CZ a quarter)
     int fixed_mask = 0, fixed_val = 0;
