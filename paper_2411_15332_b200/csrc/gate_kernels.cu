@@ -101,7 +101,19 @@ __device__ __forceinline__ double2 pair_row(int rk, int rc, double2 a, double2 b
     return madd(madd(make_double2(0.0, 0.0), a, x0), b, x1);
 }
 
-template <int ITEMS>
+__device__ __forceinline__ void ld256(const double2* p, double2& a, double2& b) {
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+                 : "l"(p));
+}
+__device__ __forceinline__ void st256(double2* p, double2 a, double2 b) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+                 : "memory");
+}
+
+// ADJ: the two members are the halves of one 32-byte sector (the free bit is basis bit 0, both
+// loaded and both stored): one 256-bit load and store per group.
+template <int ITEMS, bool ADJ>
 __global__ void __launch_bounds__(256) k_pair(double2* __restrict__ a, u64 ngroups, const __grid_constant__ Pair p) {
     const u64 stride = u64(gridDim.x) * blockDim.x;
     const u64 t0 = u64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -111,13 +123,22 @@ __global__ void __launch_bounds__(256) k_pair(double2* __restrict__ a, u64 ngrou
     for (int it = 0; it < ITEMS; ++it) {
         idx[it] = insert_zeros(t0 + it * stride, p.k, p.pos) | p.fixed;
         if (t0 + it * stride < ngroups) {
-            if (p.load0) x0[it] = ld_stream(a + idx[it]);
-            if (p.load1) x1[it] = ld_stream(a + (idx[it] | p.off1));
+            if (ADJ) {
+                ld256(a + idx[it], x0[it], x1[it]);
+            } else {
+                if (p.load0) x0[it] = ld_stream(a + idx[it]);
+                if (p.load1) x1[it] = ld_stream(a + (idx[it] | p.off1));
+            }
         }
     }
 #pragma unroll
     for (int it = 0; it < ITEMS; ++it) {
         if (t0 + it * stride >= ngroups) continue;
+        if (ADJ) {
+            st256(a + idx[it], pair_row(p.rk[0], p.rc[0], p.a[0], p.b[0], x0[it], x1[it]),
+                  pair_row(p.rk[1], p.rc[1], p.a[1], p.b[1], x0[it], x1[it]));
+            continue;
+        }
         if (p.rk[0]) st_stream(a + idx[it], pair_row(p.rk[0], p.rc[0], p.a[0], p.b[0], x0[it], x1[it]));
         if (p.rk[1]) st_stream(a + (idx[it] | p.off1), pair_row(p.rk[1], p.rc[1], p.a[1], p.b[1], x0[it], x1[it]));
     }
@@ -222,6 +243,15 @@ int items_override() {
     return v;
 }
 
+// Tuning hook: QCS_GATE_ADJ=0 disables the 256-bit adjacent-pair path.
+int adj_override() {
+    static const int v = [] {
+        const char* e = std::getenv("QCS_GATE_ADJ");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 }  // namespace
 
 void launch_gate(double2* amps, int n, const GateDesc& d, cudaStream_t st) {
@@ -259,10 +289,17 @@ void launch_gate(double2* amps, int n, const GateDesc& d, cudaStream_t st) {
             }
         }
         const char* cls = dense ? "gate_pair_dense" : "gate_pair_monomial";
+        const bool adj = p.off1 == 1 && p.load0 && p.load1 && p.rk[0] && p.rk[1];
         const int items = ov ? ov : (b0 != -1 ? 4 : 2);
-        if (items == 1) launch_k(k_pair<1>, amps, n, d.k, d, p, 1, st, cls);
-        else if (items == 4) launch_k(k_pair<4>, amps, n, d.k, d, p, 4, st, cls);
-        else launch_k(k_pair<2>, amps, n, d.k, d, p, 2, st, cls);
+        if (adj && adj_override() != 0) {
+            if (items == 1) launch_k(k_pair<1, true>, amps, n, d.k, d, p, 1, st, cls);
+            else if (items == 4) launch_k(k_pair<4, true>, amps, n, d.k, d, p, 4, st, cls);
+            else launch_k(k_pair<2, true>, amps, n, d.k, d, p, 2, st, cls);
+            return;
+        }
+        if (items == 1) launch_k(k_pair<1, false>, amps, n, d.k, d, p, 1, st, cls);
+        else if (items == 4) launch_k(k_pair<4, false>, amps, n, d.k, d, p, 4, st, cls);
+        else launch_k(k_pair<2, false>, amps, n, d.k, d, p, 2, st, cls);
         return;
     }
     const int z = max_nnz(d);
