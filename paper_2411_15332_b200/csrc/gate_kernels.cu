@@ -290,7 +290,9 @@ void launch_gate(double2* amps, int n, const GateDesc& d, cudaStream_t st) {
         }
         const char* cls = dense ? "gate_pair_dense" : "gate_pair_monomial";
         const bool adj = p.off1 == 1 && p.load0 && p.load1 && p.rk[0] && p.rk[1];
-        const int items = ov ? ov : (b0 != -1 ? 4 : 2);
+        // measured on B200 (tools/gate_timing.py): sector pairs 1 group per thread, bit 0
+        // elsewhere in the group 4, otherwise 2
+        const int items = ov ? ov : (adj ? 1 : (b0 != -1 ? 4 : 2));
         if (adj && adj_override() != 0) {
             if (items == 1) launch_k(k_pair<1, true>, amps, n, d.k, d, p, 1, st, cls);
             else if (items == 4) launch_k(k_pair<4, true>, amps, n, d.k, d, p, 4, st, cls);
