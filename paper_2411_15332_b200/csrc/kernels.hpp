@@ -90,7 +90,7 @@ struct RegOp {
     std::uint16_t ref;        // TOP_SIGN / shared-memory gates / 3-bit diagonals: index into the plan's TileOp array
     std::uint32_t lctrl_mask; // controls on tile bits (local-index mask / required value)
     std::uint32_t lctrl_val;
-    std::uint32_t pad0;
+    std::uint32_t sidx;       // TOP_SIGN: index among the pass's sign steps
     std::uint64_t gctrl_mask; // controls outside the tile (basis bits / required value)
     std::uint64_t gctrl_val;
     std::uint64_t pad1;
@@ -107,6 +107,7 @@ constexpr int kPassMaxOps = 236;
 struct PassParams {           // <= 32 KB: the kernel parameter limit
     int m;                    // tile bits (3..12)
     int nrounds;
+    int nops;
     int bits[16];             // basis-bit positions, ascending; bits[0..2] = 0, 1, 2
     RoundDesc rounds[kPassMaxOps];
     RegOp ops[kPassMaxOps];

@@ -236,7 +236,7 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                 rounds.push_back({false, t, {idx}});
             }
         }
-        int nops = 0;
+        int nops = 0, nsign = 0;
         std::uint64_t flip_off = 0, flip_cnt = 0;
         for (auto& r : rounds) {
             if (P.nrounds >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many rounds in a pass");
@@ -330,6 +330,7 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                         use_big = f.dk == 3;
                         break;
                     case TOP_SIGN:
+                        o.sidx = std::uint32_t(nsign++);
                         big.flip_off = out.flips.size();
                         big.flip_cnt = f.flips.size();
                         big.flip_rest = f.flip_rest;
@@ -352,6 +353,7 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
             }
             rd.op_count = std::uint16_t(nops - rd.op_begin);
         }
+        P.nops = nops;
         out.passes.push_back(P);
         out.pass_ops.push_back(pp.ops);
         out.single_flip_off.push_back(flip_off);

@@ -188,6 +188,11 @@ __device__ __noinline__ void smem_gate(double2* sm, const TileOp& o, int m, unsi
 constexpr int kThreads = 256;
 constexpr int kMaxBits = 12;
 
+enum : unsigned { F_GATE = 1, F_DIAG = 2, F_SIGN = 4, F_SMEM = 8 };
+
+// F: the operation kinds present in the pass (the host picks the instantiation), so a pass
+// without gates or diagonals compiles to the lean butterfly/sign kernel.
+template <unsigned F>
 __global__ void __launch_bounds__(kThreads, 2)
     k_tile(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,
            const u64* __restrict__ flipped) {
@@ -204,10 +209,24 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (j >> (b - 3) & 1) v |= u64(1) << P.bits[b];
         hi_tab[j] = v;
     }
-    u64 base = blockIdx.x;
+    u64 base = blockIdx.x, tile_mask = 0;
     for (int b = 0; b < m; ++b) {  // bits[] ascending: insert zeros from the lowest position up
         const int pos = P.bits[b];
         base = ((base >> pos) << (pos + 1)) | (base & ((u64(1) << pos) - 1));
+        tile_mask |= u64(1) << pos;
+    }
+    // sign steps whose listed indices miss this tile act uniformly (negate all or nothing):
+    // decide that once per tile (bit s = sign op s has a listed index inside the tile)
+    unsigned sign_hit = 0;
+    if (F & F_SIGN) {
+        for (int oi = 0; oi < P.nops; ++oi) {
+            const RegOp& o = P.ops[oi];
+            if (o.kind != TOP_SIGN) continue;
+            const TileOp& so = big[o.ref];
+            bool hit = so.flip_cnt > 64;  // long lists: search per element
+            for (u64 e = 0; e < so.flip_cnt && !hit; ++e) hit = (__ldg(flipped + so.flip_off + e) & ~tile_mask) == base;
+            if (hit) sign_hit |= 1u << (o.sidx & 31);
+        }
     }
     __syncthreads();
     for (unsigned j = t; j < sz; j += bt) cp_async16(sm + swz(j), a + (base | (j & 7u) | hi_tab[j >> 3]));
@@ -215,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     for (int ri = 0; ri < P.nrounds; ++ri) {
         const RoundDesc& R = P.rounds[ri];
-        if (R.smem) {
+        if ((F & F_SMEM) && R.smem) {
             for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
                 const TileOp& o = big[P.ops[oi].ref];
                 if (!(o.gctrl_mask && (base & o.gctrl_mask) != o.gctrl_val)) {
@@ -228,55 +247,74 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         const int r0 = R.r[0], r1 = R.r[1], r2 = R.r[2];
         const unsigned ro[3] = {1u << r0, 1u << r1, 1u << r2};
-        const u64 go[3] = {u64(1) << P.bits[r0], u64(1) << P.bits[r1], u64(1) << P.bits[r2]};
+        unsigned off[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) off[q] = ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u);
         for (unsigned g = t; g < ngroups; g += bt) {
             const unsigned lb = insert_zero(insert_zero(insert_zero(g, r0), r1), r2);
             double2 v[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                v[q] = sm[swz(lb | ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u))];
-            const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];  // basis index of register 0
+            for (int q = 0; q < 8; ++q) v[q] = sm[swz(lb | off[q])];
             for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
                 const RegOp& o = P.ops[oi];
                 if (o.gctrl_mask && (base & o.gctrl_mask) != o.gctrl_val) continue;
-                switch (o.kind) {
-                    case TOP_GATE:
-                        if (o.t == 0) gate1<0>(v, o, lb, ro);
-                        else if (o.t == 1) gate1<1>(v, o, lb, ro);
-                        else gate1<2>(v, o, lb, ro);
-                        break;
-                    case TOP_WHT:
-                        if (o.t & 1) butterfly<0>(v);
-                        if (o.t & 2) butterfly<1>(v);
-                        if (o.t & 4) butterfly<2>(v);
-                        break;
-                    case TOP_SCALE: {
-                        const double s = o.c[0].x;
+                const int kind = o.kind;
+                if (kind == TOP_WHT) {
+                    const int tm = o.t;
+                    if (tm & 1) butterfly<0>(v);
+                    if (tm & 2) butterfly<1>(v);
+                    if (tm & 4) butterfly<2>(v);
+                } else if (kind == TOP_SCALE) {
+                    const double sc = o.c[0].x;
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) v[q] = make_double2(v[q].x * s, v[q].y * s);
-                        break;
-                    }
-                    case TOP_DIAG: diag_op(v, o, big, g0); break;
-                    case TOP_SIGN: {
-                        const TileOp& so = big[o.ref];
+                    for (int q = 0; q < 8; ++q) v[q] = make_double2(v[q].x * sc, v[q].y * sc);
+                } else if ((F & F_GATE) && kind == TOP_GATE) {
+                    if (o.t == 0) gate1<0>(v, o, lb, ro);
+                    else if (o.t == 1) gate1<1>(v, o, lb, ro);
+                    else gate1<2>(v, o, lb, ro);
+                } else if ((F & F_DIAG) && kind == TOP_DIAG) {
+                    diag_op(v, o, big, base | (lb & 7u) | hi_tab[lb >> 3]);
+                } else if ((F & F_SIGN) && kind == TOP_SIGN) {
+                    const TileOp& so = big[o.ref];
+                    if (!(sign_hit >> (o.sidx & 31) & 1)) {
+                        if (so.flip_rest) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) v[q] = neg_exact(v[q]);
+                        }
+                    } else {
                         const u64* f = flipped + so.flip_off;
+                        const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            const u64 gi = g0 | ((q & 1) ? go[0] : 0) | ((q & 2) ? go[1] : 0) | ((q & 4) ? go[2] : 0);
+                            const unsigned j = lb | off[q];
+                            const u64 gi = base | (j & 7u) | hi_tab[j >> 3];
+                            (void)g0;
                             if (listed(f, so.flip_cnt, gi) != (so.flip_rest != 0)) v[q] = neg_exact(v[q]);
                         }
-                        break;
                     }
-                    default: break;
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                sm[swz(lb | ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u))] = v[q];
+            for (int q = 0; q < 8; ++q) sm[swz(lb | off[q])] = v[q];
         }
         __syncthreads();
     }
     for (unsigned j = t; j < sz; j += bt) __stcs(a + (base | (j & 7u) | hi_tab[j >> 3]), sm[swz(j)]);
+}
+
+template <unsigned F>
+void launch_f(double2* amps, const PassParams& p, const TileOp* big_dev, const std::uint64_t* flipped_dev, unsigned tiles,
+              int threads, std::size_t smem, cudaStream_t st) {
+    static bool attr_set[64] = {};  // per device and instantiation
+    int dev = 0;
+    QCS_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && !attr_set[dev]) {
+        const int max_smem = (1 << kMaxBits) * 16 + (1 << (kMaxBits - 3)) * 8;
+        QCS_CUDA(cudaFuncSetAttribute(k_tile<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+        QCS_CUDA(cudaFuncSetAttribute(k_tile<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attr_set[dev] = true;
+    }
+    k_tile<F><<<tiles, threads, smem, st>>>(amps, p, big_dev, flipped_dev);
 }
 
 }  // namespace
@@ -287,20 +325,27 @@ void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* b
                       cudaStream_t st) {
     if (p.m < 3 || p.m > kMaxBits || p.m > n) raise(QCS_ERR_ARG, "tile bits out of range");
     const std::size_t smem = (std::size_t(1) << p.m) * sizeof(double2) + (std::size_t(1) << (p.m - 3)) * sizeof(u64);
-    static bool attr_set[64] = {};  // per device
-    int dev = 0;
-    QCS_CUDA(cudaGetDevice(&dev));
-    if (dev < 64 && !attr_set[dev]) {
-        const int max_smem = (1 << kMaxBits) * 16 + (1 << (kMaxBits - 3)) * 8;
-        QCS_CUDA(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-        QCS_CUDA(cudaFuncSetAttribute(k_tile, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        attr_set[dev] = true;
-    }
     const u64 tiles = u64(1) << (n - p.m);
     if (tiles > 0x7fffffffull) raise(QCS_ERR_CAPACITY, "too many tiles for one launch");
     const int threads = std::min(kThreads, std::max(32, 1 << (p.m - 3)));
+    unsigned f = 0;
+    for (int r = 0; r < p.nrounds; ++r)
+        if (p.rounds[r].smem) f |= F_SMEM;
+    for (int i = 0; i < p.nops; ++i) {
+        if (p.ops[i].kind == TOP_GATE) f |= F_GATE;
+        if (p.ops[i].kind == TOP_DIAG) f |= F_DIAG;
+        if (p.ops[i].kind == TOP_SIGN) f |= F_SIGN;
+    }
     TimedLaunch tl("tile_pass", 32.0 * double(u64(1) << n), st);
-    k_tile<<<unsigned(tiles), threads, smem, st>>>(amps, p, big_dev, flipped_dev);
+    switch (f) {
+#define QCS_TILE_CASE(x) \
+    case x: launch_f<x>(amps, p, big_dev, flipped_dev, unsigned(tiles), threads, smem, st); break;
+        QCS_TILE_CASE(0) QCS_TILE_CASE(1) QCS_TILE_CASE(2) QCS_TILE_CASE(3) QCS_TILE_CASE(4) QCS_TILE_CASE(5)
+        QCS_TILE_CASE(6) QCS_TILE_CASE(7) QCS_TILE_CASE(8) QCS_TILE_CASE(9) QCS_TILE_CASE(10) QCS_TILE_CASE(11)
+        QCS_TILE_CASE(12) QCS_TILE_CASE(13) QCS_TILE_CASE(14) QCS_TILE_CASE(15)
+#undef QCS_TILE_CASE
+        default: break;
+    }
     check_launch("k_tile");
 }
 
