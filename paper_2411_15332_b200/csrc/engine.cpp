@@ -435,7 +435,10 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
         if (!o.fuse) run_fused(s, ops);  // one step: fused only within the step
         if (reports) reports[i] = r;
     }
-    if (o.fuse) run_fused(s, ops);
+    if (o.fuse) {
+        merge_single_qubit(n, ops);
+        run_fused(s, ops);
+    }
 }
 
 void memory_report(int n, const qcs_step* steps, int nsteps, int engine, qcs_step_report* reports) {

@@ -139,7 +139,54 @@ namespace {
 
 bool elementwise(const FOp& f) { return f.kind == TOP_DIAG || f.kind == TOP_SIGN || f.kind == TOP_SCALE; }
 
+// one uncontrolled single-qubit gate or one-bit diagonal: returns its basis bit, else -1
+int single_qubit_bit(const FOp& f) {
+    if (f.src.k != 1) return -1;
+    if (f.kind == TOP_GATE && f.K == 1 && f.ctrl_mask == 0) return f.tpos[0];
+    if (f.kind == TOP_DIAG && f.dk == 1) return f.dpos[0];
+    return -1;
+}
+
 }  // namespace
+
+// Gate fusion for fused passes: a run of single-qubit operations on the same qubit, with no
+// operation touching that qubit in between, becomes one 2x2 -- their product (later * earlier).
+// Halves the FP64 work of layers like C4's RY-then-RZ; an identity product disappears.
+void merge_single_qubit(int n, std::vector<FOp>& ops) {
+    std::vector<int> open(std::size_t(n), -1);  // index in `out` of the chain head on each bit
+    std::vector<FOp> out;
+    out.reserve(ops.size());
+    for (FOp& f : ops) {
+        const int bit = single_qubit_bit(f);
+        if (bit >= 0 && open[std::size_t(bit)] >= 0) {
+            FOp& head = out[std::size_t(open[std::size_t(bit)])];
+            GateOp g;
+            g.k = 1;
+            g.pos[0] = bit;
+            g.m.resize(4);
+            for (int r = 0; r < 2; ++r)
+                for (int c = 0; c < 2; ++c)
+                    g.m[std::size_t(r * 2 + c)] =
+                        f.src.m[std::size_t(r * 2)] * head.src.m[std::size_t(c)] +
+                        f.src.m[std::size_t(r * 2 + 1)] * head.src.m[std::size_t(2 + c)];
+            FOp merged;
+            if (make_fop(g, merged)) {
+                head = std::move(merged);
+            } else {  // the product is the identity
+                head.kind = -1;
+                open[std::size_t(bit)] = -1;
+            }
+            continue;
+        }
+        for (int b = 0; b < n; ++b)
+            if (f.touch >> b & 1) open[std::size_t(b)] = -1;
+        out.push_back(std::move(f));
+        if (bit >= 0) open[std::size_t(bit)] = int(out.size()) - 1;
+    }
+    ops.clear();
+    for (FOp& f : out)
+        if (f.kind >= 0) ops.push_back(std::move(f));
+}
 
 Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
     Plan plan;

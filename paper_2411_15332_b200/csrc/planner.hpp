@@ -52,6 +52,7 @@ struct Plan {
     std::vector<PlannedPass> passes;
 };
 Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits);
+void merge_single_qubit(int n, std::vector<FOp>& ops);
 
 struct Lowered {
     std::vector<PassParams> passes;
