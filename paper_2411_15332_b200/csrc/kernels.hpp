@@ -93,7 +93,9 @@ struct RegOp {
     std::uint32_t sidx;       // TOP_SIGN: index among the pass's sign steps
     std::uint64_t gctrl_mask; // controls outside the tile (basis bits / required value)
     std::uint64_t gctrl_val;
-    std::uint64_t pad1;
+    std::uint16_t dtab;       // TOP_DIAG (dk <= 2): register part of the entry index for q = 0..7, 2 bits each
+    std::uint16_t fast;       // TOP_GATE: dense 2x2 without tile-local controls
+    std::uint32_t pad1;
     double2 c[4];             // TOP_GATE: a0, b0, a1, b1; TOP_DIAG: entries; TOP_SCALE: c[0].x
 };
 

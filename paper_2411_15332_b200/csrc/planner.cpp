@@ -351,6 +351,7 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                                     o.c[3] = b2;
                                 }
                             }
+                            o.fast = std::uint16_t(o.rk0 == 2 && o.rk1 == 2 && o.lctrl_mask == 0);
                         }
                         break;
                     case TOP_WHT: {  // a run of single-bit butterflies becomes one masked op
@@ -368,6 +369,12 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                             o.dpos[i] = std::uint8_t(f.dpos[i]);
                             const int rb = loc[f.dpos[i]] >= 0 ? reg(f.dpos[i]) : -1;
                             o.dreg[i] = rb >= 0 ? std::uint8_t(rb) : 0xff;
+                        }
+                        for (int q = 0; q < 8 && f.dk <= 2; ++q) {  // register part of the entry index
+                            unsigned rp = 0;
+                            for (int i = 0; i < f.dk; ++i)
+                                if (o.dreg[i] < 3) rp |= ((unsigned(q) >> o.dreg[i]) & 1u) << (f.dk - 1 - i);
+                            o.dtab = std::uint16_t(o.dtab | (rp << (2 * q)));
                         }
                         for (int g = 0; g < (1 << f.dk); ++g) {
                             if (f.dskip[g]) o.dskip = std::uint8_t(o.dskip | (1u << g));

@@ -88,8 +88,18 @@ __device__ __forceinline__ double2 gate_row(int rk, int rc, double2 a, double2 b
 
 template <int T>
 __device__ __forceinline__ void gate1(double2 (&v)[8], const RegOp& o, unsigned lb, const unsigned (&ro)[3]) {
-    const int rk0 = o.rk0, rk1 = o.rk1, rc0 = o.rc0, rc1 = o.rc1;
     const double2 a0 = o.c[0], b0 = o.c[1], a1 = o.c[2], b1 = o.c[3];
+    if (o.fast) {  // dense 2x2, no tile-local control: straight-line
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q & (1 << T)) continue;
+            const double2 x0 = v[q], x1 = v[q | (1 << T)];
+            v[q] = cmul2_f(a0, x0, b0, x1);
+            v[q | (1 << T)] = cmul2_f(a1, x0, b1, x1);
+        }
+        return;
+    }
+    const int rk0 = o.rk0, rk1 = o.rk1, rc0 = o.rc0, rc1 = o.rc1;
     const unsigned cm = o.lctrl_mask, cv = o.lctrl_val;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -119,6 +129,24 @@ __device__ __forceinline__ void butterfly(double2 (&v)[8]) {
 // q, the others are constant over the thread's group (taken from the group's first element).
 __device__ __forceinline__ void diag_op(double2 (&v)[8], const RegOp& o, const TileOp* big, u64 g0) {
     const int dk = o.dk;
+    if (dk <= 2) {  // the host tabulated the register part of g for every q (2 bits each)
+        int cg = 0;
+        if (o.dreg[0] == 0xff && dk >= 1) cg |= int((g0 >> o.dpos[0]) & 1) << (dk - 1);
+        if (dk == 2 && o.dreg[1] == 0xff) cg |= int((g0 >> o.dpos[1]) & 1);
+        const unsigned tab = o.dtab, skip = o.dskip;
+        const double2 c0 = o.c[0], c1 = o.c[1], c2 = o.c[2], c3 = o.c[3];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int g = cg | int((tab >> (2 * q)) & 3u);
+            double2 d = c0;
+            if (g == 1) d = c1;
+            if (g == 2) d = c2;
+            if (g == 3) d = c3;
+            const double2 r = cmul_f(d, v[q]);
+            if (!(skip >> g & 1)) v[q] = r;
+        }
+        return;
+    }
     int cg = 0;
     int regbit[3] = {-1, -1, -1};
 #pragma unroll
