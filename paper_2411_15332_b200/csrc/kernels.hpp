@@ -77,9 +77,14 @@ struct TileOp {
     std::uint8_t dskip[8];       // TOP_DIAG: entry g is exactly 1 (left untouched)
 };
 
+// RegOp::kind flags above the kind bits
+constexpr int KF_KIND = 0x0f;
+constexpr int KF_SIGNED = 0x40;  // TOP_DIAG with entries in {+1, -1}: dskip holds the -1 entries
+constexpr int KF_GCTRL = 0x80;   // has controls outside the tile (gctrl_mask / gctrl_val)
+
 // Compact register-round operation; a pass's list travels in the kernel parameter space.
 struct RegOp {
-    std::uint8_t kind;        // TOP_GATE (one target), TOP_DIAG, TOP_SIGN, TOP_WHT, TOP_SCALE
+    std::uint8_t kind;        // TOP_GATE (one target), TOP_DIAG, TOP_SIGN, TOP_WHT, TOP_SCALE | KF_* flags
     std::uint8_t t;           // TOP_GATE: target register bit; TOP_WHT: register-bit mask
     std::uint8_t rk0, rk1;    // TOP_GATE: row kind (0 untouched, 1 one product, 2 two products)
     std::uint8_t rc0, rc1;    // TOP_GATE: column of a single-product row

@@ -403,6 +403,20 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                     o.ref = std::uint16_t(out.big.size());
                     out.big.push_back(big);
                 }
+                if (o.gctrl_mask) o.kind = std::uint8_t(o.kind | KF_GCTRL);
+                if (f.kind == TOP_DIAG && f.dk <= 2) {  // +-1 diagonals (Z, CZ, sign parts): sign flips
+                    bool signed_only = true;
+                    unsigned neg = 0;
+                    for (int g = 0; g < (1 << f.dk); ++g) {
+                        const double2 d = f.dval[g];
+                        if (d.y != 0.0 || (d.x != 1.0 && d.x != -1.0)) signed_only = false;
+                        if (d.x == -1.0) neg |= 1u << g;
+                    }
+                    if (signed_only) {
+                        o.kind = std::uint8_t(o.kind | KF_SIGNED);
+                        o.dskip = std::uint8_t(neg);
+                    }
+                }
                 P.ops[nops++] = o;
             }
             rd.op_count = std::uint16_t(nops - rd.op_begin);

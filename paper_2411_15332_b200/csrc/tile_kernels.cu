@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (F & F_SIGN) {
         for (int oi = 0; oi < P.nops; ++oi) {
             const RegOp& o = P.ops[oi];
-            if (o.kind != TOP_SIGN) continue;
+            if ((o.kind & KF_KIND) != TOP_SIGN) continue;
             const TileOp& so = big[o.ref];
             bool hit = so.flip_cnt > 64;  // long lists: search per element
             for (u64 e = 0; e < so.flip_cnt && !hit; ++e) hit = (__ldg(flipped + so.flip_off + e) & ~tile_mask) == base;
@@ -305,8 +305,21 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int q = 0; q < 8; ++q) v[q] = sm[swz(lb | off[q])];
             for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
                 const RegOp& o = P.ops[oi];
-                if (o.gctrl_mask && (base & o.gctrl_mask) != o.gctrl_val) continue;
-                const int kind = o.kind;
+                const int kb = o.kind;  // low bits: kind; KF_GCTRL: controls outside the tile
+                if ((kb & KF_GCTRL) && (base & o.gctrl_mask) != o.gctrl_val) continue;
+                const int kind = kb & KF_KIND;
+                if ((F & F_DIAG) && (kb & KF_SIGNED)) {  // diagonal of +-1 entries: exact sign flips
+                    const unsigned tab = o.dtab, neg = o.dskip;
+                    int cg = 0;
+                    if (o.dreg[0] == 0xff) cg |= int(((base | (lb & 7u) | hi_tab[lb >> 3]) >> o.dpos[0]) & 1) << (o.dk - 1);
+                    if (o.dk == 2 && o.dreg[1] == 0xff) cg |= int(((base | (lb & 7u) | hi_tab[lb >> 3]) >> o.dpos[1]) & 1);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int g = cg | int((tab >> (2 * q)) & 3u);
+                        if (neg >> g & 1) v[q] = make_double2(-v[q].x, -v[q].y);
+                    }
+                    continue;
+                }
                 if (kind == TOP_WHT) {
                     const int tm = o.t;
                     if (tm & 1) butterfly<0>(v);
@@ -380,9 +393,10 @@ void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* b
     for (int r = 0; r < p.nrounds; ++r)
         if (p.rounds[r].smem) f |= F_SMEM;
     for (int i = 0; i < p.nops; ++i) {
-        if (p.ops[i].kind == TOP_GATE) f |= F_GATE;
-        if (p.ops[i].kind == TOP_DIAG) f |= F_DIAG;
-        if (p.ops[i].kind == TOP_SIGN) f |= F_SIGN;
+        const int kind = p.ops[i].kind & KF_KIND;
+        if (kind == TOP_GATE) f |= F_GATE;
+        if (kind == TOP_DIAG) f |= F_DIAG;
+        if (kind == TOP_SIGN) f |= F_SIGN;
     }
     TimedLaunch tl("tile_pass", 32.0 * double(u64(1) << n), st);
     switch (f) {
