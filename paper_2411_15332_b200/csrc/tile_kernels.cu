@@ -241,7 +241,9 @@ enum : unsigned { F_GATE = 1, F_DIAG = 2, F_SIGN = 4, F_SMEM = 8 };
 // F: the operation kinds present in the pass (the host picks the instantiation), so a pass
 // without gates or diagonals compiles to the lean butterfly/sign kernel.
 template <unsigned F>
-__global__ void __launch_bounds__(kThreads, 2)
+// butterfly / sign-only passes are lean enough for 3 resident tiles per SM (the smem limit);
+// passes with gates or diagonals need the registers of 2
+__global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG | F_SMEM)) ? 2 : 3)
     k_tile(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,
            const u64* __restrict__ flipped) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
