@@ -1,0 +1,137 @@
+"""Test-side pieces for the partitioner: a CPU shard backend (the oracle does the local compute:
+tests may use it) and an in-process transport that lets P threads stand in for P ranks."""
+import threading
+
+import numpy as np
+import torch
+
+
+class OracleBackend:
+    """Local shard as a CPU complex128 tensor; local steps through the C oracle."""
+
+    def __init__(self, n_local, oracle):
+        self.n = n_local
+        self.O = oracle
+        self.tensor = torch.zeros(1 << n_local, dtype=torch.complex128)
+
+    def set_basis(self, index):
+        self.tensor.zero_()
+        if index is not None:
+            self.tensor[index] = 1.0
+
+    def _set(self, arr):
+        self.tensor.copy_(torch.from_numpy(arr))
+
+    def apply(self, matrix, local_qubits, name="custom"):
+        self._set(self.O.apply_step(self.n, [(list(local_qubits), np.asarray(matrix))], self.tensor.numpy()))
+
+    def apply_diag(self, flipped, flip_rest):
+        self._set(self.O.apply_diag(self.n, flipped, flip_rest, self.tensor.numpy()))
+
+    def apply_rh(self):
+        self._set(self.O.wht(self.n, self.tensor.numpy()))
+
+    def chunk(self, upper, start, count):
+        base = (1 << (self.n - 1)) if upper else 0
+        return self.tensor[base + start: base + start + count]
+
+    def empty(self, count):
+        return torch.empty(count, dtype=torch.complex128)
+
+    def sync(self):
+        pass
+
+    def numpy(self):
+        return self.tensor.numpy().copy()
+
+
+class ThreadTransport:
+    """P threads in one process exchanging through mailboxes (an emulated fabric)."""
+
+    def __init__(self):
+        self.cv = threading.Condition()
+        self.box = {}
+
+    def endpoint(self, rank):
+        return _Endpoint(self, rank)
+
+
+class _Endpoint:
+    def __init__(self, hub, rank):
+        self.hub, self.rank = hub, rank
+
+    def exchange(self, send, recv, peer):
+        with self.hub.cv:  # per-(source, destination) FIFO: messages are matched in order
+            self.hub.box.setdefault((self.rank, peer), []).append(send.clone())
+            self.hub.cv.notify_all()
+            while not self.hub.box.get((peer, self.rank)):
+                self.hub.cv.wait()
+            data = self.hub.box[(peer, self.rank)].pop(0)
+        recv.copy_(data)
+
+
+def run_ranks(world, fn):
+    """Run fn(rank) in `world` threads; re-raise the first failure."""
+    errs, outs = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            outs[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            errs[r] = e
+
+    ths = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    return outs
+
+
+def gather(states, parts):
+    """Assemble the logical state from every rank's (ShardedState, local amplitudes)."""
+    n = states[0].n
+    full = np.zeros(1 << n, dtype=np.complex128)
+    for st, loc in zip(states, parts):
+        full[st.logical_amplitude_map()] = loc
+    return full
+
+
+def circuit_ops(circuit):
+    """Circuit -> flat op list for ShardedState: ('gate', m, qubits, name) / ('diag', f, r) / ('rh',)."""
+    ops = []
+    for st in circuit.steps:
+        if int(st.kind) == 1:
+            ops.append(("diag", list(st.diag.flipped), st.diag.flip_rest))
+        elif st.is_hadamard_all(circuit.n):
+            ops.append(("rh",))
+        else:
+            for p in st.placements:
+                ops.append(("gate", p.gate.matrix, p.qubit_list(), p.gate.name))
+    return ops
+
+
+def run_ops(state, ops):
+    for op in ops:
+        if op[0] == "gate":
+            state.apply_gate(op[1], op[2], op[3])
+        elif op[0] == "diag":
+            state.apply_diag(op[1], op[2])
+        else:
+            state.apply_rh()
+
+
+def oracle_full(oracle, circuit):
+    x = np.zeros(1 << circuit.n, dtype=np.complex128)
+    x[circuit.initial] = 1
+    for st in circuit.steps:
+        if int(st.kind) == 1:
+            x = oracle.apply_diag(circuit.n, st.diag.flipped, st.diag.flip_rest, x)
+        elif st.is_hadamard_all(circuit.n):
+            x = oracle.wht(circuit.n, x)
+        else:
+            x = oracle.apply_step(circuit.n, [(p.qubit_list(), p.gate.matrix) for p in st.placements], x)
+    return x

@@ -1,0 +1,128 @@
+"""Multi-rank partitioner (paper_2411_15332_b200/partition.py) on the CPU.
+
+* world 2 and 4 with torch.distributed over gloo (separate processes, 127.0.0.1), the shard
+  compute done by the C oracle: the exchange / remap / reduction logic is what is under test;
+* P threads in one process with an in-process transport (many layouts quickly).
+Reference results: the oracle on the full state ("P-GPU versus 1-GPU
+equality on the same circuit")."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+from partition_helpers import (OracleBackend, ThreadTransport, circuit_ops, gather, oracle_full, run_ops,
+                               run_ranks)
+
+
+def circuits():
+    from paper_2411_15332_b200 import configs
+    from paper_2411_15332_b200 import qcsim as Q
+    return {
+        "c4": configs.c4_circuit(n=8, layers=2),
+        "c5": configs.c5_circuit(n=9, layers=2, global_qubits=2),
+        "grover": Q.build_grover(7, 77, 3),
+        "c1": configs.c1_circuit(n=6, layers=1),
+    }
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name", ["c4", "c5", "grover", "c1"])
+def test_threads_match_full_state(oracle, world, name):
+    from paper_2411_15332_b200.partition import ShardedState
+    c = circuits()[name]
+    want = oracle_full(oracle, c)
+    hub = ThreadTransport()
+    g = world.bit_length() - 1
+
+    def rank_fn(r):
+        st = ShardedState(c.n, world, r, OracleBackend(c.n - g, oracle), hub.endpoint(r), initial=c.initial,
+                          chunk_elems=7)
+        run_ops(st, circuit_ops(c))
+        return st, st.local_numpy()
+
+    outs = run_ranks(world, rank_fn)
+    got = gather([o[0] for o in outs], [o[1] for o in outs])
+    assert np.abs(got - want).max() < 1e-12
+    assert sum(o[0].swaps for o in outs) > 0 or name == "c1" and world == 2
+
+
+def test_global_controls_and_diagonals_need_no_exchange(oracle):
+    from paper_2411_15332_b200 import qcsim as Q
+    from paper_2411_15332_b200.partition import ShardedState
+    n, world = 6, 4
+    c = Q.Circuit(n, [Q.hadamard_all(n),
+                      Q.CircuitStep.of_gates([Q.Placement(Q.gate_catalog_lookup("CZ"), qubits=[0, 4])]),
+                      Q.CircuitStep.of_gates([Q.Placement(Q.gate_catalog_lookup("CNOT"), qubits=[1, 5])]),
+                      Q.CircuitStep.of_gates([Q.Placement(Q.gate_catalog_lookup("RZ", [0.7]), 0)]),
+                      Q.CircuitStep.of_gates([Q.Placement(Q.gate_catalog_lookup("Toffoli"), qubits=[0, 1, 3])]),
+                      Q.CircuitStep.of_diag(Q.DiagSign([5, 40], False))])
+    want = oracle_full(oracle, c)
+    hub = ThreadTransport()
+    ops = circuit_ops(c)
+    ops[0] = ("rh_local_only",)
+
+    def rank_fn(r):
+        st = ShardedState(n, world, r, OracleBackend(n - 2, oracle), hub.endpoint(r))
+        # H on all qubits without moving qubits: local WHT + H on the two global qubits would
+        # swap, so prepare the uniform state by hand instead
+        st.backend.tensor.fill_(1.0 / np.sqrt(2 ** n))
+        run_ops(st, ops[1:])
+        return st, st.local_numpy()
+
+    outs = run_ranks(world, rank_fn)
+    assert all(o[0].swaps == 0 for o in outs)
+    assert np.abs(gather([o[0] for o in outs], [o[1] for o in outs]) - want).max() < 1e-12
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, name, result_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle_py import Oracle
+    from paper_2411_15332_b200.partition import DistTransport, ShardedState
+    Oracle.lib()
+    c = circuits()[name]
+    g = world.bit_length() - 1
+    st = ShardedState(c.n, world, rank, OracleBackend(c.n - g, Oracle), DistTransport(), initial=c.initial,
+                      chunk_elems=5)
+    run_ops(st, circuit_ops(c))
+    loc = torch.from_numpy(st.local_numpy())
+    amap = torch.from_numpy(st.logical_amplitude_map())
+    if rank == 0:
+        locs = [torch.zeros_like(loc) for _ in range(world)]
+        maps = [torch.zeros_like(amap) for _ in range(world)]
+    else:
+        locs = maps = None
+    dist.gather(torch.view_as_real(loc), [torch.view_as_real(x) for x in locs] if locs else None, dst=0)
+    dist.gather(amap, maps, dst=0)
+    if rank == 0:
+        full = np.zeros(1 << c.n, dtype=np.complex128)
+        for lo, mp_ in zip(locs, maps):
+            full[mp_.numpy()] = lo.numpy()
+        np.save(result_path, full)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,name", [(2, "c5"), (4, "c4"), (2, "grover")])
+def test_gloo_ranks_match_full_state(oracle, tmp_path, world, name):
+    path = str(tmp_path / "full.npy")
+    mp.start_processes(_gloo_worker, args=(world, _free_port(), name, path), nprocs=world, join=True,
+                       start_method="spawn")
+    want = oracle_full(oracle, circuits()[name])
+    assert np.abs(np.load(path) - want).max() < 1e-12

@@ -1,0 +1,34 @@
+"""The partitioner with real B200 kernels: P ranks emulated by P threads on one GPU, each with
+its own device shard (DeviceBackend: a torch tensor wrapped by qcs_state_wrap) and an
+in-process transport for the pairwise half-shard exchanges.  Compared with the single-GPU
+engine (qcsim.simulate) on the same circuits ('a fake partition running
+P shards on one GPU, which exercises the exchange logic without NVLink')."""
+import numpy as np
+import pytest
+
+from partition_helpers import ThreadTransport, circuit_ops, gather, run_ops, run_ranks
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_emulated_ranks_match_single_gpu(world):
+    from paper_2411_15332_b200 import configs
+    from paper_2411_15332_b200 import qcsim as Q
+    from paper_2411_15332_b200.partition import DeviceBackend, ShardedState
+    g = world.bit_length() - 1
+    for c in (configs.c4_circuit(n=16, layers=2), configs.c5_circuit(n=17, layers=2, global_qubits=g)):
+        want = Q.simulate(c, Q.Engine.rh_dax).final.download()
+        hub = ThreadTransport()
+
+        def rank_fn(r):
+            st = ShardedState(c.n, world, r, DeviceBackend(c.n - g), hub.endpoint(r), initial=c.initial,
+                              chunk_elems=1 << 12)
+            run_ops(st, circuit_ops(c))
+            return st, st.local_numpy()
+
+        outs = run_ranks(world, rank_fn)
+        got = gather([o[0] for o in outs], [o[1] for o in outs])
+        assert np.abs(got - want).max() < 1e-12
+        assert np.linalg.norm(got - want) < 1e-10
+        assert all(o[0].swaps > 0 for o in outs)
