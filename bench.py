@@ -330,6 +330,88 @@ def run_b200_arm(args, rank, world, local_rank):
     return 0
 
 
+def run_circuit_arm(args, rank, world, local_rank):
+    """Whole BASELINE circuits (C1, C3, C4, C5) through the fused engine.  World 1: qcsim.simulate
+    on one device state.  World > 1: the state sharded over the ranks by its top log2(world)
+    qubits (paper_2411_15332_b200/partition.py), half-shard exchanges over NCCL ("strong" scaling:
+    the circuit is fixed)."""
+    import torch
+    from paper_2411_15332_b200 import configs
+    from paper_2411_15332_b200 import qcsim as Q
+    w = args.workload
+    n = args.n_circuit
+    build = {"c1": lambda: configs.c1_circuit(n or 12), "c3": lambda: configs.c3_circuit(n or 30),
+             "c4": lambda: configs.c4_circuit(n or 32), "c5": lambda: configs.c5_circuit(n or 35)}[w]
+    c = build()
+    updates = {"c1": configs.c1_updates(c.n), "c3": configs.c3_updates(c.n), "c4": configs.c4_updates(c.n),
+               "c5": configs.c5_updates(c.n)}[w]
+    dist = Dist(world, local_rank)
+    dev = local_rank if world > 1 else 0
+    torch.cuda.set_device(dev)
+    if world == 1:
+        state = Q.DeviceState(c.n, c.initial, dev)
+
+        def step():
+            Q.simulate(c, Q.Engine.rh_dax, state=state)
+        sync = state.sync
+    else:
+        from paper_2411_15332_b200.partition import DeviceBackend, DistTransport, ShardedState
+        g = world.bit_length() - 1
+        backend = DeviceBackend(c.n - g, dev)
+        sh = ShardedState(c.n, world, rank, backend, DistTransport(), initial=c.initial)
+        ops = []
+        for st in c.steps:
+            if int(st.kind) == 1:
+                ops.append(("diag", list(st.diag.flipped), st.diag.flip_rest))
+            elif st.is_hadamard_all(c.n):
+                ops.append(("rh",))
+            else:
+                ops += [("gate", p.gate.matrix, p.qubit_list(), p.gate.name) for p in st.placements]
+
+        def step():
+            sh.phys = list(range(c.n))
+            sh.set_basis(c.initial)
+            for op in ops:
+                if op[0] == "gate":
+                    sh.apply_gate(op[1], op[2], op[3])
+                elif op[0] == "diag":
+                    sh.apply_diag(op[1], op[2])
+                else:
+                    sh.apply_rh()
+            sh.flush()
+
+        def sync():
+            torch.cuda.synchronize(dev)
+    for _ in range(args.warmup):
+        step()
+    sync()
+    dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        sync()
+        ev1.record()
+        ev1.synchronize()
+    ms = dist.max(ev0.elapsed_time(ev1))
+    value = updates * args.steps / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "c128 (f64 complex)",
+            "data": "synthetic", "config": {"workload": f"{w.upper()} circuit, n={c.n}", "n_qubits": c.n,
+                                            "amplitude_updates_per_step": updates,
+                                            "parallelism": f"sharded over {world} ranks (top qubits)" if world > 1
+                                            else "single GPU, fused passes"},
+            "clocks": clocks.summary()}
+    if world > 1:
+        line["exchanges_per_step"] = sh.swaps / (args.steps + args.warmup)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -337,11 +419,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=28)
+    ap.add_argument("--workload", default="c2", choices=["c2", "c1", "c3", "c4", "c5"],
+                    help="c2 (default): the single-gate sweep; c1/c3/c4/c5: whole BASELINE circuits")
+    ap.add_argument("--n-circuit", type=int, default=0, help="qubits for c1/c3/c4/c5 (default: BASELINE size)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank, world, local_rank = dist_env()
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
+    if args.workload != "c2":
+        return run_circuit_arm(args, rank, world, local_rank)
     return run_b200_arm(args, rank, world, local_rank)
 
 

@@ -66,6 +66,20 @@ class DeviceBackend:
     def apply_rh(self) -> None:
         self.state.apply_rh()
 
+    def run(self, ops) -> None:
+        """Apply a batch of local operations with one fused qcs_simulate call."""
+        Q = self.Q
+        steps = []
+        for op in ops:
+            if op[0] == "gate":
+                steps.append(Q.CircuitStep.of_gates([Q.Placement(Q.custom_gate(op[1], op[3]), qubits=list(op[2]))]))
+            elif op[0] == "diag":
+                steps.append(Q.CircuitStep.of_diag(Q.DiagSign(list(op[1]), op[2])))
+            else:
+                steps.append(Q.hadamard_all(self.n))
+        if steps:
+            Q.run(Q.Circuit(self.n, steps), self.state, Q.Engine.rh_dax)
+
     def half(self, upper: bool):
         h = 1 << (self.n - 1)
         return self.tensor[h:] if upper else self.tensor[:h]
@@ -118,6 +132,7 @@ class ShardedState:
         self.phys = list(range(n))  # phys[logical qubit] = physical qubit
         self.swaps = 0              # global<->local exchanges performed
         self.exchanged_bytes = 0    # bytes sent by this rank
+        self.pending = []           # local operations not yet handed to the backend
         self.set_basis(initial)
 
     # ------------------------------------------------------------ index mapping
@@ -137,7 +152,28 @@ class ShardedState:
         """Value of global physical qubit `phys_qubit` (< g) on this rank."""
         return (self.rank >> (self.g - 1 - phys_qubit)) & 1
 
+    # ------------------------------------------------------------ local work, batched
+    def _local(self, op) -> None:
+        self.pending.append(op)
+
+    def flush(self) -> None:
+        """Hand the pending local operations to the backend (one fused launch sequence)."""
+        if not self.pending:
+            return
+        ops, self.pending = self.pending, []
+        if hasattr(self.backend, "run"):
+            self.backend.run(ops)
+            return
+        for op in ops:
+            if op[0] == "gate":
+                self.backend.apply(op[1], op[2], op[3])
+            elif op[0] == "diag":
+                self.backend.apply_diag(op[1], op[2])
+            else:
+                self.backend.apply_rh()
+
     def set_basis(self, logical_index: int) -> None:
+        self.pending = []
         owner, local = self._owner(self._to_phys_index(logical_index))
         self.backend.set_basis(local if owner == self.rank else None)
 
@@ -147,6 +183,7 @@ class ShardedState:
         ranks r and r ^ bit exchange their halves whose top local bit differs from their own
         global bit; the amplitude (global = a, local = b) moves to (global = b, local = a)."""
         assert gq < self.g and lq == self.g
+        self.flush()
         if self.world > 1:
             a = self._rank_bit(gq)
             peer = self.rank ^ (1 << (self.g - 1 - gq))
@@ -184,12 +221,12 @@ class ShardedState:
                 if not loc:  # all qubits global: a scalar phase on this rank's shard
                     d = m[want, want]
                     if d != 1:
-                        self.backend.apply(np.array([[d, 0], [0, d]]), [0], name)  # phase on any qubit
+                        self._local(("gate", np.array([[d, 0], [0, d]]), [0], name))  # phase on any qubit
                     return
                 sel = [want | sum(((j >> (len(loc) - 1 - t)) & 1) << (k - 1 - loc[t]) for t in range(len(loc)))
                        for j in range(1 << len(loc))]
                 sub = m[np.ix_(sel, sel)]
-                self.backend.apply(sub, [phys[i] - self.g for i in loc], name)
+                self._local(("gate", sub, [phys[i] - self.g for i in loc], name))
                 return
             # bring each mixing global qubit local (swap with the top local qubit, which must
             # not be one of this gate's own qubits: move it aside first if needed)
@@ -205,11 +242,11 @@ class ShardedState:
                     self._local_swap(top, free)
                 self._swap_global_local(self.phys[logical_qubits[i]], top)
             phys = [self.phys[q] for q in logical_qubits]
-        self.backend.apply(m, [p - self.g for p in phys], name)
+        self._local(("gate", m, [p - self.g for p in phys], name))
 
     def _local_swap(self, pa: int, pb: int) -> None:
         swap = np.eye(4, dtype=np.complex128)[[0, 2, 1, 3]]
-        self.backend.apply(swap, [pa - self.g, pb - self.g], "Swap")
+        self._local(("gate", swap, [pa - self.g, pb - self.g], "Swap"))
         qa, qb = self.phys.index(pa), self.phys.index(pb)
         self.phys[qa], self.phys[qb] = pb, pa
 
@@ -224,11 +261,12 @@ class ShardedState:
             owner, local = self._owner(self._to_phys_index(int(x)))
             if owner == self.rank:
                 mine.append(local)
-        self.backend.apply_diag(sorted(set(mine)), flip_rest)
+        if mine or flip_rest:
+            self._local(("diag", sorted(set(mine)), flip_rest))
 
     def apply_rh(self) -> None:
         """H on all n qubits: local WHT over the local qubits, then one H per global qubit."""
-        self.backend.apply_rh()
+        self._local(("rh",))
         if self.g:
             h = np.array([[1, 1], [1, -1]], dtype=np.complex128) / math.sqrt(2.0)
             for q in [q for q in range(self.n) if self.phys[q] < self.g]:
@@ -236,6 +274,7 @@ class ShardedState:
 
     # ------------------------------------------------------------ inspection
     def local_numpy(self) -> np.ndarray:
+        self.flush()
         return self.backend.numpy()
 
     def logical_amplitude_map(self):

@@ -543,6 +543,20 @@ def simulate(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOptio
     return SimReport(state, steps, sum(s.sign_count for s in steps) & mask, sum(s.madd_count for s in steps) & mask)
 
 
+def run(c: Circuit, state: DeviceState, engine: Engine = Engine.rh_dax, opts: Optional[SimOptions] = None
+        ) -> List[StepReport]:
+    """Apply the circuit's steps to `state` as it is (no reset to |initial>): the in-place form
+    of simulate used by the partitioner between exchanges."""
+    opts = opts or SimOptions()
+    if state.n != c.n:
+        raise DimensionError("state qubit count mismatch")
+    arr, keep = _steps(c.steps)
+    o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)))
+    rep = (L.qcs_step_report * max(1, len(c.steps)))()
+    _check(L.lib().qcs_simulate(state.handle, arr, len(c.steps), int(engine), C.byref(o), rep))
+    return _reports(rep, len(c.steps))
+
+
 def memory_report(c: Circuit, engine: Engine) -> List[StepReport]:  # engine.cpp:212-234
     c.validate()
     arr, keep = _steps(c.steps)
