@@ -100,7 +100,7 @@ struct RegOp {
     std::uint64_t gctrl_val;
     std::uint16_t dtab;       // TOP_DIAG (dk <= 2): register part of the entry index for q = 0..7, 2 bits each
     std::uint16_t fast;       // TOP_GATE: dense 2x2 without tile-local controls
-    std::uint32_t pad1;
+    std::uint32_t smask;      // KF_SIGNED: byte cg = registers q that flip when the constant bits spell cg
     double2 c[4];             // TOP_GATE: a0, b0, a1, b1; TOP_DIAG: entries; TOP_SCALE: c[0].x
 };
 

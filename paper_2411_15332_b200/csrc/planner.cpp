@@ -415,6 +415,15 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                     if (signed_only) {
                         o.kind = std::uint8_t(o.kind | KF_SIGNED);
                         o.dskip = std::uint8_t(neg);
+                        // for each value cg of the group-constant bits: the registers that flip
+                        for (int cg = 0; cg < 4; ++cg) {
+                            unsigned byte = 0;
+                            for (int q = 0; q < 8; ++q) {
+                                const int g = cg | int((o.dtab >> (2 * q)) & 3u);
+                                if (neg >> g & 1) byte |= 1u << q;
+                            }
+                            o.smask |= byte << (8 * cg);
+                        }
                     }
                 }
                 P.ops[nops++] = o;

@@ -305,22 +305,27 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG | F_SMEM)) ? 2
             double2 v[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) v[q] = sm[swz(lb | off[q])];
+            const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];  // basis index of register 0
+            unsigned negacc = 0;  // pending sign flips of the +-1 diagonals (they commute)
             for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
                 const RegOp& o = P.ops[oi];
                 const int kb = o.kind;  // low bits: kind; KF_GCTRL: controls outside the tile
                 if ((kb & KF_GCTRL) && (base & o.gctrl_mask) != o.gctrl_val) continue;
-                const int kind = kb & KF_KIND;
-                if ((F & F_DIAG) && (kb & KF_SIGNED)) {  // diagonal of +-1 entries: exact sign flips
-                    const unsigned tab = o.dtab, neg = o.dskip;
+                if ((F & F_DIAG) && (kb & KF_SIGNED)) {
+                    // +-1 diagonal: the host tabulated, for each value of the bits that are
+                    // constant over the group, which registers flip (one byte per value)
                     int cg = 0;
-                    if (o.dreg[0] == 0xff) cg |= int(((base | (lb & 7u) | hi_tab[lb >> 3]) >> o.dpos[0]) & 1) << (o.dk - 1);
-                    if (o.dk == 2 && o.dreg[1] == 0xff) cg |= int(((base | (lb & 7u) | hi_tab[lb >> 3]) >> o.dpos[1]) & 1);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int g = cg | int((tab >> (2 * q)) & 3u);
-                        if (neg >> g & 1) v[q] = make_double2(-v[q].x, -v[q].y);
-                    }
+                    if (o.dreg[0] == 0xff) cg |= int((g0 >> o.dpos[0]) & 1) << (o.dk - 1);
+                    if (o.dk == 2 && o.dreg[1] == 0xff) cg |= int((g0 >> o.dpos[1]) & 1);
+                    negacc ^= (o.smask >> (8 * cg)) & 0xffu;
                     continue;
+                }
+                const int kind = kb & KF_KIND;
+                if (negacc && (kind == TOP_WHT || kind == TOP_GATE)) {  // flush before non-diagonals
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (negacc >> q & 1) v[q] = make_double2(-v[q].x, -v[q].y);
+                    negacc = 0;
                 }
                 if (kind == TOP_WHT) {
                     const int tm = o.t;
@@ -336,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG | F_SMEM)) ? 2
                     else if (o.t == 1) gate1<1>(v, o, lb, ro);
                     else gate1<2>(v, o, lb, ro);
                 } else if ((F & F_DIAG) && kind == TOP_DIAG) {
-                    diag_op(v, o, big, base | (lb & 7u) | hi_tab[lb >> 3]);
+                    diag_op(v, o, big, g0);
                 } else if ((F & F_SIGN) && kind == TOP_SIGN) {
                     const TileOp& so = big[o.ref];
                     if (!(sign_hit >> (o.sidx & 31) & 1)) {
@@ -358,7 +363,10 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG | F_SMEM)) ? 2
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) sm[swz(lb | off[q])] = v[q];
+            for (int q = 0; q < 8; ++q) {
+                if (negacc >> q & 1) v[q] = make_double2(-v[q].x, -v[q].y);
+                sm[swz(lb | off[q])] = v[q];
+            }
         }
         __syncthreads();
     }
