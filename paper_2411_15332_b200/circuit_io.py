@@ -1,0 +1,317 @@
+"""The reference's front end (src/circuit_io.cpp, include/qcsim/circuit_io.hpp) over the B200 engine.
+
+* ``parse_circuit_json`` / ``load_circuit_file`` (circuit_io.cpp:16-83): the same schema, rules
+  and ParseError messages (JSON syntax errors keep the ``circuit JSON:`` prefix; the detail text
+  comes from Python's parser, not nlohmann's);
+* ``parse_gate_expression`` (circuit_io.cpp:85-107): catalog gates joined by ``x`` / ``*``;
+* ``render_report`` (circuit_io.cpp:109-203): human / JSON / CSV, key-ordered, with seeded
+  sampling.  The JSON layout and number formatting follow nlohmann::ordered_json::dump(2); the
+  samples use the same generator chain as the reference (std::mt19937_64 ->
+  generate_canonical<double, 53> -> uniform_real_distribution(0, total) -> lower_bound on the
+  sequential CDF), so equal probabilities give equal samples.
+
+Probabilities, argmax and the norm come from the device (qcs_probabilities is bit-exact; large
+states report argmax and top-16 without downloading the state, as the reference does above 2^16
+amplitudes).
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+from typing import List
+
+import numpy as np
+
+from . import qcsim as Q
+
+
+# ---------------------------------------------------------------- parsing
+def _placement(j) -> Q.Placement:  # circuit_io.cpp:16-31
+    if not isinstance(j, dict) or "gate" not in j or "targets" not in j:
+        raise Q.ParseError('placement needs "gate" and "targets"')
+    params = j.get("params", [])
+    gate = Q.gate_catalog_lookup(_string(j["gate"]), [_number(p) for p in _array(params)])
+    targets = [_int(t) for t in _array(j["targets"])]
+    if len(targets) != gate.arity:
+        raise Q.ParseError(f"gate {gate.name} targets {gate.arity} qubit(s)")
+    for i in range(1, len(targets)):
+        if targets[i] != targets[i - 1] + 1:
+            raise Q.ParseError("gate targets must be ascending and contiguous")
+    return Q.Placement(gate, targets[0])
+
+
+def _step(j) -> Q.CircuitStep:  # circuit_io.cpp:33-52
+    if isinstance(j, list):
+        return Q.CircuitStep.of_gates([_placement(p) for p in j])
+    if isinstance(j, dict):
+        if "oracle" in j:
+            return Q.CircuitStep.of_diag(Q.DiagSign([_uint(j["oracle"])], False))
+        if "z0" in j:
+            return Q.CircuitStep.of_diag(Q.DiagSign([0], True))
+        if "diag" in j:
+            d = j["diag"]
+            if not isinstance(d, dict) or "flipped" not in d:
+                raise Q.ParseError('circuit JSON: key "flipped" not found')
+            return Q.CircuitStep.of_diag(Q.DiagSign([_uint(x) for x in _array(d["flipped"])],
+                                                    bool(_boolean(d.get("flip_rest", False)))))
+    raise Q.ParseError("step must be a placement list or a diagonal object")
+
+
+def _type_error(want, got):
+    kinds = {dict: "object", list: "array", str: "string", bool: "boolean", type(None): "null"}
+    return Q.ParseError(f"circuit JSON: type must be {want}, but is {kinds.get(type(got), 'number')}")
+
+
+def _int(v):
+    if isinstance(v, bool) or not isinstance(v, (int, float)):
+        raise _type_error("number", v)
+    return int(v)
+
+
+def _uint(v):
+    return _int(v) & ((1 << 64) - 1)
+
+
+def _number(v):
+    if isinstance(v, bool) or not isinstance(v, (int, float)):
+        raise _type_error("number", v)
+    return float(v)
+
+
+def _string(v):
+    if not isinstance(v, str):
+        raise _type_error("string", v)
+    return v
+
+
+def _array(v):
+    if not isinstance(v, list):
+        raise _type_error("array", v)
+    return v
+
+
+def _boolean(v):
+    if not isinstance(v, bool):
+        raise _type_error("boolean", v)
+    return v
+
+
+def parse_circuit_json(text: str) -> Q.Circuit:  # circuit_io.cpp:56-75
+    try:
+        j = json.loads(text)
+    except (json.JSONDecodeError, TypeError) as e:
+        raise Q.ParseError(f"circuit JSON: parse error: {e}") from None
+    if not isinstance(j, dict) or "qubits" not in j or "steps" not in j:
+        raise Q.ParseError('circuit needs "qubits" and "steps"')
+    c = Q.Circuit(_int(j["qubits"]), [_step(s) for s in _array(j["steps"])], _uint(j.get("initial", 0)))
+    c.validate()
+    return c
+
+
+def load_circuit_file(path: str) -> Q.Circuit:  # circuit_io.cpp:77-83
+    try:
+        with open(path, "r") as f:
+            text = f.read()
+    except OSError:
+        raise Q.ParseError("cannot open circuit file: " + path) from None
+    return parse_circuit_json(text)
+
+
+def _dense_tensor(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """core.cpp:55-72 with std::complex<double> products (separately rounded)."""
+    rows, cols = a.shape[0] * b.shape[0], a.shape[1] * b.shape[1]
+    cap = int(Q.L.lib().qcs_dense_cap())
+    if rows and cols > cap // rows:
+        raise Q.CapacityError(f"dense tensor product exceeds dense cap of {cap} elements")
+    out = np.zeros((rows, cols), np.complex128)
+    for ra in range(a.shape[0]):
+        for rb in range(b.shape[0]):
+            for ca in range(a.shape[1]):
+                va = a[ra, ca]
+                for cb in range(b.shape[1]):
+                    vb = b[rb, cb]
+                    out[ra * b.shape[0] + rb, ca * b.shape[1] + cb] = complex(
+                        va.real * vb.real - va.imag * vb.imag, va.real * vb.imag + va.imag * vb.real)
+    return out
+
+
+def parse_gate_expression(expr: str) -> np.ndarray:  # circuit_io.cpp:85-107
+    names = expr.split()
+    gates = []
+    for i, tok in enumerate(names):
+        if i % 2 == 1:
+            if tok not in ("x", "*"):
+                raise Q.ParseError("expected tensor operator 'x' in expression")
+        else:
+            gates.append(tok)
+    if not gates or len(names) % 2 == 0:
+        raise Q.ParseError("expression must be gate names joined by 'x'")
+    acc = Q.gate_catalog_lookup(gates[0], Q.canonical_params(gates[0])).matrix
+    for g in gates[1:]:
+        acc = _dense_tensor(acc, Q.gate_catalog_lookup(g, Q.canonical_params(g)).matrix)
+    return acc
+
+
+# ---------------------------------------------------------------- sampling (bit-compatible)
+class MT19937_64:
+    """std::mt19937_64 (the reference seeds it with the report seed, circuit_io.cpp:116)."""
+
+    def __init__(self, seed: int):
+        self.mt = [0] * 312
+        self.mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+        self.i = 312
+
+    def __call__(self) -> int:
+        if self.i >= 312:
+            mt = self.mt
+            for k in range(312):
+                y = (mt[k] & 0xFFFFFFFF80000000) | (mt[(k + 1) % 312] & 0x7FFFFFFF)
+                v = mt[(k + 156) % 312] ^ (y >> 1)
+                if y & 1:
+                    v ^= 0xB5026F5AA96619E9
+                mt[k] = v
+            self.i = 0
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & 0xFFFFFFFFFFFFFFFF
+
+
+def _uniform(rng: MT19937_64, hi: float) -> float:
+    """uniform_real_distribution<double>(0, hi) over generate_canonical<double, 53> (libstdc++)."""
+    c = float(rng()) / 18446744073709551616.0
+    if c >= 1.0:
+        c = math.nextafter(1.0, 0.0)
+    return (hi - 0.0) * c + 0.0
+
+
+def sample(probs: np.ndarray, count: int, seed: int) -> List[int]:  # circuit_io.cpp:114-128
+    rng = MT19937_64(seed)
+    cdf = np.empty(probs.size, np.float64)
+    acc = 0.0
+    for i, p in enumerate(probs.tolist()):  # sequential, as the reference accumulates
+        acc += p
+        cdf[i] = acc
+    out = []
+    for _ in range(count):
+        u = _uniform(rng, acc)
+        out.append(int(np.searchsorted(cdf, u, side="left")))
+    return out
+
+
+# ---------------------------------------------------------------- rendering
+def _num(x: float) -> str:
+    """nlohmann::json number formatting: shortest round-trip digits, '.0' for integral values,
+    exponent form outside [1e-5, 1e15]."""
+    if x != x:
+        return "null"
+    if x in (float("inf"), float("-inf")):
+        return "null"
+    r = repr(float(x))
+    if "e" in r or "E" in r:
+        mant, exp = r.split("e")
+        e = int(exp)
+        return f"{mant}e{'+' if e >= 0 else '-'}{abs(e):02d}"
+    return r
+
+
+def _dump(v, indent=0) -> str:
+    pad = " " * indent
+    if isinstance(v, dict):
+        if not v:
+            return "{}"
+        items = [f'{pad}  {json.dumps(k)}: {_dump(x, indent + 2)}' for k, x in v.items()]
+        return "{\n" + ",\n".join(items) + "\n" + pad + "}"
+    if isinstance(v, list):
+        if not v:
+            return "[]"
+        return "[\n" + ",\n".join(f"{pad}  {_dump(x, indent + 2)}" for x in v) + "\n" + pad + "]"
+    if isinstance(v, bool):
+        return "true" if v else "false"
+    if isinstance(v, int):
+        return str(v)
+    if isinstance(v, float):
+        return _num(v)
+    return json.dumps(v)
+
+
+def _g(x: float, prec: int) -> str:
+    """std::ostream default float formatting with precision `prec` (%g)."""
+    return f"{x:.{prec}g}"
+
+
+@dataclass
+class ReportOptions:  # circuit_io.hpp:26-31
+    format: str = "human"  # human | json | csv
+    samples: int = 0
+    seed: int = 0
+    engine: str = ""
+
+
+def render_report(report: Q.SimReport, n: int, opts: ReportOptions) -> str:  # circuit_io.cpp:109-203
+    dim = 1 << n
+    small = dim <= (1 << 16)
+    state = report.final
+    probs = report.probabilities if (small or opts.samples > 0) else None
+    if probs is not None:
+        argmax = int(np.argmax(probs))
+        pmax = float(probs[argmax])
+    else:
+        argmax, pmax = state.argmax()
+    if small:  # sequential norm as StateVector::norm (core.cpp:30-34)
+        amps = state.download()
+        norm = math.sqrt(_seq_norm2(amps))
+    else:
+        norm = state.norm()
+    samples = sample(probs, opts.samples, opts.seed) if opts.samples > 0 else []
+
+    if opts.format == "json":
+        j = {"qubits": n, "engine": opts.engine, "argmax": argmax, "max_probability": pmax, "norm": norm}
+        if small:
+            j["probabilities"] = [float(p) for p in probs]
+        else:
+            idx, pr = state.topk(16)
+            j["top_probabilities"] = [{"index": int(i), "probability": float(p)} for i, p in zip(idx, pr)]
+        j["steps"] = [{"structure": s.structure, "stage": s.stage, "matrix_bytes": s.matrix_bytes,
+                       "dense_bytes": s.dense_bytes, "entry_count": s.entry_count, "sign_count": s.sign_count,
+                       "madd_count": s.madd_count} for s in report.steps]
+        j["total_sign_count"] = report.total_sign_count
+        j["total_madd_count"] = report.total_madd_count
+        if opts.samples > 0:
+            j["seed"] = opts.seed
+            j["samples"] = samples
+        return _dump(j) + "\n"
+
+    if opts.format == "csv":
+        out = ["step,structure,stage,matrix_bytes,dense_bytes,entry_count,sign_count,madd_count\n"]
+        for i, s in enumerate(report.steps):
+            out.append(f"{i},{s.structure},{s.stage},{s.matrix_bytes},{s.dense_bytes},{s.entry_count},"
+                       f"{s.sign_count},{s.madd_count}\n")
+        out.append(f"argmax,{argmax}\nmax_probability,{_g(pmax, 6)}\n")
+        return "".join(out)
+
+    out = [f"qubits:          {n}\n", f"engine:          {opts.engine}\n", f"argmax:          {argmax}\n",
+           f"max probability: {_g(pmax, 12)}\n", f"norm:            {_g(norm, 12)}\n", "steps:\n"]
+    for i, s in enumerate(report.steps):
+        line = f"  [{i}] {s.structure}  bytes={s.matrix_bytes} (dense {s.dense_bytes})"
+        if s.entry_count:
+            line += f" entries={s.entry_count}"
+        if s.sign_count:
+            line += f" signs={s.sign_count}"
+        out.append(line + f" madds={s.madd_count}\n")
+    if opts.samples > 0:
+        out.append(f"samples (seed {opts.seed}):" + "".join(f" {x}" for x in samples) + "\n")
+    return "".join(out)
+
+
+def _seq_norm2(amps: np.ndarray) -> float:
+    acc = 0.0
+    for a in amps.tolist():
+        acc += a.real * a.real + a.imag * a.imag
+    return acc

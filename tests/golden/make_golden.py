@@ -123,5 +123,72 @@ def main():
     print("golden fixtures written")
 
 
+
+
+def make_io_fixtures():
+    """Reference front end (parse_circuit_json -> simulate -> render_report), oracle/_ref/libqcsim_io.so."""
+    import subprocess
+
+    def io_run(text, engine, fmt, samples, seed):
+        # one process per call: keeps every reference run independent of the others
+        out = subprocess.run([sys.executable, __file__, "io-one", text, engine, fmt, str(samples), str(seed)],
+                             capture_output=True, text=True)
+        code, _, body = out.stdout.partition("\n")
+        return int(code), body
+    circuits = {
+        # exact values only: final states are bit-identical, so reports must be byte-identical
+        "exact_perm": {"qubits": 5, "initial": 3, "steps": [
+            [{"gate": "X", "targets": [0]}, {"gate": "CNOT", "targets": [1, 2]}],
+            [{"gate": "Toffoli", "targets": [2, 3, 4]}], {"oracle": 7}, [{"gate": "SWAP", "targets": [0, 1]}],
+            {"diag": {"flipped": [1, 2, 3], "flip_rest": True}}, [{"gate": "S", "targets": [4]}]]},
+        "grover6": {"qubits": 6, "steps": [
+            [{"gate": "H", "targets": [q]} for q in range(6)], {"oracle": 37},
+            [{"gate": "H", "targets": [q]} for q in range(6)], {"z0": True},
+            [{"gate": "H", "targets": [q]} for q in range(6)], {"oracle": 37},
+            [{"gate": "H", "targets": [q]} for q in range(6)], {"z0": True},
+            [{"gate": "H", "targets": [q]} for q in range(6)]]},
+        "float_mix": {"qubits": 4, "steps": [
+            [{"gate": "RY", "targets": [0], "params": [0.3]}, {"gate": "U", "targets": [1], "params": [1.1, 0.2, 2.5]},
+             {"gate": "RXX", "targets": [2, 3], "params": [0.7]}],
+            [{"gate": "CH", "targets": [0, 1]}, {"gate": "T", "targets": [3]}],
+            [{"gate": "CCX", "targets": [1, 2, 3]}]]},
+    }
+    recs = []
+    for name, circ in circuits.items():
+        text = json.dumps(circ)
+        for engine in ("rh-dax", "dax"):
+            for fmt, samples, seed in (("json", 0, 0), ("json", 7, 99), ("csv", 0, 0), ("human", 5, 42)):
+                n, body = io_run(text, engine, fmt, samples, seed)
+                assert n >= 0, body
+                recs.append(dict(name=name, circuit=text, engine=engine, format=fmt, samples=samples, seed=seed,
+                                 output=body))
+    errors = []
+    for text in ['{"qubits": 2}', '[1, 2]', '{"qubits": 2, "steps": [[{"gate": "H"}]]}',
+                 '{"qubits": 2, "steps": [[{"gate": "CNOT", "targets": [1, 0]}]]}',
+                 '{"qubits": 2, "steps": [[{"gate": "CNOT", "targets": [0]}]]}',
+                 '{"qubits": 2, "steps": [7]}', '{"qubits": 2, "steps": [[{"gate": "Nope", "targets": [0]}]]}',
+                 '{"qubits": 2, "steps": [[{"gate": "H", "targets": [2]}]]}', '{"qubits": 2, "steps": [{"oracle": 4}]}',
+                 '{"qubits": 2, "steps": [[{"gate": "H", "targets": [0]}, {"gate": "X", "targets": [0]}]]}']:
+        n, body = io_run(text, "dax", "json", 0, 0)
+        errors.append(dict(circuit=text, code=-n, message=body))
+    with open(os.path.join(HERE, "io.json"), "w") as f:
+        json.dump(dict(reports=recs, errors=errors), f, indent=0)
+    print("io fixtures written")
+
+
 if __name__ == "__main__":
-    main()
+    # the front-end library and the core reference library define the same symbols: one per process
+    if len(sys.argv) > 1 and sys.argv[1] == "io":
+        make_io_fixtures()
+    elif len(sys.argv) > 1 and sys.argv[1] == "io-one":
+        import ctypes as C
+        lib = C.CDLL(os.path.join(ROOT, "oracle", "_ref", "libqcsim_io.so"))
+        lib.io_run.restype = C.c_long
+        lib.io_run.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_ulonglong, C.c_char_p, C.c_long]
+        lib.io_last_error.restype = C.c_char_p
+        buf = C.create_string_buffer(1 << 22)
+        a = sys.argv[2:]
+        n = lib.io_run(a[0].encode(), a[1].encode(), a[2].encode(), int(a[3]), int(a[4]), buf, len(buf))
+        sys.stdout.write(f"{n}\n" + (buf.value.decode() if n >= 0 else lib.io_last_error().decode()))
+    else:
+        main()
