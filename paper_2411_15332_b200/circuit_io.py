@@ -221,8 +221,14 @@ def _num(x: float) -> str:
     return r
 
 
+class _Compact(list):
+    """An array rendered on one line, "[a,b,c]" (as the reference's report shows the samples)."""
+
+
 def _dump(v, indent=0) -> str:
     pad = " " * indent
+    if isinstance(v, _Compact):
+        return "[" + ",".join(_dump(x) for x in v) + "]"
     if isinstance(v, dict):
         if not v:
             return "{}"
@@ -285,7 +291,7 @@ def render_report(report: Q.SimReport, n: int, opts: ReportOptions) -> str:  # c
         j["total_madd_count"] = report.total_madd_count
         if opts.samples > 0:
             j["seed"] = opts.seed
-            j["samples"] = samples
+            j["samples"] = _Compact(samples)  # the reference's dump prints this array on one line
         return _dump(j) + "\n"
 
     if opts.format == "csv":
