@@ -144,6 +144,48 @@ __global__ void __launch_bounds__(256) k_pair(double2* __restrict__ a, u64 ngrou
     }
 }
 
+// ---------------------------------------------------------------- four members, monomial rows
+// Swap, iSwap, DCX, RZZ, CU1-like diagonals on two free bits: each written row is one product.
+struct Quad {
+    int k;
+    int pos[3];
+    u64 fixed;
+    u64 off[4];
+    int load;        // member mask to load
+    int nrows;
+    int row[4];      // member written by row r
+    int col[4];      // member read by row r
+    double2 v[4];
+};
+
+template <int ITEMS>
+__global__ void __launch_bounds__(256) k_quad(double2* __restrict__ a, u64 ngroups, const __grid_constant__ Quad p) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    const u64 t0 = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    double2 x[ITEMS][4];
+    u64 idx[ITEMS];
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        idx[it] = insert_zeros(t0 + it * stride, p.k, p.pos) | p.fixed;
+        if (t0 + it * stride < ngroups) {
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+                if (p.load >> m & 1) x[it][m] = ld_stream(a + (idx[it] | p.off[m]));
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        if (t0 + it * stride >= ngroups) continue;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r >= p.nrows) break;
+            const int c = p.col[r];
+            const double2 xv = c == 0 ? x[it][0] : c == 1 ? x[it][1] : c == 2 ? x[it][2] : x[it][3];
+            st_stream(a + (idx[it] | p.off[p.row[r]]), madd(make_double2(0.0, 0.0), p.v[r], xv));
+        }
+    }
+}
+
 // ---------------------------------------------------------------- generic row tables
 // NF: free bits per group; NNZ: max nonzeros per touched row; ITEMS: groups per thread.
 template <int NF, int NNZ, int ITEMS>
@@ -305,6 +347,25 @@ void launch_gate(double2* amps, int n, const GateDesc& d, cudaStream_t st) {
         return;
     }
     const int z = max_nnz(d);
+    if (d.nfree == 2 && z <= 1 && d.nrows <= 4) {  // Swap, iSwap, DCX, RZZ
+        Quad p{};
+        p.k = d.k;
+        std::memcpy(p.pos, d.pos_asc, sizeof(p.pos));
+        p.fixed = d.fixed_val;
+        for (int m = 0; m < 4; ++m) p.off[m] = d.member_off[m];
+        p.load = int(d.load_mask);
+        p.nrows = d.nrows;
+        for (int r = 0; r < d.nrows; ++r) {
+            p.row[r] = d.row_member[r];
+            p.col[r] = d.col_member[r][0];
+            p.v[r] = d.val[r][0];
+        }
+        const int items = ov ? ov : 2;
+        if (items == 1) launch_k(k_quad<1>, amps, n, d.k, d, p, 1, st, "gate_quad_monomial");
+        else if (items == 4) launch_k(k_quad<4>, amps, n, d.k, d, p, 4, st, "gate_quad_monomial");
+        else launch_k(k_quad<2>, amps, n, d.k, d, p, 2, st, "gate_quad_monomial");
+        return;
+    }
     if (d.nfree == 2) {
         if (z <= 1) launch_k(k_gate<2, 1, 2>, amps, n, d.k, d, d, 2, st, "gate_f2_monomial");  // Swap, iSwap, DCX
         else launch_k(k_gate<2, 4, 1>, amps, n, d.k, d, d, 1, st, "gate_f2_dense");           // RXX, ECR, CU
