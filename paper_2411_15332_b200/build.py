@@ -22,6 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC",
           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "--expt-relaxed-constexpr"]
+# tuning experiments only (e.g. "-DQCS_TILE_NG=1"); part of the build stamp
+COMMON += os.environ.get("QCS_EXTRA_NVCC", "").split()
 
 SOURCES = ["gates.cpp", "ops.cpp", "planner.cpp", "engine.cpp", "abi.cpp", "timing.cpp",
            "gate_kernels.cu", "tile_kernels.cu", "state_kernels.cu", "encode_kernels.cu"]

@@ -234,6 +234,14 @@ __device__ __noinline__ void smem_gate(double2* sm, const TileOp& o, int m, unsi
 }
 
 constexpr int kThreads = 256;
+// gate/diagonal passes: groups per thread in the register rounds, and the resident-tile
+// target that sets their register budget (compile-time tuning knobs)
+#ifndef QCS_TILE_NG
+#define QCS_TILE_NG 1
+#endif
+#ifndef QCS_TILE_MINB
+#define QCS_TILE_MINB 2
+#endif
 constexpr int kMaxBits = 12;
 
 enum : unsigned { F_GATE = 1, F_DIAG = 2, F_SIGN = 4, F_SMEM = 8 };
@@ -242,8 +250,8 @@ enum : unsigned { F_GATE = 1, F_DIAG = 2, F_SIGN = 4, F_SMEM = 8 };
 // without gates or diagonals compiles to the lean butterfly/sign kernel.
 template <unsigned F>
 // butterfly / sign-only passes are lean enough for 3 resident tiles per SM (the smem limit);
-// passes with gates or diagonals need the registers of 2
-__global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG | F_SMEM)) ? 2 : 3)
+// passes with gates or diagonals trade residency for registers (QCS_TILE_MINB)
+__global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_MINB : (F & F_SMEM) ? 2 : 3)
     k_tile(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,
            const u64* __restrict__ flipped) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -300,13 +308,25 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG | F_SMEM)) ? 2
         unsigned off[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) off[q] = ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u);
-        for (unsigned g = t; g < ngroups; g += bt) {
-            const unsigned lb = insert_zero(insert_zero(insert_zero(g, r0), r1), r2);
-            double2 v[8];
+        // NG groups per thread at once: gate-heavy passes are FP64/issue bound, and two
+        // independent register groups per operation halve the per-operation dispatch cost
+        constexpr int NG = (F & (F_GATE | F_DIAG)) ? QCS_TILE_NG : 1;
+        for (unsigned gb = t; gb < ngroups; gb += NG * bt) {
+            unsigned lb[NG];
+            bool ok[NG];
+            u64 g0[NG];
+            unsigned negacc[NG];
+            double2 v[NG][8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = sm[swz(lb | off[q])];
-            const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];  // basis index of register 0
-            unsigned negacc = 0;  // pending sign flips of the +-1 diagonals (they commute)
+            for (int r = 0; r < NG; ++r) {
+                const unsigned g = gb + unsigned(r) * bt;
+                ok[r] = g < ngroups;
+                lb[r] = insert_zero(insert_zero(insert_zero(ok[r] ? g : gb, r0), r1), r2);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[r][q] = sm[swz(lb[r] | off[q])];
+                g0[r] = base | (lb[r] & 7u) | hi_tab[lb[r] >> 3];  // basis index of register 0
+                negacc[r] = 0;  // pending sign flips of the +-1 diagonals (they commute)
+            }
             for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
                 const RegOp& o = P.ops[oi];
                 const int kb = o.kind;  // low bits: kind; KF_GCTRL: controls outside the tile
@@ -314,58 +334,84 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG | F_SMEM)) ? 2
                 if ((F & F_DIAG) && (kb & KF_SIGNED)) {
                     // +-1 diagonal: the host tabulated, for each value of the bits that are
                     // constant over the group, which registers flip (one byte per value)
-                    int cg = 0;
-                    if (o.dreg[0] == 0xff) cg |= int((g0 >> o.dpos[0]) & 1) << (o.dk - 1);
-                    if (o.dk == 2 && o.dreg[1] == 0xff) cg |= int((g0 >> o.dpos[1]) & 1);
-                    negacc ^= (o.smask >> (8 * cg)) & 0xffu;
+                    const int dk = o.dk, p0 = o.dpos[0], p1 = o.dpos[1];
+                    const bool c0 = o.dreg[0] == 0xff, c1 = dk == 2 && o.dreg[1] == 0xff;
+                    const unsigned sm_ = o.smask;
+#pragma unroll
+                    for (int r = 0; r < NG; ++r) {
+                        int cg = 0;
+                        if (c0) cg |= int((g0[r] >> p0) & 1) << (dk - 1);
+                        if (c1) cg |= int((g0[r] >> p1) & 1);
+                        negacc[r] ^= (sm_ >> (8 * cg)) & 0xffu;
+                    }
                     continue;
                 }
                 const int kind = kb & KF_KIND;
-                if (negacc && (kind == TOP_WHT || kind == TOP_GATE)) {  // flush before non-diagonals
+                if (kind == TOP_WHT || kind == TOP_GATE) {  // flush sign flips before non-diagonals
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        if (negacc >> q & 1) v[q] = make_double2(-v[q].x, -v[q].y);
-                    negacc = 0;
+                    for (int r = 0; r < NG; ++r) {
+                        if (negacc[r]) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (negacc[r] >> q & 1) v[r][q] = make_double2(-v[r][q].x, -v[r][q].y);
+                            negacc[r] = 0;
+                        }
+                    }
                 }
                 if (kind == TOP_WHT) {
                     const int tm = o.t;
-                    if (tm & 1) butterfly<0>(v);
-                    if (tm & 2) butterfly<1>(v);
-                    if (tm & 4) butterfly<2>(v);
+#pragma unroll
+                    for (int r = 0; r < NG; ++r) {
+                        if (tm & 1) butterfly<0>(v[r]);
+                        if (tm & 2) butterfly<1>(v[r]);
+                        if (tm & 4) butterfly<2>(v[r]);
+                    }
                 } else if (kind == TOP_SCALE) {
                     const double sc = o.c[0].x;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) v[q] = make_double2(v[q].x * sc, v[q].y * sc);
+                    for (int r = 0; r < NG; ++r)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) v[r][q] = make_double2(v[r][q].x * sc, v[r][q].y * sc);
                 } else if ((F & F_GATE) && kind == TOP_GATE) {
-                    if (o.t == 0) gate1<0>(v, o, lb, ro);
-                    else if (o.t == 1) gate1<1>(v, o, lb, ro);
-                    else gate1<2>(v, o, lb, ro);
+                    const int tt = o.t;
+#pragma unroll
+                    for (int r = 0; r < NG; ++r) {
+                        if (tt == 0) gate1<0>(v[r], o, lb[r], ro);
+                        else if (tt == 1) gate1<1>(v[r], o, lb[r], ro);
+                        else gate1<2>(v[r], o, lb[r], ro);
+                    }
                 } else if ((F & F_DIAG) && kind == TOP_DIAG) {
-                    diag_op(v, o, big, g0);
+#pragma unroll
+                    for (int r = 0; r < NG; ++r) diag_op(v[r], o, big, g0[r]);
                 } else if ((F & F_SIGN) && kind == TOP_SIGN) {
                     const TileOp& so = big[o.ref];
-                    if (!(sign_hit >> (o.sidx & 31) & 1)) {
-                        if (so.flip_rest) {
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) v[q] = neg_exact(v[q]);
-                        }
-                    } else {
-                        const u64* f = flipped + so.flip_off;
-                        const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];
+                    for (int r = 0; r < NG; ++r) {
+                        if (!(sign_hit >> (o.sidx & 31) & 1)) {
+                            if (so.flip_rest) {
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const unsigned j = lb | off[q];
-                            const u64 gi = base | (j & 7u) | hi_tab[j >> 3];
-                            (void)g0;
-                            if (listed(f, so.flip_cnt, gi) != (so.flip_rest != 0)) v[q] = neg_exact(v[q]);
+                                for (int q = 0; q < 8; ++q) v[r][q] = neg_exact(v[r][q]);
+                            }
+                        } else {
+                            const u64* f = flipped + so.flip_off;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const unsigned j = lb[r] | off[q];
+                                const u64 gi = base | (j & 7u) | hi_tab[j >> 3];
+                                if (listed(f, so.flip_cnt, gi) != (so.flip_rest != 0)) v[r][q] = neg_exact(v[r][q]);
+                            }
                         }
                     }
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (negacc >> q & 1) v[q] = make_double2(-v[q].x, -v[q].y);
-                sm[swz(lb | off[q])] = v[q];
+            for (int r = 0; r < NG; ++r) {
+                if (!ok[r]) continue;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (negacc[r] >> q & 1) v[r][q] = make_double2(-v[r][q].x, -v[r][q].y);
+                    sm[swz(lb[r] | off[q])] = v[r][q];
+                }
             }
         }
         __syncthreads();
