@@ -79,6 +79,7 @@ struct TileOp {
 
 // RegOp::kind flags above the kind bits
 constexpr int KF_KIND = 0x0f;
+constexpr int KF_FLUSH = 0x20;   // apply the pending +-1 sign flips before this op (set by the planner)
 constexpr int KF_SIGNED = 0x40;  // TOP_DIAG with entries in {+1, -1}: dskip holds the -1 entries
 constexpr int KF_GCTRL = 0x80;   // has controls outside the tile (gctrl_mask / gctrl_val)
 
@@ -86,8 +87,6 @@ constexpr int KF_GCTRL = 0x80;   // has controls outside the tile (gctrl_mask / 
 struct RegOp {
     std::uint8_t kind;        // TOP_GATE (one target), TOP_DIAG, TOP_SIGN, TOP_WHT, TOP_SCALE | KF_* flags
     std::uint8_t t;           // TOP_GATE: target register bit; TOP_WHT: register-bit mask
-    std::uint8_t rk0, rk1;    // TOP_GATE: row kind (0 untouched, 1 one product, 2 two products)
-    std::uint8_t rc0, rc1;    // TOP_GATE: column of a single-product row
     std::uint8_t dk;          // TOP_DIAG: phase bits (<= 3)
     std::uint8_t dskip;       // TOP_DIAG: bit g set = entry g is exactly 1 (untouched)
     std::uint8_t dreg[3];     // TOP_DIAG: register bit of phase bit i, 0xff = constant over a group
@@ -99,9 +98,8 @@ struct RegOp {
     std::uint64_t gctrl_mask; // controls outside the tile (basis bits / required value)
     std::uint64_t gctrl_val;
     std::uint16_t dtab;       // TOP_DIAG (dk <= 2): register part of the entry index for q = 0..7, 2 bits each
-    std::uint16_t fast;       // TOP_GATE: dense 2x2 without tile-local controls
     std::uint32_t smask;      // KF_SIGNED: byte cg = registers q that flip when the constant bits spell cg
-    double2 c[4];             // TOP_GATE: a0, b0, a1, b1; TOP_DIAG: entries; TOP_SCALE: c[0].x
+    double2 c[4];             // TOP_GATE: the 2x2 matrix m00, m01, m10, m11; TOP_DIAG: entries; TOP_SCALE: c[0].x
 };
 
 struct RoundDesc {

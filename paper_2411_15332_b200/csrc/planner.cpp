@@ -301,6 +301,7 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                 return -1;
             };
             rd.op_begin = std::uint16_t(nops);
+            bool pending_signs = false;  // a +-1 diagonal since the last butterfly / gate
             for (int idx : r.ops) {
                 const FOp& f = ops[std::size_t(idx)];
                 if (nops >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many operations in a pass");
@@ -336,27 +337,20 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                             use_big = true;
                         } else {
                             o.t = std::uint8_t(reg(f.tpos[0]));
+                            // dense 2x2 (rows the gate leaves alone stay identity rows): the
+                            // kernel's one straight-line form; zeros and ones are exact under fma
+                            o.c[0] = o.c[3] = make_double2(1.0, 0.0);
+                            o.c[1] = o.c[2] = make_double2(0.0, 0.0);
                             for (int row = 0; row < f.nrows; ++row) {
-                                const double2 a = f.val[row][0];
-                                const double2 b2 = f.nnz[row] > 1 ? f.val[row][1] : make_double2(0.0, 0.0);
-                                if (f.row_member[row] == 0) {
-                                    o.rk0 = f.nnz[row];
-                                    o.rc0 = f.col_member[row][0];
-                                    o.c[0] = a;
-                                    o.c[1] = b2;
-                                } else {
-                                    o.rk1 = f.nnz[row];
-                                    o.rc1 = f.col_member[row][0];
-                                    o.c[2] = a;
-                                    o.c[3] = b2;
-                                }
+                                const int rm = f.row_member[row];
+                                o.c[2 * rm] = o.c[2 * rm + 1] = make_double2(0.0, 0.0);
+                                for (int z = 0; z < f.nnz[row]; ++z) o.c[2 * rm + f.col_member[row][z]] = f.val[row][z];
                             }
-                            o.fast = std::uint16_t(o.rk0 == 2 && o.rk1 == 2 && o.lctrl_mask == 0);
                         }
                         break;
                     case TOP_WHT: {  // a run of single-bit butterflies becomes one masked op
                         const unsigned bit = 1u << reg(f.tpos[0]);
-                        if (nops > rd.op_begin && P.ops[nops - 1].kind == TOP_WHT && !(P.ops[nops - 1].t & bit)) {
+                        if (nops > rd.op_begin && (P.ops[nops - 1].kind & ~KF_FLUSH) == TOP_WHT && !(P.ops[nops - 1].t & bit)) {
                             P.ops[nops - 1].t = std::uint8_t(P.ops[nops - 1].t | bit);
                             continue;
                         }
@@ -425,6 +419,11 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                             o.smask |= byte << (8 * cg);
                         }
                     }
+                }
+                if (o.kind & KF_SIGNED) pending_signs = true;
+                if ((f.kind == TOP_WHT || f.kind == TOP_GATE) && pending_signs) {
+                    o.kind = std::uint8_t(o.kind | KF_FLUSH);
+                    pending_signs = false;
                 }
                 P.ops[nops++] = o;
             }

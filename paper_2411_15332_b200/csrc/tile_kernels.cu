@@ -78,39 +78,20 @@ __device__ __forceinline__ double2 cmul2_f(double2 a, double2 x0, double2 b, dou
                         fma(a.x, x0.y, fma(a.y, x0.x, fma(b.x, x1.y, b.y * x1.x))));
 }
 
-// Row recipe of a one-target gate: rk = 0 untouched, 1 one product (column rc), 2 two products.
-__device__ __forceinline__ double2 gate_row(int rk, int rc, double2 a, double2 b, double2 x0, double2 x1,
-                                            double2 self) {
-    if (rk == 0) return self;
-    if (rk == 1) return cmul_f(a, rc ? x1 : x0);
-    return cmul2_f(a, x0, b, x1);
-}
-
-template <int T>
-__device__ __forceinline__ void gate1(double2 (&v)[8], const RegOp& o, unsigned lb, const unsigned (&ro)[3]) {
+// One-target gate as a dense 2x2 on the register pairs along bit T; `en` = the registers whose
+// tile-local controls hold (0xff without controls).  One straight-line form for every gate keeps
+// the register allocation of the round loop free of per-kind copies.
+template <int T, bool CTRL>
+__device__ __forceinline__ void gate1(double2 (&v)[8], const RegOp& o, unsigned en) {
     const double2 a0 = o.c[0], b0 = o.c[1], a1 = o.c[2], b1 = o.c[3];
-    if (o.fast) {  // dense 2x2, no tile-local control: straight-line
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if (q & (1 << T)) continue;
-            const double2 x0 = v[q], x1 = v[q | (1 << T)];
-            v[q] = cmul2_f(a0, x0, b0, x1);
-            v[q | (1 << T)] = cmul2_f(a1, x0, b1, x1);
-        }
-        return;
-    }
-    const int rk0 = o.rk0, rk1 = o.rk1, rc0 = o.rc0, rc1 = o.rc1;
-    const unsigned cm = o.lctrl_mask, cv = o.lctrl_val;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         if (q & (1 << T)) continue;
-        if (cm) {
-            const unsigned l = lb | ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u);
-            if ((l & cm) != cv) continue;
-        }
         const double2 x0 = v[q], x1 = v[q | (1 << T)];
-        v[q] = gate_row(rk0, rc0, a0, b0, x0, x1, x0);
-        v[q | (1 << T)] = gate_row(rk1, rc1, a1, b1, x0, x1, x1);
+        const double2 n0 = cmul2_f(a0, x0, b0, x1), n1 = cmul2_f(a1, x0, b1, x1);
+        const bool on = !CTRL || ((en >> q) & 1u);
+        v[q] = on ? n0 : x0;
+        v[q | (1 << T)] = on ? n1 : x1;
     }
 }
 
@@ -330,6 +311,18 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
             for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
                 const RegOp& o = P.ops[oi];
                 const int kb = o.kind;  // low bits: kind; KF_GCTRL: controls outside the tile
+                if (kb & KF_FLUSH) {  // pending sign flips before a butterfly / gate: xor of sign bits
+#pragma unroll
+                    for (int r = 0; r < NG; ++r) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const long long m = (long long)((negacc[r] >> q) & 1u) << 63;
+                            v[r][q] = make_double2(__longlong_as_double(__double_as_longlong(v[r][q].x) ^ m),
+                                                   __longlong_as_double(__double_as_longlong(v[r][q].y) ^ m));
+                        }
+                        negacc[r] = 0;
+                    }
+                }
                 if ((kb & KF_GCTRL) && (base & o.gctrl_mask) != o.gctrl_val) continue;
                 if ((F & F_DIAG) && (kb & KF_SIGNED)) {
                     // +-1 diagonal: the host tabulated, for each value of the bits that are
@@ -347,17 +340,6 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                     continue;
                 }
                 const int kind = kb & KF_KIND;
-                if (kind == TOP_WHT || kind == TOP_GATE) {  // flush sign flips before non-diagonals
-#pragma unroll
-                    for (int r = 0; r < NG; ++r) {
-                        if (negacc[r]) {
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                if (negacc[r] >> q & 1) v[r][q] = make_double2(-v[r][q].x, -v[r][q].y);
-                            negacc[r] = 0;
-                        }
-                    }
-                }
                 if (kind == TOP_WHT) {
                     const int tm = o.t;
 #pragma unroll
@@ -374,11 +356,21 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                         for (int q = 0; q < 8; ++q) v[r][q] = make_double2(v[r][q].x * sc, v[r][q].y * sc);
                 } else if ((F & F_GATE) && kind == TOP_GATE) {
                     const int tt = o.t;
+                    const unsigned cm = o.lctrl_mask, cv = o.lctrl_val;
 #pragma unroll
                     for (int r = 0; r < NG; ++r) {
-                        if (tt == 0) gate1<0>(v[r], o, lb[r], ro);
-                        else if (tt == 1) gate1<1>(v[r], o, lb[r], ro);
-                        else gate1<2>(v[r], o, lb[r], ro);
+                        if (cm) {
+                            unsigned en = 0;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) en |= unsigned(((lb[r] | off[q]) & cm) == cv) << q;
+                            if (tt == 0) gate1<0, true>(v[r], o, en);
+                            else if (tt == 1) gate1<1, true>(v[r], o, en);
+                            else gate1<2, true>(v[r], o, en);
+                        } else {
+                            if (tt == 0) gate1<0, false>(v[r], o, 0xffu);
+                            else if (tt == 1) gate1<1, false>(v[r], o, 0xffu);
+                            else gate1<2, false>(v[r], o, 0xffu);
+                        }
                     }
                 } else if ((F & F_DIAG) && kind == TOP_DIAG) {
 #pragma unroll
