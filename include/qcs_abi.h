@@ -173,6 +173,22 @@ int qcs_simulate(qcs_state* s, const qcs_step* steps, int num_steps, int engine,
 int qcs_memory_report(int n, const qcs_step* steps, int num_steps, int engine,
                       qcs_step_report* reports);
 
+/* Fused-pass plan of a circuit, host only (no device needed): what qcs_simulate with the same
+ * engine and options launches.  B200-specific (the reference has no planner); used by the
+ * tests and the measurement tools to count HBM sweeps. */
+typedef struct qcs_plan_info {
+    int64_t ops;            /* state operations after single-qubit merging (fuse) */
+    int64_t passes;         /* HBM sweeps over the state: tile passes + single-op launches */
+    int64_t tile_passes;
+    int64_t single_passes;  /* passes of one operation, run by the dedicated gate kernels */
+    int64_t rounds;         /* register + shared-memory rounds over all tile passes */
+    int64_t smem_rounds;
+    int64_t reg_ops;        /* operations in the register rounds (after butterfly merging) */
+    int64_t max_tile_bits;  /* tile size used (log2 amplitudes) */
+} qcs_plan_info;
+int qcs_plan_stats(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
+                   qcs_plan_info* out);
+
 /* ------------------------------------------------------------------ compressed structures
  * The device gate encoder: materialise step_matrix_dax / step_matrix_das (engine.hpp:38-39)
  * on the GPU, byte-identical to the reference, without ever forming dense operators.

@@ -40,6 +40,11 @@ class qcs_step_report(C.Structure):
                 ("madd_count", C.c_uint64)]
 
 
+class qcs_plan_info(C.Structure):
+    _fields_ = [(f, C.c_int64) for f in ("ops", "passes", "tile_passes", "single_passes", "rounds",
+                                         "smem_rounds", "reg_ops", "max_tile_bits")]
+
+
 _P = C.c_void_p
 _PS = C.POINTER(_P)
 _D = C.POINTER(C.c_double)
@@ -81,6 +86,8 @@ SIGNATURES = {
     "qcs_simulate": (C.c_int, [_P, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
                                C.POINTER(qcs_step_report)]),
     "qcs_memory_report": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_step_report)]),
+    "qcs_plan_stats": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
+                                 C.POINTER(qcs_plan_info)]),
     "qcs_step_dax": (C.c_int, [C.c_int, C.POINTER(qcs_placement), C.c_int, C.c_int, _P, _P, _P, C.c_uint64,
                                C.c_int, _U64]),
     "qcs_step_das": (C.c_int, [C.c_int, C.POINTER(qcs_placement), C.c_int, C.c_int, _P, _P, _P, C.c_uint64,

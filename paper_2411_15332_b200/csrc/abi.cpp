@@ -323,6 +323,14 @@ int qcs_memory_report(int n, const qcs_step* steps, int num_steps, int engine, q
     });
 }
 
+int qcs_plan_stats(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
+                   qcs_plan_info* out) {
+    return guarded([&] {
+        need(out, "out");
+        qcs::plan_stats(n, steps, num_steps, engine, opts, out);
+    });
+}
+
 // ---------------------------------------------------------------- compressed structures
 
 int qcs_step_dax(int n, const qcs_placement* placements, int num_placements, int device, uint64_t* rows,

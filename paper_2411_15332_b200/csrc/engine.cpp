@@ -441,6 +441,56 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
     }
 }
 
+namespace {
+void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out) {
+    if (ops.empty()) return;
+    out->ops += std::int64_t(ops.size());
+    if (n < 3) {
+        out->passes += std::int64_t(ops.size());
+        out->single_passes += std::int64_t(ops.size());
+        return;
+    }
+    Lowered low;
+    lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
+    for (std::size_t i = 0; i < low.passes.size(); ++i) {
+        ++out->passes;
+        if (low.pass_ops[i].size() == 1) {
+            ++out->single_passes;
+            continue;
+        }
+        const PassParams& p = low.passes[i];
+        ++out->tile_passes;
+        out->rounds += p.nrounds;
+        for (int r = 0; r < p.nrounds; ++r)
+            if (p.rounds[r].flags & RD_SMEM) ++out->smem_rounds;
+            else out->reg_ops += p.rounds[r].op_count;
+    }
+}
+}  // namespace
+
+void plan_stats(int n, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
+                qcs_plan_info* out) {
+    validate_circuit(n, steps, nsteps);
+    if (engine < QCS_ENGINE_DENSE || engine > QCS_ENGINE_RH_DAX) raise(QCS_ERR_ARG, "unknown engine");
+    qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1};
+    if (opts) o = *opts;
+    *out = qcs_plan_info{};
+    out->max_tile_bits = std::min(tile_max_bits(), n);
+    std::vector<FOp> ops;
+    for (int i = 0; i < nsteps; ++i) {
+        const bool use_rh = engine == QCS_ENGINE_RH_DAX && is_hadamard_all(steps[i], n);
+        append_step_ops(n, steps[i], use_rh, ops);
+        if (!o.fuse) {
+            add_plan_stats(n, ops, out);
+            ops.clear();
+        }
+    }
+    if (o.fuse) {
+        merge_single_qubit(n, ops);
+        add_plan_stats(n, ops, out);
+    }
+}
+
 void memory_report(int n, const qcs_step* steps, int nsteps, int engine, qcs_step_report* reports) {
     validate_circuit(n, steps, nsteps);
     for (int i = 0; i < nsteps; ++i) {

@@ -48,6 +48,8 @@ void apply_rh(qcs_state* s);
 
 void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
               qcs_step_report* reports);
+void plan_stats(int n, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
+                qcs_plan_info* out);
 void memory_report(int n, const qcs_step* steps, int nsteps, int engine, qcs_step_report* reports);
 void validate_circuit(int n, const qcs_step* steps, int nsteps);
 

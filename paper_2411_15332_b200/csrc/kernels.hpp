@@ -102,8 +102,10 @@ struct RegOp {
     double2 c[4];             // TOP_GATE: the 2x2 matrix m00, m01, m10, m11; TOP_DIAG: entries; TOP_SCALE: c[0].x
 };
 
+constexpr int RD_SMEM = 1;    // gates on 2-3 targets, run straight on shared memory
+constexpr int RD_SIGNS = 2;   // register round ending with pending +-1 sign flips
 struct RoundDesc {
-    std::uint8_t smem;        // 1: gates on 2-3 targets, run straight on shared memory
+    std::uint8_t flags;       // RD_*
     std::uint8_t r[3];        // local tile bits held in registers (ascending)
     std::uint16_t op_begin, op_count;
 };

@@ -288,9 +288,12 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
         for (auto& r : rounds) {
             if (P.nrounds >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many rounds in a pass");
             unsigned mask = r.mask;
+            // pad to 3 register bits, preferring bits above 2: a round without bits 0..2 can
+            // move its amplitudes to and from HBM directly (whole 128-byte runs per warp)
+            for (int b = 3; b < P.m && __builtin_popcount(mask) < 3; ++b) mask |= 1u << b;
             for (int b = 0; b < P.m && __builtin_popcount(mask) < 3; ++b) mask |= 1u << b;
             RoundDesc& rd = P.rounds[P.nrounds++];
-            rd.smem = r.smem ? 1 : 0;
+            rd.flags = r.smem ? RD_SMEM : 0;
             int c = 0;
             for (int b = 0; b < P.m; ++b)
                 if (mask >> b & 1) rd.r[c++] = std::uint8_t(b);
@@ -322,7 +325,7 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                 bool use_big = false;
                 switch (f.kind) {
                     case TOP_GATE:
-                        if (rd.smem) {
+                        if (rd.flags & RD_SMEM) {
                             big.gcase = f.K;
                             for (int i = 0; i < f.K; ++i) big.tl[i] = loc[f.tpos[i]];
                             big.nrows = f.nrows;
@@ -428,6 +431,7 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                 P.ops[nops++] = o;
             }
             rd.op_count = std::uint16_t(nops - rd.op_begin);
+            if (pending_signs) rd.flags = std::uint8_t(rd.flags | RD_SIGNS);
         }
         P.nops = nops;
         out.passes.push_back(P);

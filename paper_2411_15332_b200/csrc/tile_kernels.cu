@@ -95,6 +95,22 @@ __device__ __forceinline__ void gate1(double2 (&v)[8], const RegOp& o, unsigned 
     }
 }
 
+// Apply and clear the pending +-1 flips (bit q of negacc: negate register q) by xor of the sign
+// bits: straight-line, so the round loop keeps one register assignment.
+template <int NG>
+__device__ __forceinline__ void flip_signs(double2 (&v)[NG][8], unsigned (&negacc)[NG]) {
+#pragma unroll
+    for (int r = 0; r < NG; ++r) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const long long m = (long long)((negacc[r] >> q) & 1u) << 63;
+            v[r][q] = make_double2(__longlong_as_double(__double_as_longlong(v[r][q].x) ^ m),
+                                   __longlong_as_double(__double_as_longlong(v[r][q].y) ^ m));
+        }
+        negacc[r] = 0;
+    }
+}
+
 template <int B>
 __device__ __forceinline__ void butterfly(double2 (&v)[8]) {
 #pragma unroll
@@ -223,6 +239,9 @@ constexpr int kThreads = 256;
 #ifndef QCS_TILE_MINB
 #define QCS_TILE_MINB 2
 #endif
+#ifndef QCS_TILE_IO  // bit 0: first register round straight from HBM; bit 1: last straight to HBM
+#define QCS_TILE_IO 2
+#endif
 constexpr int kMaxBits = 12;
 
 enum : unsigned { F_GATE = 1, F_DIAG = 2, F_SIGN = 4, F_SMEM = 8 };
@@ -267,13 +286,22 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
             if (hit) sign_hit |= 1u << (o.sidx & 31);
         }
     }
+    // a register round at either end reads its amplitudes straight from HBM (first) or writes
+    // them straight back (last): one shared-memory round trip less per amplitude at each end
+    // (only when bits 0..2 are not register bits: then a warp moves whole 128-byte runs)
+    const RoundDesc& R0 = P.rounds[0];
+    const RoundDesc& RL = P.rounds[P.nrounds - 1];
+    const bool io_first = (QCS_TILE_IO & 1) && !((F & F_SMEM) && (R0.flags & RD_SMEM)) && R0.r[0] >= 3;
+    const bool io_last = (QCS_TILE_IO & 2) && !((F & F_SMEM) && (RL.flags & RD_SMEM)) && RL.r[0] >= 3;
     __syncthreads();
-    for (unsigned j = t; j < sz; j += bt) cp_async16(sm + swz(j), a + (base | (j & 7u) | hi_tab[j >> 3]));
-    cp_async_wait_all();
-    __syncthreads();
+    if (!io_first) {
+        for (unsigned j = t; j < sz; j += bt) cp_async16(sm + swz(j), a + (base | (j & 7u) | hi_tab[j >> 3]));
+        cp_async_wait_all();
+        __syncthreads();
+    }
     for (int ri = 0; ri < P.nrounds; ++ri) {
         const RoundDesc& R = P.rounds[ri];
-        if ((F & F_SMEM) && R.smem) {
+        if ((F & F_SMEM) && (R.flags & RD_SMEM)) {
             for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
                 const TileOp& o = big[P.ops[oi].ref];
                 if (!(o.gctrl_mask && (base & o.gctrl_mask) != o.gctrl_val)) {
@@ -303,26 +331,23 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                 const unsigned g = gb + unsigned(r) * bt;
                 ok[r] = g < ngroups;
                 lb[r] = insert_zero(insert_zero(insert_zero(ok[r] ? g : gb, r0), r1), r2);
+                if (io_first && ri == 0) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) v[r][q] = sm[swz(lb[r] | off[q])];
+                    for (int q = 0; q < 8; ++q) {
+                        const unsigned j = lb[r] | off[q];
+                        v[r][q] = a[base | (j & 7u) | hi_tab[j >> 3]];
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) v[r][q] = sm[swz(lb[r] | off[q])];
+                }
                 g0[r] = base | (lb[r] & 7u) | hi_tab[lb[r] >> 3];  // basis index of register 0
                 negacc[r] = 0;  // pending sign flips of the +-1 diagonals (they commute)
             }
             for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
                 const RegOp& o = P.ops[oi];
                 const int kb = o.kind;  // low bits: kind; KF_GCTRL: controls outside the tile
-                if (kb & KF_FLUSH) {  // pending sign flips before a butterfly / gate: xor of sign bits
-#pragma unroll
-                    for (int r = 0; r < NG; ++r) {
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const long long m = (long long)((negacc[r] >> q) & 1u) << 63;
-                            v[r][q] = make_double2(__longlong_as_double(__double_as_longlong(v[r][q].x) ^ m),
-                                                   __longlong_as_double(__double_as_longlong(v[r][q].y) ^ m));
-                        }
-                        negacc[r] = 0;
-                    }
-                }
+                if ((F & F_DIAG) && (kb & KF_FLUSH)) flip_signs<NG>(v, negacc);  // before a butterfly / gate
                 if ((kb & KF_GCTRL) && (base & o.gctrl_mask) != o.gctrl_val) continue;
                 if ((F & F_DIAG) && (kb & KF_SIGNED)) {
                     // +-1 diagonal: the host tabulated, for each value of the bits that are
@@ -396,19 +421,27 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                     }
                 }
             }
+            if ((F & F_DIAG) && (R.flags & RD_SIGNS)) flip_signs<NG>(v, negacc);
+            const bool to_hbm = io_last && ri == P.nrounds - 1;
 #pragma unroll
             for (int r = 0; r < NG; ++r) {
                 if (!ok[r]) continue;
+                if (to_hbm) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    if (negacc[r] >> q & 1) v[r][q] = make_double2(-v[r][q].x, -v[r][q].y);
-                    sm[swz(lb[r] | off[q])] = v[r][q];
+                    for (int q = 0; q < 8; ++q) {
+                        const unsigned j = lb[r] | off[q];
+                        __stcs(a + (base | (j & 7u) | hi_tab[j >> 3]), v[r][q]);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) sm[swz(lb[r] | off[q])] = v[r][q];
                 }
             }
         }
         __syncthreads();
     }
-    for (unsigned j = t; j < sz; j += bt) __stcs(a + (base | (j & 7u) | hi_tab[j >> 3]), sm[swz(j)]);
+    if (!io_last)
+        for (unsigned j = t; j < sz; j += bt) __stcs(a + (base | (j & 7u) | hi_tab[j >> 3]), sm[swz(j)]);
 }
 
 template <unsigned F>
@@ -439,7 +472,7 @@ void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* b
     const int threads = std::min(kThreads, std::max(32, 1 << (p.m - 3)));
     unsigned f = 0;
     for (int r = 0; r < p.nrounds; ++r)
-        if (p.rounds[r].smem) f |= F_SMEM;
+        if (p.rounds[r].flags & RD_SMEM) f |= F_SMEM;
     for (int i = 0; i < p.nops; ++i) {
         const int kind = p.ops[i].kind & KF_KIND;
         if (kind == TOP_GATE) f |= F_GATE;

@@ -565,6 +565,17 @@ def memory_report(c: Circuit, engine: Engine) -> List[StepReport]:  # engine.cpp
     return _reports(rep, len(c.steps))
 
 
+def plan_stats(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOptions] = None) -> dict:
+    """The fused-pass plan simulate() would launch for `c` (host only, no device): operation,
+    pass, round counts.  B200-specific; the reference has no planner."""
+    opts = opts or SimOptions()
+    arr, keep = _steps(c.steps)
+    o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)))
+    info = L.qcs_plan_info()
+    _check(L.lib().qcs_plan_stats(c.n, arr, len(c.steps), int(engine), C.byref(o), C.byref(info)))
+    return {f: int(getattr(info, f)) for f, _ in L.qcs_plan_info._fields_}
+
+
 # ---------------------------------------------------------------- compressed structures
 @dataclass
 class DaxMatrix:  # dax.hpp:22-28
