@@ -1,0 +1,73 @@
+"""Fused-pass planner (host only, no GPU): pass counts through qcs_plan_stats.
+
+The planner is B200-specific (the reference applies one step at a time, engine.cpp:153-210);
+these tests pin its contract: every operation is scheduled, fusing never needs more HBM
+sweeps than stepwise execution, and the BASELINE circuits get the pass counts DESIGN.md
+quotes."""
+import numpy as np
+import pytest
+
+from paper_2411_15332_b200 import configs
+from paper_2411_15332_b200 import qcsim as Q
+
+STEPWISE = Q.SimOptions(fuse=False)
+
+
+def test_c1_is_one_pass():
+    st = Q.plan_stats(configs.c1_circuit())
+    assert st["passes"] == 1 and st["tile_passes"] == 1
+    assert st["max_tile_bits"] == 12
+
+
+def test_c3_grover_pass_count():
+    st = Q.plan_stats(configs.c3_circuit(30))
+    assert st["passes"] == 35          # 8 iterations, A.oracle.A and C.Z0.C fused
+    assert Q.plan_stats(configs.c3_circuit(30), opts=STEPWISE)["passes"] > st["passes"]
+
+
+def test_rh_is_ceil_passes():
+    # H on every qubit: a 12-bit tile takes bits 0..11, later tiles 9 new bits each (0..2 fixed)
+    for n, want in [(12, 1), (21, 2), (28, 3), (30, 3), (32, 4)]:
+        c = Q.Circuit(n, [Q.hadamard_all(n)])
+        assert Q.plan_stats(c)["passes"] == want, n
+
+
+def test_rh_engine_only_for_rh_dax():
+    c = Q.Circuit(14, [Q.hadamard_all(14)])
+    rh = Q.plan_stats(c, Q.Engine.rh_dax)
+    dax = Q.plan_stats(c, Q.Engine.dax)
+    assert rh["ops"] == 15             # the scale plus 14 butterflies
+    assert dax["ops"] == 14            # 14 Hadamard placements
+    assert rh["passes"] == dax["passes"] == 2
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fused_never_needs_more_passes(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(13, 26))
+    names = ["Hadamard", "Pauli-X", "T", "RY", "Controlled-X", "Controlled-Z", "Swap"]
+    steps = []
+    for _ in range(int(rng.integers(5, 30))):
+        name = names[int(rng.integers(0, len(names)))]
+        g = Q.gate_catalog_lookup(name, [float(rng.uniform(0, 6.28))] if name == "RY" else [])
+        qs = [int(q) for q in rng.choice(n, g.arity, replace=False)]
+        steps.append(Q.CircuitStep.of_gates([Q.Placement(g, qubits=qs)]))
+    c = Q.Circuit(n, steps)
+    fused = Q.plan_stats(c)
+    step = Q.plan_stats(c, opts=STEPWISE)
+    assert fused["passes"] <= step["passes"]
+    assert step["ops"] == len(steps)
+    assert fused["ops"] <= step["ops"]
+    assert fused["passes"] == fused["tile_passes"] + fused["single_passes"]
+
+
+def test_small_states_run_one_op_per_pass():
+    c = Q.Circuit(2, [Q.CircuitStep.of_gates([Q.Placement(Q.gate_catalog_lookup("Hadamard"), 0)]),
+                      Q.CircuitStep.of_gates([Q.Placement(Q.gate_catalog_lookup("Pauli-X"), 1)])])
+    st = Q.plan_stats(c)
+    assert st["tile_passes"] == 0 and st["single_passes"] == st["passes"] == 2
+
+
+def test_invalid_circuit_rejected_like_simulate():
+    with pytest.raises(Q.SimError):
+        Q.plan_stats(Q.Circuit(3, [Q.CircuitStep.of_gates([Q.Placement(Q.gate_catalog_lookup("Pauli-X"), 5)])]))
