@@ -185,6 +185,8 @@ typedef struct qcs_plan_info {
     int64_t smem_rounds;
     int64_t reg_ops;        /* operations in the register rounds (after butterfly merging) */
     int64_t max_tile_bits;  /* tile size used (log2 amplitudes) */
+    int64_t alt_passes;     /* tile passes with a simplified program for tiles no sign step reaches */
+    int64_t skip_passes;    /* ... where that program is the identity: only the reached tiles move */
 } qcs_plan_info;
 int qcs_plan_stats(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
                    qcs_plan_info* out);

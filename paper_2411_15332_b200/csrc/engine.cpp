@@ -254,24 +254,29 @@ void run_fused(qcs_state* s, const std::vector<FOp>& ops) {
             low.passes.emplace_back();
         }
     }
+    // plan buffer: [TileOps | flip lists | u64 tables], 256-byte aligned sections
     const std::size_t bb = low.big.size() * sizeof(TileOp);
     const std::size_t fb = low.flips.size() * sizeof(u64);
+    const std::size_t tb = low.tables.size() * sizeof(u64);
     const std::size_t f_off = (bb + 255) & ~std::size_t(255);
-    if (bb + fb) {
-        ensure_plan(s, f_off + fb + 8);
-        std::vector<unsigned char> host(f_off + fb);
+    const std::size_t t_off = (f_off + fb + 255) & ~std::size_t(255);
+    if (bb + fb + tb) {
+        ensure_plan(s, t_off + tb + 8);
+        std::vector<unsigned char> host(t_off + tb);
         if (bb) std::memcpy(host.data(), low.big.data(), bb);
         if (fb) std::memcpy(host.data() + f_off, low.flips.data(), fb);
+        if (tb) std::memcpy(host.data() + t_off, low.tables.data(), tb);
         // pageable copy: staged before the call returns, so `host` may go out of scope
         QCS_CUDA(cudaMemcpyAsync(s->plan_buf, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
     }
     auto* base = static_cast<unsigned char*>(s->plan_buf);
     const auto* big_dev = reinterpret_cast<const TileOp*>(base);
     const auto* flips_dev = reinterpret_cast<const u64*>(base + f_off);
+    const auto* tables_dev = reinterpret_cast<const u64*>(base + t_off);
     for (std::size_t i = 0; i < low.passes.size(); ++i) {
         const auto& po = low.pass_ops[i];
         if (po.size() == 1) run_single(s, ops[std::size_t(po[0])], flips_dev + low.single_flip_off[i], low.single_flip_cnt[i]);
-        else launch_tile_pass(s->amps, n, low.passes[i], big_dev, flips_dev, s->stream);
+        else launch_tile_pass(s->amps, n, low.passes[i], big_dev, flips_dev, tables_dev, s->stream);
     }
 }
 
@@ -460,6 +465,8 @@ void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out) {
         }
         const PassParams& p = low.passes[i];
         ++out->tile_passes;
+        if (p.alt_mode != ALT_NONE) ++out->alt_passes;
+        if (p.alt_mode == ALT_SKIP) ++out->skip_passes;
         out->rounds += p.nrounds;
         for (int r = 0; r < p.nrounds; ++r)
             if (p.rounds[r].flags & RD_SMEM) ++out->smem_rounds;

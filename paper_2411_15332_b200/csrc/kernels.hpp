@@ -111,17 +111,25 @@ struct RoundDesc {
 };
 
 constexpr int kPassMaxOps = 236;
+enum : std::uint8_t { ALT_NONE = 0, ALT_ROUNDS = 1, ALT_SKIP = 2 };
 struct PassParams {           // <= 32 KB: the kernel parameter limit
     int m;                    // tile bits (3..12)
     int nrounds;
     int nops;
     int bits[16];             // basis-bit positions, ascending; bits[0..2] = 0, 1, 2
+    // tiles that no sign step's listed index reaches (sign_hit == 0) run the alternative:
+    // ALT_ROUNDS: rounds [alt_begin, alt_begin + alt_nrounds); ALT_SKIP: nothing (identity)
+    std::uint8_t alt_mode;
+    std::uint16_t alt_begin, alt_nrounds;
+    std::uint32_t hi_off;     // this pass's table of run offsets (tile bits 3..m-1) in the plan's tables
+    std::uint32_t list_off, list_cnt;  // list_cnt > 0: run only these tiles (ALT_SKIP passes)
     RoundDesc rounds[kPassMaxOps];
     RegOp ops[kPassMaxOps];
 };
 
+// tables_dev: the plan's u64 tables (Lowered::tables): run offsets and tile lists
 void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* big_dev,
-                      const std::uint64_t* flipped_dev, cudaStream_t st);
+                      const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, cudaStream_t st);
 int tile_max_bits();
 
 // ---------------------------------------------------------------- reductions

@@ -199,6 +199,11 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
         int used = __builtin_popcountll(S);
         std::vector<int> chosen, skipped;
         u64 nd_block = 0, d_block = 0;  // supports of skipped non-diagonal / diagonal ops
+        // once a sign step is in the pass, later non-elementwise ops must target bits the pass
+        // used before it: then on the tiles the sign step misses, the pass mirrors around it
+        // and collapses (missed_tile_program), e.g. Grover's H..H Z0 H..H
+        bool signed_pass = false;
+        u64 pre_sign = 0;
         for (int idx : remaining) {
             const FOp& f = ops[std::size_t(idx)];
             const bool conflict = (f.touch & nd_block) || (!f.diagonal && (f.touch & d_block));
@@ -209,17 +214,21 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
                 } else {
                     u64 need = 0;
                     for (int i = 0; i < f.K; ++i) need |= u64(1) << f.tpos[i];
+                    const u64 targets = need;
+                    if (signed_pass && (need & ~pre_sign)) need = ~u64(0);  // not mirrored: later
                     need &= ~S;
                     const int add = __builtin_popcountll(need);
                     if (used + add <= M) {
                         S |= need;
                         used += add;
                         take = true;
+                        if (!signed_pass) pre_sign |= targets;
                     }
                 }
             }
             if (take && int(chosen.size()) >= kPassMaxOps - 4) take = false;
             if (take) {
+                if (f.kind == TOP_SIGN) signed_pass = true;
                 chosen.push_back(idx);
             } else {
                 skipped.push_back(idx);
@@ -238,11 +247,92 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
     return plan;
 }
 
+// The program a pass runs on tiles that none of its sign steps' listed indices fall in: each
+// sign step is then the scalar -1 (flip_rest) or +1, scalars commute with everything, and a
+// butterfly pair on one bit with nothing between them touching that bit is 2 I.  Returns false
+// when the pass has no sign step; alt = the remaining operations (a leading scale if the
+// scalar is not 1), empty when the pass is the identity on those tiles.  Exact: the scalars are
+// +-1, the H^n scales 2^(-n/2) and the factors 2.
+bool missed_tile_program(const std::vector<FOp>& ops, const std::vector<int>& list, std::vector<FOp>& alt) {
+    bool any_sign = false;
+    for (int idx : list) any_sign |= ops[std::size_t(idx)].kind == TOP_SIGN;
+    if (!any_sign) return false;
+    double s = 1.0;
+    std::vector<int> keep;
+    for (int idx : list) {
+        const FOp& f = ops[std::size_t(idx)];
+        if (f.kind == TOP_SIGN) {
+            if (f.flip_rest) s = -s;
+            continue;
+        }
+        if (f.kind == TOP_SCALE) {
+            s *= f.scale;
+            continue;
+        }
+        if (f.kind == TOP_WHT) {
+            const u64 bit = u64(1) << f.tpos[0];
+            int j = int(keep.size()) - 1;
+            while (j >= 0 && !(ops[std::size_t(keep[std::size_t(j)])].touch & bit)) --j;
+            if (j >= 0 && ops[std::size_t(keep[std::size_t(j)])].kind == TOP_WHT &&
+                ops[std::size_t(keep[std::size_t(j)])].tpos[0] == f.tpos[0]) {
+                keep.erase(keep.begin() + j);
+                s *= 2.0;
+                continue;
+            }
+        }
+        keep.push_back(idx);
+    }
+    alt.clear();
+    if (s != 1.0) alt.push_back(make_scale(s));
+    for (int idx : keep) alt.push_back(ops[std::size_t(idx)]);
+    return true;
+}
+
 // Lower planned passes to kernel descriptors: one PassParams (constant-bank operation list) per
 // pass, plus the plan-wide TileOp array (shared-memory gates, sign steps, 3-bit diagonals).
-void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& out) {
+void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered& out) {
     out = Lowered{};
-    for (const PlannedPass& pp : plan.passes) {
+    // Missed-tile programs (tile-kernel passes of >= 2 operations).  One that is only a scalar
+    // s becomes a skip: the pass's tiles reached by a sign step get scale(1/s) appended, and the
+    // product of the s moves to a pass that runs every tile (scalars commute with everything).
+    const std::size_t np = plan.passes.size();
+    std::vector<std::vector<int>> lists(np);
+    std::vector<std::vector<FOp>> alts(np);
+    std::vector<char> has_alt(np, 0);
+    int carrier = -1;
+    for (std::size_t i = 0; i < np; ++i) {
+        lists[i] = plan.passes[i].ops;
+        if (lists[i].size() >= 2) has_alt[i] = missed_tile_program(ops_in, lists[i], alts[i]);
+        if (!has_alt[i] && carrier < 0) carrier = int(i);
+    }
+    std::vector<FOp> ext;  // ops_in plus the scales the deferral adds
+    bool extended = false;
+    auto add_op = [&](const FOp& f) {
+        if (!extended) {
+            ext = ops_in;
+            extended = true;
+        }
+        ext.push_back(f);
+        return int(ext.size()) - 1;
+    };
+    double carry = 1.0;
+    for (std::size_t i = 0; i < np && carrier >= 0; ++i) {
+        if (!has_alt[i] || alts[i].size() > 1 || (alts[i].size() == 1 && alts[i][0].kind != TOP_SCALE)) continue;
+        const double sc = alts[i].empty() ? 1.0 : alts[i][0].scale;
+        if (sc != 1.0) {
+            if (std::fabs(std::log2(std::fabs(carry * sc))) > 400.0) continue;  // keep clear of under/overflow
+            lists[i].push_back(add_op(make_scale(1.0 / sc)));
+            carry *= sc;
+        }
+        alts[i].clear();
+    }
+    if (carry != 1.0) {
+        auto& cl = lists[std::size_t(carrier)];
+        cl.insert(cl.begin(), add_op(make_scale(carry)));
+    }
+    const std::vector<FOp>& ops = extended ? ext : ops_in;
+    for (std::size_t pi = 0; pi < np; ++pi) {
+        const PlannedPass& pp = plan.passes[pi];
         PassParams P{};
         int loc[64];
         std::fill(loc, loc + 64, -1);
@@ -251,15 +341,18 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                 loc[b] = P.m;
                 P.bits[P.m++] = b;
             }
+        int nops = 0, nsign = 0;
+        std::uint64_t flip_off = 0, flip_cnt = 0;
         // rounds of <= 3 register bits; gates on 2-3 targets get shared-memory rounds
         struct RoundPlan {
             bool smem;
             unsigned mask;
             std::vector<int> ops;
         };
+        auto lower_list = [&](const std::vector<FOp>& src, const std::vector<int>& list) {
         std::vector<RoundPlan> rounds;
-        for (int idx : pp.ops) {
-            const FOp& f = ops[std::size_t(idx)];
+        for (int idx : list) {
+            const FOp& f = src[std::size_t(idx)];
             const bool smem = f.kind == TOP_GATE && f.K >= 2;
             unsigned t = 0;
             if (!elementwise(f))
@@ -283,8 +376,6 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
                 rounds.push_back({false, t, {idx}});
             }
         }
-        int nops = 0, nsign = 0;
-        std::uint64_t flip_off = 0, flip_cnt = 0;
         for (auto& r : rounds) {
             if (P.nrounds >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many rounds in a pass");
             unsigned mask = r.mask;
@@ -306,7 +397,7 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
             rd.op_begin = std::uint16_t(nops);
             bool pending_signs = false;  // a +-1 diagonal since the last butterfly / gate
             for (int idx : r.ops) {
-                const FOp& f = ops[std::size_t(idx)];
+                const FOp& f = src[std::size_t(idx)];
                 if (nops >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many operations in a pass");
                 RegOp o{};
                 o.kind = std::uint8_t(f.kind);
@@ -433,9 +524,58 @@ void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& o
             rd.op_count = std::uint16_t(nops - rd.op_begin);
             if (pending_signs) rd.flags = std::uint8_t(rd.flags | RD_SIGNS);
         }
+        };
+        lower_list(ops, lists[pi]);
+        // tiles that no sign step's listed indices reach see every sign step as a scalar +-1;
+        // there the pass often collapses (H_b H_b = 2 I for the unnormalised butterflies), so
+        // such passes carry a second, simplified program for those tiles
+        if (has_alt[pi]) {
+            const std::vector<FOp>& alt = alts[pi];
+            if (alt.empty()) {
+                P.alt_mode = ALT_SKIP;
+            } else if (nops + int(alt.size()) < kPassMaxOps && P.nrounds + int(alt.size()) < kPassMaxOps) {
+                std::vector<int> idx(alt.size());
+                for (std::size_t i = 0; i < alt.size(); ++i) idx[i] = int(i);
+                P.alt_begin = std::uint16_t(P.nrounds);
+                lower_list(alt, idx);
+                P.alt_nrounds = std::uint16_t(P.nrounds - P.alt_begin);
+                P.nrounds = P.alt_begin;  // the main program's rounds; the alternative follows
+                P.alt_mode = ALT_ROUNDS;
+            }
+        }
+        // the basis offset of each run of 8 (tile bits 3..m-1), copied into shared memory per tile
+        if (out.tables.size() & 1) out.tables.push_back(0);  // 16-byte aligned (cp.async)
+        P.hi_off = std::uint32_t(out.tables.size());
+        for (unsigned k = 0; k < (1u << (P.m - 3)); ++k) {
+            u64 v = 0;
+            for (int b = 3; b < P.m; ++b)
+                if (k >> (b - 3) & 1) v |= u64(1) << P.bits[b];
+            out.tables.push_back(v);
+        }
+        if (P.alt_mode == ALT_SKIP) {  // launch only the tiles a sign step reaches
+            std::vector<u64> hit;
+            for (int idx : lists[pi]) {
+                const FOp& f = ops[std::size_t(idx)];
+                if (f.kind != TOP_SIGN) continue;
+                for (u64 e : f.flips) {
+                    u64 tile = 0;  // e's bits outside the tile, compressed
+                    for (int b = 0, k = 0; b < n; ++b)
+                        if (!(pp.tile >> b & 1)) tile |= ((e >> b) & 1) << k++;
+                    hit.push_back(tile);
+                }
+            }
+            std::sort(hit.begin(), hit.end());
+            hit.erase(std::unique(hit.begin(), hit.end()), hit.end());
+            const u64 ntiles = u64(1) << (n - P.m);
+            if (!hit.empty() && hit.size() <= ntiles / 4) {
+                P.list_off = std::uint32_t(out.tables.size());
+                P.list_cnt = std::uint32_t(hit.size());
+                out.tables.insert(out.tables.end(), hit.begin(), hit.end());
+            }
+        }
         P.nops = nops;
         out.passes.push_back(P);
-        out.pass_ops.push_back(pp.ops);
+        out.pass_ops.push_back(lists[pi]);
         out.single_flip_off.push_back(flip_off);
         out.single_flip_cnt.push_back(flip_cnt);
     }

@@ -58,6 +58,7 @@ struct Lowered {
     std::vector<PassParams> passes;
     std::vector<TileOp> big;                 // shared-memory gates, sign steps, 3-bit diagonals
     std::vector<u64> flips;
+    std::vector<u64> tables;                 // per pass: run offsets (PassParams::hi_off), tile lists
     std::vector<std::vector<int>> pass_ops;  // FOp indices per pass
     std::vector<u64> single_flip_off, single_flip_cnt;  // sign step of a single-op pass
 };

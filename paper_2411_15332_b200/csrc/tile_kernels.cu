@@ -239,7 +239,7 @@ constexpr int kThreads = 256;
 #ifndef QCS_TILE_MINB
 #define QCS_TILE_MINB 2
 #endif
-#ifndef QCS_TILE_IO  // bit 0: first register round straight from HBM; bit 1: last straight to HBM
+#ifndef QCS_TILE_IO  // bit 1: last register round straight to HBM (bit 0, loads, measured slower: removed)
 #define QCS_TILE_IO 2
 #endif
 constexpr int kMaxBits = 12;
@@ -253,21 +253,16 @@ template <unsigned F>
 // passes with gates or diagonals trade residency for registers (QCS_TILE_MINB)
 __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_MINB : (F & F_SMEM) ? 2 : 3)
     k_tile(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,
-           const u64* __restrict__ flipped) {
+           const u64* __restrict__ flipped, const u64* __restrict__ tables) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = P.m;
     const unsigned sz = 1u << m;
     const unsigned ngroups = sz >> 3;  // 8 amplitudes per group
     double2* sm = reinterpret_cast<double2*>(smem_raw);
-    u64* hi_tab = reinterpret_cast<u64*>(sm + sz);  // basis offset of local bits 3..m-1
+    u64* hi_tab = reinterpret_cast<u64*>(sm + sz);  // basis offset of local bits 3..m-1 (host table)
     const unsigned t = threadIdx.x, bt = blockDim.x;
-    for (unsigned j = t; j < ngroups; j += bt) {
-        u64 v = 0;
-        for (int b = 3; b < m; ++b)
-            if (j >> (b - 3) & 1) v |= u64(1) << P.bits[b];
-        hi_tab[j] = v;
-    }
-    u64 base = blockIdx.x, tile_mask = 0;
+    for (unsigned j = 2 * t; j < ngroups; j += 2 * bt) cp_async16(hi_tab + j, tables + P.hi_off + j);
+    u64 base = P.list_cnt ? __ldg(tables + P.list_off + blockIdx.x) : u64(blockIdx.x), tile_mask = 0;
     for (int b = 0; b < m; ++b) {  // bits[] ascending: insert zeros from the lowest position up
         const int pos = P.bits[b];
         base = ((base >> pos) << (pos + 1)) | (base & ((u64(1) << pos) - 1));
@@ -286,20 +281,23 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
             if (hit) sign_hit |= 1u << (o.sidx & 31);
         }
     }
-    // a register round at either end reads its amplitudes straight from HBM (first) or writes
-    // them straight back (last): one shared-memory round trip less per amplitude at each end
-    // (only when bits 0..2 are not register bits: then a warp moves whole 128-byte runs)
-    const RoundDesc& R0 = P.rounds[0];
-    const RoundDesc& RL = P.rounds[P.nrounds - 1];
-    const bool io_first = (QCS_TILE_IO & 1) && !((F & F_SMEM) && (R0.flags & RD_SMEM)) && R0.r[0] >= 3;
-    const bool io_last = (QCS_TILE_IO & 2) && !((F & F_SMEM) && (RL.flags & RD_SMEM)) && RL.r[0] >= 3;
-    __syncthreads();
-    if (!io_first) {
-        for (unsigned j = t; j < sz; j += bt) cp_async16(sm + swz(j), a + (base | (j & 7u) | hi_tab[j >> 3]));
-        cp_async_wait_all();
-        __syncthreads();
+    // tiles no sign step reaches run the pass's simplified program (or nothing at all)
+    int rb = 0, re = P.nrounds;
+    if ((F & F_SIGN) && P.alt_mode != ALT_NONE && sign_hit == 0) {
+        if (P.alt_mode == ALT_SKIP) return;  // the pass is the identity here: no HBM traffic
+        rb = P.alt_begin;
+        re = rb + P.alt_nrounds;
     }
-    for (int ri = 0; ri < P.nrounds; ++ri) {
+    // a register round at the end writes its amplitudes straight back to HBM (one shared-memory
+    // round trip less); only when bits 0..2 are not register bits, so a warp stores whole runs
+    const RoundDesc& RL = P.rounds[re - 1];
+    const bool io_last = (QCS_TILE_IO & 2) && !((F & F_SMEM) && (RL.flags & RD_SMEM)) && RL.r[0] >= 3;
+    cp_async_wait_all();  // the run-offset table
+    __syncthreads();
+    for (unsigned j = t; j < sz; j += bt) cp_async16(sm + swz(j), a + (base | (j & 7u) | hi_tab[j >> 3]));
+    cp_async_wait_all();
+    __syncthreads();
+    for (int ri = rb; ri < re; ++ri) {
         const RoundDesc& R = P.rounds[ri];
         if ((F & F_SMEM) && (R.flags & RD_SMEM)) {
             for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
@@ -331,16 +329,8 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                 const unsigned g = gb + unsigned(r) * bt;
                 ok[r] = g < ngroups;
                 lb[r] = insert_zero(insert_zero(insert_zero(ok[r] ? g : gb, r0), r1), r2);
-                if (io_first && ri == 0) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const unsigned j = lb[r] | off[q];
-                        v[r][q] = a[base | (j & 7u) | hi_tab[j >> 3]];
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) v[r][q] = sm[swz(lb[r] | off[q])];
-                }
+                for (int q = 0; q < 8; ++q) v[r][q] = sm[swz(lb[r] | off[q])];
                 g0[r] = base | (lb[r] & 7u) | hi_tab[lb[r] >> 3];  // basis index of register 0
                 negacc[r] = 0;  // pending sign flips of the +-1 diagonals (they commute)
             }
@@ -422,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                 }
             }
             if ((F & F_DIAG) && (R.flags & RD_SIGNS)) flip_signs<NG>(v, negacc);
-            const bool to_hbm = io_last && ri == P.nrounds - 1;
+            const bool to_hbm = io_last && ri == re - 1;
 #pragma unroll
             for (int r = 0; r < NG; ++r) {
                 if (!ok[r]) continue;
@@ -446,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
 
 template <unsigned F>
 void launch_f(double2* amps, const PassParams& p, const TileOp* big_dev, const std::uint64_t* flipped_dev, unsigned tiles,
-              int threads, std::size_t smem, cudaStream_t st) {
+              const std::uint64_t* tables_dev, int threads, std::size_t smem, cudaStream_t st) {
     static bool attr_set[64] = {};  // per device and instantiation
     int dev = 0;
     QCS_CUDA(cudaGetDevice(&dev));
@@ -456,7 +446,7 @@ void launch_f(double2* amps, const PassParams& p, const TileOp* big_dev, const s
         QCS_CUDA(cudaFuncSetAttribute(k_tile<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr_set[dev] = true;
     }
-    k_tile<F><<<tiles, threads, smem, st>>>(amps, p, big_dev, flipped_dev);
+    k_tile<F><<<tiles, threads, smem, st>>>(amps, p, big_dev, flipped_dev, tables_dev);
 }
 
 }  // namespace
@@ -464,10 +454,11 @@ void launch_f(double2* amps, const PassParams& p, const TileOp* big_dev, const s
 int tile_max_bits() { return kMaxBits; }
 
 void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* big_dev, const std::uint64_t* flipped_dev,
-                      cudaStream_t st) {
+                      const std::uint64_t* tables_dev, cudaStream_t st) {
     if (p.m < 3 || p.m > kMaxBits || p.m > n) raise(QCS_ERR_ARG, "tile bits out of range");
-    const std::size_t smem = (std::size_t(1) << p.m) * sizeof(double2) + (std::size_t(1) << (p.m - 3)) * sizeof(u64);
-    const u64 tiles = u64(1) << (n - p.m);
+    // the tile, then its run-offset table (copied in 16-byte pieces)
+    const std::size_t smem = (std::size_t(1) << p.m) * sizeof(double2) + std::max<std::size_t>(16, (std::size_t(1) << (p.m - 3)) * sizeof(u64));
+    const u64 tiles = p.list_cnt ? u64(p.list_cnt) : u64(1) << (n - p.m);
     if (tiles > 0x7fffffffull) raise(QCS_ERR_CAPACITY, "too many tiles for one launch");
     const int threads = std::min(kThreads, std::max(32, 1 << (p.m - 3)));
     unsigned f = 0;
@@ -479,10 +470,10 @@ void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* b
         if (kind == TOP_DIAG) f |= F_DIAG;
         if (kind == TOP_SIGN) f |= F_SIGN;
     }
-    TimedLaunch tl("tile_pass", 32.0 * double(u64(1) << n), st);
+    TimedLaunch tl("tile_pass", 32.0 * double(tiles) * double(1u << p.m), st);
     switch (f) {
 #define QCS_TILE_CASE(x) \
-    case x: launch_f<x>(amps, p, big_dev, flipped_dev, unsigned(tiles), threads, smem, st); break;
+    case x: launch_f<x>(amps, p, big_dev, flipped_dev, unsigned(tiles), tables_dev, threads, smem, st); break;
         QCS_TILE_CASE(0) QCS_TILE_CASE(1) QCS_TILE_CASE(2) QCS_TILE_CASE(3) QCS_TILE_CASE(4) QCS_TILE_CASE(5)
         QCS_TILE_CASE(6) QCS_TILE_CASE(7) QCS_TILE_CASE(8) QCS_TILE_CASE(9) QCS_TILE_CASE(10) QCS_TILE_CASE(11)
         QCS_TILE_CASE(12) QCS_TILE_CASE(13) QCS_TILE_CASE(14) QCS_TILE_CASE(15)
