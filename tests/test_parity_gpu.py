@@ -156,6 +156,38 @@ def test_grover_golden_reference(Q, golden):
         assert np.abs(rep.final.download() - g[f"n{n}"]).max() <= 1e-12
 
 
+@pytest.mark.parametrize("n", [13, 16, 19])
+def test_sign_sandwiches_fused_vs_oracle(Q, oracle, n):
+    """Sign steps between H^n steps and gates: the fused planner runs the tiles no sign step
+    reaches with a simplified (often empty) program.  Lists of 1, 5 and 80 (> 64: searched
+    per element) indices, flip_rest both ways, against the oracle step by step."""
+    rng = np.random.default_rng(n)
+    H = Q.hadamard_all(n)
+    ry = Q.gate_catalog_lookup("RY", [0.37])
+    signs = [Q.DiagSign([int(i) for i in rng.choice(1 << n, k, replace=False)], rest)
+             for k, rest in ((1, False), (1, True), (5, False), (80, True), (0, True), (3, True))]
+    steps = [H]
+    for d in signs:
+        steps += [Q.CircuitStep.of_diag(d), H]
+    steps.insert(4, Q.CircuitStep.of_gates([Q.Placement(ry, 2)]))
+    c = Q.Circuit(n, steps)
+    st = Q.plan_stats(c)
+    assert st["alt_passes"] > 0
+    x = np.zeros(1 << n, np.complex128)
+    x[0] = 1
+    for step in steps:
+        if step.is_hadamard_all(n):
+            x = oracle.wht(n, x)
+        elif int(step.kind) == 1:
+            x = oracle.apply_diag(n, sorted(set(step.diag.flipped)), step.diag.flip_rest, x)
+        else:
+            x = oracle.apply_step(n, [(p.qubit_list(), p.gate.matrix) for p in step.placements], x)
+    for fuse in (True, False):
+        got = Q.simulate(c, Q.Engine.rh_dax, Q.SimOptions(fuse=fuse)).final.download()
+        assert np.abs(got - x).max() <= TOL_AMP, fuse
+        assert np.linalg.norm(got - x) <= TOL_L2, fuse
+
+
 # ------------------------------------------------------------------ whole circuits
 def test_c1_against_reference_golden(Q, cfg, golden):
     g = golden("c1.npz")

@@ -25,6 +25,15 @@ def test_c3_grover_pass_count():
     assert Q.plan_stats(configs.c3_circuit(30), opts=STEPWISE)["passes"] > st["passes"]
 
 
+def test_grover_sign_passes_skip_missed_tiles():
+    # each oracle / Z0 step sits in a pass mirrored around it (H_b ... sign ... H_b): on the
+    # tiles it does not reach the pass is a scalar, carried by another pass, so only the
+    # reached tiles are launched
+    for n in (22, 30):
+        st = Q.plan_stats(configs.c3_circuit(n))
+        assert st["skip_passes"] == st["alt_passes"] == 16, n
+
+
 def test_rh_is_ceil_passes():
     # H on every qubit: a 12-bit tile takes bits 0..11, later tiles 9 new bits each (0..2 fixed)
     for n, want in [(12, 1), (21, 2), (28, 3), (30, 3), (32, 4)]:
