@@ -19,15 +19,14 @@ QCS_STEP_GATES, QCS_STEP_DIAG = 0, 1
 MAX_ARITY = 3
 
 
+# pointer members as void* (same ABI): plain integer addresses assign without ctypes casts
 class qcs_placement(C.Structure):
-    _fields_ = [("arity", C.c_int), ("qubits", C.POINTER(C.c_int)), ("matrix", C.POINTER(C.c_double)),
-                ("name", C.c_char_p)]
+    _fields_ = [("arity", C.c_int), ("qubits", C.c_void_p), ("matrix", C.c_void_p), ("name", C.c_char_p)]
 
 
 class qcs_step(C.Structure):
-    _fields_ = [("kind", C.c_int), ("stage", C.c_int), ("placements", C.POINTER(qcs_placement)),
-                ("num_placements", C.c_int), ("flipped", C.POINTER(C.c_uint64)), ("num_flipped", C.c_uint64),
-                ("flip_rest", C.c_int)]
+    _fields_ = [("kind", C.c_int), ("stage", C.c_int), ("placements", C.c_void_p), ("num_placements", C.c_int),
+                ("flipped", C.c_void_p), ("num_flipped", C.c_uint64), ("flip_rest", C.c_int)]
 
 
 class qcs_sim_options(C.Structure):

@@ -466,40 +466,58 @@ StateVector = DeviceState
 
 
 def _placements(placements: Sequence[Placement]):
-    """-> (ctypes array of qcs_placement, keep-alive list)."""
-    arr = (L.qcs_placement * max(1, len(placements)))()
-    keep = []
-    for i, p in enumerate(placements):
-        qs = np.ascontiguousarray(np.asarray(p.qubit_list(), dtype=np.int32))
-        m = np.ascontiguousarray(np.asarray(p.gate.matrix, dtype=np.complex128))
-        if m.size != 4 ** p.gate.arity or qs.size != p.gate.arity:
+    """-> (ctypes array of qcs_placement, keep-alive list).  Qubits and matrices of all the
+    placements are packed into one int32 and one complex128 array (two numpy calls, not two per
+    placement): marshalling dominates the host cost of small circuits."""
+    n = len(placements)
+    arr = (L.qcs_placement * max(1, n))()
+    if n == 0:
+        return arr, []
+    qlists = [p.qubit_list() for p in placements]
+    mats = [p.gate.matrix for p in placements]
+    for p, q, m in zip(placements, qlists, mats):
+        if len(q) != p.gate.arity or np.size(m) != 4 ** p.gate.arity:
             raise DimensionError("placement matrix / qubit count does not match the gate arity")
-        name = p.gate.name.encode()
-        keep += [qs, m, name]
-        arr[i].arity = p.gate.arity
-        arr[i].qubits = qs.ctypes.data_as(C.POINTER(C.c_int))
-        arr[i].matrix = m.ctypes.data_as(C.POINTER(C.c_double))
-        arr[i].name = name
-    return arr, keep
+    qs = np.fromiter((x for q in qlists for x in q), dtype=np.int32)
+    ms = np.concatenate([np.asarray(m, dtype=np.complex128).ravel() for m in mats])
+    names = [p.gate.name.encode() for p in placements]
+    qa, ma = qs.ctypes.data, ms.ctypes.data
+    qo = mo = 0
+    for i, p in enumerate(placements):
+        k = p.gate.arity
+        e = arr[i]
+        e.arity = k
+        e.qubits = qa + 4 * qo
+        e.matrix = ma + 16 * mo
+        e.name = names[i]
+        qo += k
+        mo += 1 << (2 * k)
+    return arr, [qs, ms, names]
 
 
 def _steps(steps: Sequence[CircuitStep]):
     arr = (L.qcs_step * max(1, len(steps)))()
     keep = []
+    gate_steps = [st for st in steps if st.kind != StepKind.diag]
+    pa, k = _placements([p for st in gate_steps for p in st.placements])
+    keep += [pa, k]
+    base = C.addressof(pa)
+    size = C.sizeof(L.qcs_placement)
+    off = 0
     for i, st in enumerate(steps):
-        arr[i].kind = int(st.kind)
-        arr[i].stage = st.stage
+        e = arr[i]
+        e.kind = int(st.kind)
+        e.stage = st.stage
         if st.kind == StepKind.diag:
             f = np.ascontiguousarray(np.asarray(st.diag.flipped, dtype=np.uint64))
             keep.append(f)
-            arr[i].flipped = f.ctypes.data_as(C.POINTER(C.c_uint64)) if f.size else None
-            arr[i].num_flipped = f.size
-            arr[i].flip_rest = int(st.diag.flip_rest)
+            e.flipped = f.ctypes.data if f.size else None
+            e.num_flipped = f.size
+            e.flip_rest = int(st.diag.flip_rest)
         else:
-            pa, k = _placements(st.placements)
-            keep += [pa, k]
-            arr[i].placements = C.cast(pa, C.POINTER(L.qcs_placement))
-            arr[i].num_placements = len(st.placements)
+            e.placements = base + size * off
+            e.num_placements = len(st.placements)
+            off += len(st.placements)
     return arr, keep
 
 
