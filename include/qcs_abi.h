@@ -117,6 +117,21 @@ int qcs_apply_step(qcs_state* s, const qcs_placement* placements, int count);
  * index is listed XOR flip_rest.  Bit-exact. */
 int qcs_apply_diag(qcs_state* s, const uint64_t* flipped, uint64_t count, int flip_rest);
 
+/* A one-qubit gate (optionally controlled by local qubits) on a shard-GLOBAL qubit of a state
+ * sharded by its top qubits, computed straight over peer memory: `s` is this rank's shard,
+ * `peer_amps` the partner shard (the rank differing in that global bit), mapped into this
+ * device's address space (NVLink P2P; on one device, another buffer).  This rank takes the
+ * pairs whose local top bit equals self_bit (its own value of the global qubit), loads the
+ * partner amplitude, and stores both outputs.  Blocks: 2^num_sel matrices of 2x2 complex
+ * (interleaved, row-major m00 m01 m10 m11) on the global qubit, block v selected by the local
+ * basis bits sel_bits[0..num_sel-1] (most significant first); skip_mask bit v = block v is the
+ * identity and is not touched.  dax_mvm arithmetic: bit-exact with the unsharded gate.
+ * Both ranks call it for the same gate; the caller orders it after the partner's previous
+ * work on its shard and before the partner's next (a barrier on each side).  B200-specific:
+ * the reference has no multi-device code. */
+int qcs_apply_split(qcs_state* s, void* peer_amps, int self_bit, int num_sel, const int* sel_bits,
+                    const double* blocks, uint32_t skip_mask);
+
 /* rh_mvm(rh_build(n), s) (rh.hpp:64-66): H^{(x)n} as a Walsh-Hadamard butterfly, scaled once
  * by exp2(-n/2) (rh.cpp:20).  Within 1e-12 of the reference (whose own error is larger). */
 int qcs_apply_rh(qcs_state* s);

@@ -86,6 +86,7 @@ SIGNATURES = {
     "qcs_simulate": (C.c_int, [_P, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
                                C.POINTER(qcs_step_report)]),
     "qcs_memory_report": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_step_report)]),
+    "qcs_apply_split": (C.c_int, [_P, _P, C.c_int, C.c_int, _I, _D, C.c_uint32]),
     "qcs_plan_stats": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
                                  C.POINTER(qcs_plan_info)]),
     "qcs_step_dax": (C.c_int, [C.c_int, C.POINTER(qcs_placement), C.c_int, C.c_int, _P, _P, _P, C.c_uint64,

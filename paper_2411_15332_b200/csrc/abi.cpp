@@ -226,6 +226,14 @@ int qcs_apply_diag(qcs_state* s, const uint64_t* flipped, uint64_t count, int fl
     });
 }
 
+int qcs_apply_split(qcs_state* s, void* peer_amps, int self_bit, int num_sel, const int* sel_bits,
+                    const double* blocks, uint32_t skip_mask) {
+    return guarded([&] {
+        need(s, "state");
+        qcs::apply_split(s, peer_amps, self_bit, num_sel, sel_bits, blocks, skip_mask);
+    });
+}
+
 int qcs_apply_rh(qcs_state* s) {
     return guarded([&] {
         need(s, "state");

@@ -197,6 +197,33 @@ void apply_diag(qcs_state* s, const u64* flipped, u64 count, int flip_rest) {
     // the host vector may be freed: pageable cudaMemcpyAsync has staged it before returning
 }
 
+void apply_split(qcs_state* s, void* peer, int self_bit, int nsel, const int* sel, const double* blocks,
+                 unsigned skip) {
+    if (!peer) raise(QCS_ERR_ARG, "null peer shard");
+    if (s->n < 1) raise(QCS_ERR_DIMENSION, "the shard needs a local qubit");
+    if (self_bit != 0 && self_bit != 1) raise(QCS_ERR_ARG, "self_bit must be 0 or 1");
+    if (nsel < 0 || nsel > 2) raise(QCS_ERR_ARG, "at most two selector bits");
+    if (!blocks) raise(QCS_ERR_ARG, "null blocks");
+    SplitParams p{};
+    p.nl = s->n;
+    p.self_bit = self_bit;
+    p.nsel = nsel;
+    p.skip = skip & ((1u << (1 << nsel)) - 1);
+    for (int i = 0; i < nsel; ++i) {
+        if (!sel || sel[i] < 0 || sel[i] >= s->n) raise(QCS_ERR_DIMENSION, "selector bit out of range");
+        p.sel[i] = sel[i];
+    }
+    for (int v = 0; v < (1 << nsel); ++v)
+        for (int k = 0; k < 4; ++k) {
+            const double re = blocks[8 * v + 2 * k], im = blocks[8 * v + 2 * k + 1];
+            p.m[v][k] = make_double2(re, im);
+            if (re != 0.0 || im != 0.0) p.nz[v] = static_cast<unsigned char>(p.nz[v] | (1u << k));
+        }
+    DeviceGuard g(s->device);
+    TimerScope ts(s);
+    launch_split_pair(s->amps, static_cast<double2*>(peer), p, s->stream);
+}
+
 namespace {
 
 void ensure_plan(qcs_state* s, std::size_t bytes) {

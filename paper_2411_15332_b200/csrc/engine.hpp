@@ -48,6 +48,8 @@ void apply_rh(qcs_state* s);
 
 void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
               qcs_step_report* reports);
+void apply_split(qcs_state* s, void* peer, int self_bit, int nsel, const int* sel, const double* blocks,
+                 unsigned skip);
 void plan_stats(int n, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
                 qcs_plan_info* out);
 void memory_report(int n, const qcs_step* steps, int nsteps, int engine, qcs_step_report* reports);

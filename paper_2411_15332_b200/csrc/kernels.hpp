@@ -132,6 +132,20 @@ void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* b
                       const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, cudaStream_t st);
 int tile_max_bits();
 
+// A gate on a shard-global qubit over peer memory (peer_kernels.cu): blocks v (selected by the
+// local bits sel[0..nsel-1], most significant first) are 2x2 matrices m00 m01 m10 m11 on the
+// global qubit; skip bit v = block v is the identity.
+struct SplitParams {
+    int nl;          // local qubits of the shard
+    int self_bit;    // this rank's value of the global qubit
+    int nsel;        // <= 2
+    int sel[2];      // local basis-bit positions selecting the block
+    unsigned skip;
+    unsigned char nz[4];  // bit k: entry k of block v is nonzero
+    double2 m[4][4];
+};
+void launch_split_pair(double2* self, double2* peer, const SplitParams& p, cudaStream_t st);
+
 // ---------------------------------------------------------------- reductions
 double reduce_norm2(const double2* amps, int n, double* scratch_dev, cudaStream_t st);
 void probabilities(const double2* amps, std::uint64_t dim, double* out_dev, cudaStream_t st);

@@ -7,6 +7,11 @@ physical qubit map lets qubits move between the global and the local part lazily
 * a gate whose matrix does not mix values of its global qubits (diagonal gates, controls on
   global qubits, the C4 CZ ring) is reduced to the block selected by the rank's global bits and
   applied locally -- no communication;
+* a gate that mixes exactly one qubit, a global one (H, RX, RY, U3, X, Y on a global qubit;
+  CNOT / Toffoli with local controls and a global target), runs as one kernel over peer
+  memory when the transport maps the partner shard (``peer_buffer``): each rank takes half of
+  the amplitude pairs, loads the partner's amplitude over NVLink and stores both outputs
+  (qcs_apply_split) -- the exchange and the arithmetic are fused, nothing is staged;
 * any other gate touching a global qubit first swaps that qubit with the most significant
   local qubit: the ranks r and r ^ bit exchange one contiguous half of their shards (pairwise
   send/recv, chunked through a bounded staging buffer), the map records the swap, and the gate
@@ -17,7 +22,8 @@ physical qubit map lets qubits move between the global and the local part lazily
   rank negates the ones it owns (or all but those).
 
 Communication uses torch.distributed point-to-point operations (NCCL over NVLink on the GPU
-box; gloo in the CPU tests).  Local compute goes through a backend: ``DeviceBackend`` runs the
+box; gloo in the CPU tests) for the swaps, and peer loads/stores (torch symmetric memory,
+``SymmetricTransport``) for the fused gates.  Local compute goes through a backend: ``DeviceBackend`` runs the
 B200 kernels through the C ABI on a torch-owned device shard (``qcs_state_wrap``); the tests
 plug in CPU backends.  Nothing here touches amplitudes on the host in the device path.
 """
@@ -36,7 +42,7 @@ def _bits(x: int, n: int) -> List[int]:
 class DeviceBackend:
     """A local shard of n_local qubits in a torch CUDA tensor, updated by libqcs_b200 kernels."""
 
-    def __init__(self, n_local: int, device: int = 0):
+    def __init__(self, n_local: int, device: int = 0, symmetric: bool = False):
         import torch
 
         from . import qcsim as Q
@@ -44,7 +50,12 @@ class DeviceBackend:
         self.Q = Q
         self.n = n_local
         self.device = device
-        self.tensor = torch.zeros(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}")
+        if symmetric:  # peer-mappable (torch symmetric memory): SymmetricTransport rendezvous
+            import torch.distributed._symmetric_memory as symm_mem
+            self.tensor = symm_mem.empty(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}")
+            self.tensor.zero_()
+        else:
+            self.tensor = torch.zeros(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}")
         stream = torch.cuda.current_stream(device).cuda_stream
         import ctypes as C
         h = C.c_void_p()
@@ -79,6 +90,11 @@ class DeviceBackend:
                 steps.append(Q.hadamard_all(self.n))
         if steps:
             Q.run(Q.Circuit(self.n, steps), self.state, Q.Engine.rh_dax)
+
+    def apply_split(self, peer, self_bit: int, sel_bits: Sequence[int], blocks: np.ndarray, skip: int) -> None:
+        """A gate on a global qubit, fused with the exchange: `peer` is the partner shard
+        (a tensor in this device's address space)."""
+        self.state.apply_split(peer.data_ptr(), self_bit, sel_bits, blocks, skip)
 
     def half(self, upper: bool):
         h = 1 << (self.n - 1)
@@ -115,11 +131,29 @@ class DistTransport:
             req.wait()
 
 
+class SymmetricTransport(DistTransport):
+    """DistTransport plus the partner shards mapped over NVLink (torch symmetric memory): the
+    fused global-qubit gates load and store them directly.  The backend must be a
+    DeviceBackend(..., symmetric=True); `attach` is collective."""
+
+    def attach(self, backend) -> None:
+        import torch.distributed._symmetric_memory as symm_mem
+        self.backend = backend
+        self.handle = symm_mem.rendezvous(backend.tensor, self.dist.group.WORLD)
+
+    def peer_buffer(self, peer: int):
+        import torch
+        return self.handle.get_buffer(peer, (self.backend.tensor.numel(),), torch.complex128)
+
+    def barrier(self) -> None:
+        self.handle.barrier(channel=0)  # stream-ordered: orders the GPU work on every rank
+
+
 class ShardedState:
     """An n-qubit state sharded over `world` ranks (a power of two); this object is rank `rank`."""
 
     def __init__(self, n: int, world: int, rank: int, backend, transport=None, initial: int = 0,
-                 chunk_elems: int = 1 << 24):
+                 chunk_elems: int = 1 << 24, peer: Optional[bool] = None):
         g = int(round(math.log2(world)))
         if 1 << g != world:
             raise ValueError("world size must be a power of two")
@@ -133,6 +167,12 @@ class ShardedState:
         self.swaps = 0              # global<->local exchanges performed
         self.exchanged_bytes = 0    # bytes sent by this rank
         self.pending = []           # local operations not yet handed to the backend
+        self.splits = 0             # gates run over peer memory (no exchange)
+        can_peer = (transport is not None and hasattr(transport, "peer_buffer") and hasattr(transport, "barrier")
+                    and hasattr(backend, "apply_split"))
+        self.peer = can_peer if peer is None else (bool(peer) and can_peer)
+        if self.peer and hasattr(transport, "attach"):
+            transport.attach(backend)
         self.set_basis(initial)
 
     # ------------------------------------------------------------ index mapping
@@ -228,6 +268,8 @@ class ShardedState:
                 sub = m[np.ix_(sel, sel)]
                 self._local(("gate", sub, [phys[i] - self.g for i in loc], name))
                 return
+            if self.peer and self._split_gate(m, phys, name):
+                return
             # bring each mixing global qubit local (swap with the top local qubit, which must
             # not be one of this gate's own qubits: move it aside first if needed)
             for i in glob:
@@ -243,6 +285,42 @@ class ShardedState:
                 self._swap_global_local(self.phys[logical_qubits[i]], top)
             phys = [self.phys[q] for q in logical_qubits]
         self._local(("gate", m, [p - self.g for p in phys], name))
+
+    def _split_gate(self, m: np.ndarray, phys: List[int], name: str) -> bool:
+        """The gate mixes exactly one of its qubits and that one is global: run it over peer
+        memory (qcs_apply_split).  Its other qubits only select 2x2 blocks -- global ones by
+        this rank's bits, local ones (<= 2) per amplitude.  False: not of that form."""
+        k = len(phys)
+        r_idx, c_idx = np.nonzero(m)
+        mixing = [i for i in range(k) if np.any(((r_idx ^ c_idx) >> (k - 1 - i)) & 1)]
+        if len(mixing) != 1 or phys[mixing[0]] >= self.g:
+            return False
+        ig = mixing[0]
+        sel = [i for i in range(k) if i != ig and phys[i] >= self.g]
+        if len(sel) > 2:
+            return False
+        fixed = sum(self._rank_bit(phys[i]) << (k - 1 - i) for i in range(k) if i != ig and phys[i] < self.g)
+        nl = self.n - self.g
+        sel_bits = [nl - 1 - (phys[i] - self.g) for i in sel]
+        nb = 1 << len(sel)
+        blocks = np.zeros((nb, 2, 2), dtype=np.complex128)
+        skip = 0
+        for v in range(nb):
+            base = fixed | sum(((v >> (len(sel) - 1 - t)) & 1) << (k - 1 - sel[t]) for t in range(len(sel)))
+            idx = [base, base | (1 << (k - 1 - ig))]
+            blocks[v] = m[np.ix_(idx, idx)]
+            if np.array_equal(blocks[v], np.eye(2)):
+                skip |= 1 << v
+        # every rank takes part in both barriers (they are world-wide); a rank pair whose blocks
+        # are all the identity (a global control that is off) launches nothing
+        self.flush()
+        self.transport.barrier()  # the partner's earlier work on its shard is done
+        if skip != (1 << nb) - 1:
+            self.backend.apply_split(self.transport.peer_buffer(self.rank ^ (1 << (self.g - 1 - phys[ig]))),
+                                     self._rank_bit(phys[ig]), sel_bits, blocks, skip)
+            self.splits += 1
+        self.transport.barrier()  # ... and ours before either shard is used again
+        return True
 
     def _local_swap(self, pa: int, pb: int) -> None:
         swap = np.eye(4, dtype=np.complex128)[[0, 2, 1, 3]]

@@ -421,6 +421,15 @@ class DeviceState:
         _check(L.lib().qcs_apply_diag(self._h, f.ctypes.data_as(C.POINTER(C.c_uint64)) if f.size else None,
                                       f.size, int(d.flip_rest)))
 
+    def apply_split(self, peer_ptr: int, self_bit: int, sel_bits: Sequence[int], blocks: np.ndarray,
+                    skip_mask: int = 0) -> None:
+        """A gate on a shard-global qubit over the partner shard at device address `peer_ptr`
+        (qcs_apply_split; partition.py drives it).  blocks: (2^len(sel_bits), 2, 2) complex."""
+        b = np.ascontiguousarray(np.asarray(blocks, dtype=np.complex128).reshape(-1, 2, 2))
+        sel = (C.c_int * max(1, len(sel_bits)))(*[int(x) for x in sel_bits])
+        _check(L.lib().qcs_apply_split(self._h, C.c_void_p(int(peer_ptr)), int(self_bit), len(sel_bits), sel,
+                                       b.ctypes.data_as(C.POINTER(C.c_double)), int(skip_mask)))
+
     def apply_rh(self) -> None:
         _check(L.lib().qcs_apply_rh(self._h))
 

@@ -35,6 +35,28 @@ class OracleBackend:
         base = (1 << (self.n - 1)) if upper else 0
         return self.tensor[base + start: base + start + count]
 
+    def apply_split(self, peer, self_bit, sel_bits, blocks, skip):
+        """qcs_apply_split's contract on the CPU: this rank's half of the pairs, both outputs,
+        dax_mvm order (acc = 0; += m[r][c] * x_c over the nonzero entries, ascending c)."""
+        half = 1 << (self.n - 1)
+        mine, other = self.tensor.numpy(), peer.numpy()
+        for j in range(half):
+            i = (half if self_bit else 0) | j
+            v = 0
+            for b in sel_bits:
+                v = (v << 1) | ((i >> b) & 1)
+            if skip >> v & 1:
+                continue
+            x = (other[i], mine[i]) if self_bit else (mine[i], other[i])
+            out = []
+            for r in range(2):
+                acc = 0j
+                for c in range(2):
+                    if blocks[v][r][c] != 0:
+                        acc = acc + blocks[v][r][c] * x[c]
+                out.append(acc)
+            mine[i], other[i] = (out[1], out[0]) if self_bit else (out[0], out[1])
+
     def empty(self, count):
         return torch.empty(count, dtype=torch.complex128)
 
@@ -46,14 +68,19 @@ class OracleBackend:
 
 
 class ThreadTransport:
-    """P threads in one process exchanging through mailboxes (an emulated fabric)."""
+    """P threads in one process exchanging through mailboxes (an emulated fabric).  With
+    peers=True the endpoints also map the other shards (peer_buffer) and share a barrier: the
+    emulated NVLink of the fused global-qubit gates."""
 
-    def __init__(self):
+    def __init__(self, world=None, peers=False):
         self.cv = threading.Condition()
         self.box = {}
+        self.peers = peers
+        self.backends = {}
+        self.bar = threading.Barrier(world) if peers else None
 
     def endpoint(self, rank):
-        return _Endpoint(self, rank)
+        return _PeerEndpoint(self, rank) if self.peers else _Endpoint(self, rank)
 
 
 class _Endpoint:
@@ -68,6 +95,20 @@ class _Endpoint:
                 self.hub.cv.wait()
             data = self.hub.box[(peer, self.rank)].pop(0)
         recv.copy_(data)
+
+
+class _PeerEndpoint(_Endpoint):
+    def attach(self, backend):
+        self.hub.backends[self.rank] = backend
+        self.hub.bar.wait()
+
+    def peer_buffer(self, peer):
+        return self.hub.backends[peer].tensor
+
+    def barrier(self):
+        # GPU emulation: every rank's kernels go to the device's default stream, so a host
+        # barrier after issuing orders them
+        self.hub.bar.wait()
 
 
 def run_ranks(world, fn):

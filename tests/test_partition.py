@@ -51,6 +51,61 @@ def test_threads_match_full_state(oracle, world, name):
     assert sum(o[0].swaps for o in outs) > 0 or name == "c1" and world == 2
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name", ["c4", "c5", "grover", "c1"])
+def test_threads_peer_gates_match_full_state(oracle, world, name):
+    """Peer mode: gates mixing only a global qubit run over the partner shard (the CPU model of
+    qcs_apply_split), everything else as before."""
+    from paper_2411_15332_b200.partition import ShardedState
+    c = circuits()[name]
+    want = oracle_full(oracle, c)
+    hub = ThreadTransport(world, peers=True)
+    g = world.bit_length() - 1
+
+    def rank_fn(r):
+        st = ShardedState(c.n, world, r, OracleBackend(c.n - g, oracle), hub.endpoint(r), initial=c.initial,
+                          chunk_elems=7)
+        assert st.peer
+        run_ops(st, circuit_ops(c))
+        return st, st.local_numpy()
+
+    outs = run_ranks(world, rank_fn)
+    got = gather([o[0] for o in outs], [o[1] for o in outs])
+    assert np.abs(got - want).max() < 1e-12
+    if name in ("c4", "grover"):  # H / RY on global qubits: no exchange at all
+        assert all(o[0].swaps == 0 and o[0].splits > 0 for o in outs)
+
+
+def test_split_blocks_for_controlled_gates(oracle):
+    """CNOT / Toffoli with local controls and a global target, CNOT with a global control
+    (identity blocks on half the ranks), a global-target Swap (two mixing qubits: swap path)."""
+    from paper_2411_15332_b200 import qcsim as Q
+    from paper_2411_15332_b200.partition import ShardedState
+    n, world = 7, 4
+    rng = np.random.default_rng(3)
+    G = Q.gate_catalog_lookup
+    steps = [Q.hadamard_all(n),
+             Q.CircuitStep.of_gates([Q.Placement(G("RY", [0.3]), 4)]),
+             Q.CircuitStep.of_gates([Q.Placement(G("CNOT"), qubits=[5, 0])]),
+             Q.CircuitStep.of_gates([Q.Placement(G("Toffoli"), qubits=[6, 3, 1])]),
+             Q.CircuitStep.of_gates([Q.Placement(G("CNOT"), qubits=[1, 0])]),
+             Q.CircuitStep.of_gates([Q.Placement(G("U", [float(x) for x in rng.uniform(0, 6, 3)]), 1)]),
+             Q.CircuitStep.of_gates([Q.Placement(G("Swap"), qubits=[0, 5])]),
+             Q.CircuitStep.of_gates([Q.Placement(G("RX", [1.1]), 0)])]
+    c = Q.Circuit(n, steps)
+    want = oracle_full(oracle, c)
+    hub = ThreadTransport(world, peers=True)
+
+    def rank_fn(r):
+        st = ShardedState(n, world, r, OracleBackend(n - 2, oracle), hub.endpoint(r), chunk_elems=3)
+        run_ops(st, circuit_ops(c))
+        return st, st.local_numpy()
+
+    outs = run_ranks(world, rank_fn)
+    assert np.abs(gather([o[0] for o in outs], [o[1] for o in outs]) - want).max() < 1e-12
+    assert all(o[0].splits >= 3 and o[0].swaps >= 1 for o in outs)
+
+
 def test_global_controls_and_diagonals_need_no_exchange(oracle):
     from paper_2411_15332_b200 import qcsim as Q
     from paper_2411_15332_b200.partition import ShardedState

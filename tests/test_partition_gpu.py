@@ -32,3 +32,60 @@ def test_emulated_ranks_match_single_gpu(world):
         assert np.abs(got - want).max() < 1e-12
         assert np.linalg.norm(got - want) < 1e-10
         assert all(o[0].swaps > 0 for o in outs)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_emulated_peer_gates_match_single_gpu(world):
+    """Peer mode on one GPU: the P shards are P buffers on the device, so qcs_apply_split's
+    partner loads/stores are plain device accesses (NVLink P2P on a multi-GPU box)."""
+    from paper_2411_15332_b200 import configs
+    from paper_2411_15332_b200 import qcsim as Q
+    from paper_2411_15332_b200.partition import DeviceBackend, ShardedState
+    g = world.bit_length() - 1
+    for c in (configs.c4_circuit(n=16, layers=2), configs.c5_circuit(n=17, layers=2, global_qubits=g),
+              Q.build_grover(15, 12345, 3)):
+        want = Q.simulate(c, Q.Engine.rh_dax).final.download()
+        hub = ThreadTransport(world, peers=True)
+
+        def rank_fn(r):
+            st = ShardedState(c.n, world, r, DeviceBackend(c.n - g), hub.endpoint(r), initial=c.initial,
+                              chunk_elems=1 << 12)
+            assert st.peer
+            run_ops(st, circuit_ops(c))
+            return st, st.local_numpy()
+
+        outs = run_ranks(world, rank_fn)
+        got = gather([o[0] for o in outs], [o[1] for o in outs])
+        assert np.abs(got - want).max() < 1e-12
+        assert np.linalg.norm(got - want) < 1e-10
+        assert all(o[0].splits > 0 for o in outs)
+
+
+def test_split_gate_bit_exact():
+    """One gate on a global qubit through qcs_apply_split equals the single-GPU gate kernel
+    bit for bit (both follow dax_mvm's arithmetic)."""
+    from conftest import bits_equal, random_state
+    from paper_2411_15332_b200 import qcsim as Q
+    from paper_2411_15332_b200.partition import DeviceBackend, ShardedState
+    n, world = 14, 4
+    x = random_state(n, 11)
+    G = Q.gate_catalog_lookup
+    for gate, qubits in ((G("Hadamard"), [0]), (G("U", [0.3, 1.7, 2.9]), [1]), (G("CNOT"), [6, 0]),
+                         (G("Toffoli"), [9, 4, 1]), (G("Pauli-Y"), [0])):
+        s = Q.DeviceState.from_numpy(x)
+        s.apply_gate(gate, qubits)
+        want = s.download()
+        hub = ThreadTransport(world, peers=True)
+
+        def rank_fn(r):
+            import torch
+            st = ShardedState(n, world, r, DeviceBackend(n - 2), hub.endpoint(r))
+            local = x.reshape(world, -1)[r]
+            st.backend.tensor.copy_(torch.from_numpy(local.copy()))
+            st.apply_gate(gate.matrix, qubits, gate.name)
+            return st, st.local_numpy()
+
+        outs = run_ranks(world, rank_fn)
+        got = gather([o[0] for o in outs], [o[1] for o in outs])
+        assert all(o[0].splits == 1 and o[0].swaps == 0 for o in outs), gate.name
+        assert bits_equal(got, want), gate.name
