@@ -359,8 +359,13 @@ def run_circuit_arm(args, rank, world, local_rank):
     else:
         from paper_2411_15332_b200.partition import DeviceBackend, DistTransport, ShardedState
         g = world.bit_length() - 1
-        backend = DeviceBackend(c.n - g, dev)
-        sh = ShardedState(c.n, world, rank, backend, DistTransport(), initial=c.initial)
+        if args.peer:  # fused global-qubit gates over NVLink peer memory (torch symmetric memory)
+            from paper_2411_15332_b200.partition import SymmetricTransport
+            backend = DeviceBackend(c.n - g, dev, symmetric=True)
+            sh = ShardedState(c.n, world, rank, backend, SymmetricTransport(), initial=c.initial)
+        else:  # half-shard swaps over NCCL send/recv
+            backend = DeviceBackend(c.n - g, dev)
+            sh = ShardedState(c.n, world, rank, backend, DistTransport(), initial=c.initial, peer=False)
         ops = []
         for st in c.steps:
             if int(st.kind) == 1:
@@ -439,6 +444,8 @@ def run_circuit_arm(args, rank, world, local_rank):
         state.close()
     if world > 1:
         line["exchanges_per_step"] = sh.swaps / (args.steps + args.warmup)
+        line["peer_gates_per_step"] = sh.splits / (args.steps + args.warmup)
+        line["config"]["global_qubit_gates"] = "peer-memory kernel" if sh.peer else "NCCL half-shard swaps"
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.close()
@@ -456,6 +463,9 @@ def main():
                     help="c2 (default): the single-gate sweep; c1/c3/c4/c5: whole BASELINE circuits")
     ap.add_argument("--n-circuit", type=int, default=0, help="qubits for c1/c3/c4/c5 (default: BASELINE size)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--peer", action="store_true",
+                    help="c4/c5 under torchrun: gates on global qubits as one kernel over NVLink peer memory "
+                         "(qcs_apply_split) instead of NCCL half-shard swaps")
     args = ap.parse_args()
     rank, world, local_rank = dist_env()
     if args.impl == "reference":
