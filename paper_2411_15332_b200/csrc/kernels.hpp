@@ -79,6 +79,8 @@ struct TileOp {
 
 // RegOp::kind flags above the kind bits
 constexpr int KF_KIND = 0x0f;
+constexpr int KF_BUNDLE = 0x10;  // TOP_GATE: dense gates on the register bits of mask t, coefficients
+                                 // in PassParams::pool[ref + 4 * bit] (m00 m01 m10 m11 per bit)
 constexpr int KF_FLUSH = 0x20;   // apply the pending +-1 sign flips before this op (set by the planner)
 constexpr int KF_SIGNED = 0x40;  // TOP_DIAG with entries in {+1, -1}: dskip holds the -1 entries
 constexpr int KF_GCTRL = 0x80;   // has controls outside the tile (gctrl_mask / gctrl_val)
@@ -110,7 +112,8 @@ struct RoundDesc {
     std::uint16_t op_begin, op_count;
 };
 
-constexpr int kPassMaxOps = 236;
+constexpr int kPassMaxOps = 200;
+constexpr int kPassPool = 528;    // double2 slots for gate bundles (12 per bundle)
 enum : std::uint8_t { ALT_NONE = 0, ALT_ROUNDS = 1, ALT_SKIP = 2 };
 struct PassParams {           // <= 32 KB: the kernel parameter limit
     int m;                    // tile bits (3..12)
@@ -125,7 +128,9 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
     std::uint32_t list_off, list_cnt;  // list_cnt > 0: run only these tiles (ALT_SKIP passes)
     RoundDesc rounds[kPassMaxOps];
     RegOp ops[kPassMaxOps];
+    double2 pool[kPassPool];
 };
+static_assert(sizeof(PassParams) <= 32764, "kernel parameter space");
 
 // tables_dev: the plan's u64 tables (Lowered::tables): run offsets and tile lists
 void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* big_dev,

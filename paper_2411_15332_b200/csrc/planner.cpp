@@ -341,7 +341,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 loc[b] = P.m;
                 P.bits[P.m++] = b;
             }
-        int nops = 0, nsign = 0;
+        int nops = 0, nsign = 0, npool = 0;
         std::uint64_t flip_off = 0, flip_cnt = 0;
         // rounds of <= 3 register bits; gates on 2-3 targets get shared-memory rounds
         struct RoundPlan {
@@ -518,6 +518,26 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 if ((f.kind == TOP_WHT || f.kind == TOP_GATE) && pending_signs) {
                     o.kind = std::uint8_t(o.kind | KF_FLUSH);
                     pending_signs = false;
+                }
+                // consecutive uncontrolled one-qubit gates on different register bits: one
+                // bundled operation (one dispatch per group instead of up to three)
+                if (f.kind == TOP_GATE && !(rd.flags & RD_SMEM) && o.kind == TOP_GATE && !o.lctrl_mask &&
+                    nops > rd.op_begin) {
+                    RegOp& prev = P.ops[nops - 1];
+                    const bool prev_gate = (prev.kind & ~(KF_BUNDLE | KF_FLUSH)) == TOP_GATE && !prev.lctrl_mask;
+                    const unsigned pmask = (prev.kind & KF_BUNDLE) ? prev.t : (1u << prev.t);
+                    if (prev_gate && !(pmask & (1u << o.t)) && ((prev.kind & KF_BUNDLE) || npool + 12 <= kPassPool)) {
+                        if (!(prev.kind & KF_BUNDLE)) {
+                            prev.ref = std::uint16_t(npool);
+                            npool += 12;
+                            for (int k = 0; k < 4; ++k) P.pool[prev.ref + 4 * prev.t + k] = prev.c[k];
+                            prev.kind = std::uint8_t(prev.kind | KF_BUNDLE);
+                            prev.t = std::uint8_t(1u << prev.t);
+                        }
+                        for (int k = 0; k < 4; ++k) P.pool[prev.ref + 4 * o.t + k] = o.c[k];
+                        prev.t = std::uint8_t(prev.t | (1u << o.t));
+                        continue;
+                    }
                 }
                 P.ops[nops++] = o;
             }

@@ -82,8 +82,8 @@ __device__ __forceinline__ double2 cmul2_f(double2 a, double2 x0, double2 b, dou
 // tile-local controls hold (0xff without controls).  One straight-line form for every gate keeps
 // the register allocation of the round loop free of per-kind copies.
 template <int T, bool CTRL>
-__device__ __forceinline__ void gate1(double2 (&v)[8], const RegOp& o, unsigned en) {
-    const double2 a0 = o.c[0], b0 = o.c[1], a1 = o.c[2], b1 = o.c[3];
+__device__ __forceinline__ void gate1(double2 (&v)[8], const double2* c, unsigned en) {
+    const double2 a0 = c[0], b0 = c[1], a1 = c[2], b1 = c[3];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         if (q & (1 << T)) continue;
@@ -369,6 +369,15 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                     for (int r = 0; r < NG; ++r)
 #pragma unroll
                         for (int q = 0; q < 8; ++q) v[r][q] = make_double2(v[r][q].x * sc, v[r][q].y * sc);
+                } else if ((F & F_GATE) && kind == TOP_GATE && (kb & KF_BUNDLE)) {
+                    const int tm = o.t;
+                    const double2* pc = P.pool + o.ref;
+#pragma unroll
+                    for (int r = 0; r < NG; ++r) {
+                        if (tm & 1) gate1<0, false>(v[r], pc, 0xffu);
+                        if (tm & 2) gate1<1, false>(v[r], pc + 4, 0xffu);
+                        if (tm & 4) gate1<2, false>(v[r], pc + 8, 0xffu);
+                    }
                 } else if ((F & F_GATE) && kind == TOP_GATE) {
                     const int tt = o.t;
                     const unsigned cm = o.lctrl_mask, cv = o.lctrl_val;
@@ -378,13 +387,13 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                             unsigned en = 0;
 #pragma unroll
                             for (int q = 0; q < 8; ++q) en |= unsigned(((lb[r] | off[q]) & cm) == cv) << q;
-                            if (tt == 0) gate1<0, true>(v[r], o, en);
-                            else if (tt == 1) gate1<1, true>(v[r], o, en);
-                            else gate1<2, true>(v[r], o, en);
+                            if (tt == 0) gate1<0, true>(v[r], o.c, en);
+                            else if (tt == 1) gate1<1, true>(v[r], o.c, en);
+                            else gate1<2, true>(v[r], o.c, en);
                         } else {
-                            if (tt == 0) gate1<0, false>(v[r], o, 0xffu);
-                            else if (tt == 1) gate1<1, false>(v[r], o, 0xffu);
-                            else gate1<2, false>(v[r], o, 0xffu);
+                            if (tt == 0) gate1<0, false>(v[r], o.c, 0xffu);
+                            else if (tt == 1) gate1<1, false>(v[r], o.c, 0xffu);
+                            else gate1<2, false>(v[r], o.c, 0xffu);
                         }
                     }
                 } else if ((F & F_DIAG) && kind == TOP_DIAG) {
