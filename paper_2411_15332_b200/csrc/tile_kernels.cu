@@ -294,7 +294,13 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
     const bool io_last = (QCS_TILE_IO & 2) && !((F & F_SMEM) && (RL.flags & RD_SMEM)) && RL.r[0] >= 3;
     cp_async_wait_all();  // the run-offset table
     __syncthreads();
-    for (unsigned j = t; j < sz; j += bt) cp_async16(sm + swz(j), a + (base | (j & 7u) | hi_tab[j >> 3]));
+    // j = t + k * bt: with bt a power of two >= 8, the run offset splits into the thread part
+    // hi_tab[t >> 3] and the CTA-uniform part hi_tab[k * bt / 8] (deposit is linear on disjoint bits)
+    if (t < sz) {
+        const u64 gt = base | (t & 7u) | hi_tab[t >> 3];
+        const unsigned rs = bt >> 3;
+        for (unsigned j = t, k = 0; j < sz; j += bt, k += rs) cp_async16(sm + swz(j), a + (gt | hi_tab[k]));
+    }
     cp_async_wait_all();
     __syncthreads();
     for (int ri = rb; ri < re; ++ri) {
@@ -312,9 +318,12 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
         }
         const int r0 = R.r[0], r1 = R.r[1], r2 = R.r[2];
         const unsigned ro[3] = {1u << r0, 1u << r1, 1u << r2};
-        unsigned off[8];
+        unsigned off[8], soff[8];  // register q's local offset, and its swizzled form
 #pragma unroll
-        for (int q = 0; q < 8; ++q) off[q] = ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u);
+        for (int q = 0; q < 8; ++q) {
+            off[q] = ((q & 1) ? ro[0] : 0u) | ((q & 2) ? ro[1] : 0u) | ((q & 4) ? ro[2] : 0u);
+            soff[q] = swz(off[q]);  // swz is xor-linear: swz(lb | off) = swz(lb) ^ swz(off)
+        }
         // NG groups per thread at once: gate-heavy passes are FP64/issue bound, and two
         // independent register groups per operation halve the per-operation dispatch cost
         constexpr int NG = (F & (F_GATE | F_DIAG)) ? QCS_TILE_NG : 1;
@@ -329,8 +338,9 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                 const unsigned g = gb + unsigned(r) * bt;
                 ok[r] = g < ngroups;
                 lb[r] = insert_zero(insert_zero(insert_zero(ok[r] ? g : gb, r0), r1), r2);
+                const unsigned slb = swz(lb[r]);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) v[r][q] = sm[swz(lb[r] | off[q])];
+                for (int q = 0; q < 8; ++q) v[r][q] = sm[slb ^ soff[q]];
                 g0[r] = base | (lb[r] & 7u) | hi_tab[lb[r] >> 3];  // basis index of register 0
                 negacc[r] = 0;  // pending sign flips of the +-1 diagonals (they commute)
             }
@@ -433,14 +443,17 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                     }
                 } else {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) sm[swz(lb[r] | off[q])] = v[r][q];
+                    for (int q = 0; q < 8; ++q) sm[swz(lb[r]) ^ soff[q]] = v[r][q];
                 }
             }
         }
         __syncthreads();
     }
-    if (!io_last)
-        for (unsigned j = t; j < sz; j += bt) __stcs(a + (base | (j & 7u) | hi_tab[j >> 3]), sm[swz(j)]);
+    if (!io_last && t < sz) {
+        const u64 gt = base | (t & 7u) | hi_tab[t >> 3];
+        const unsigned rs = bt >> 3;
+        for (unsigned j = t, k = 0; j < sz; j += bt, k += rs) __stcs(a + (gt | hi_tab[k]), sm[swz(j)]);
+    }
 }
 
 template <unsigned F>
