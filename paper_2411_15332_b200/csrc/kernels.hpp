@@ -125,6 +125,8 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
     std::uint8_t alt_mode;
     std::uint16_t alt_begin, alt_nrounds;
     std::uint32_t hi_off;     // this pass's table of run offsets (tile bits 3..m-1) in the plan's tables
+    int nruns;                // the basis bits outside the tile, as runs: a tile index deposits into them
+    std::uint8_t run_pos[16], run_len[16];
     std::uint32_t list_off, list_cnt;  // list_cnt > 0: run only these tiles (ALT_SKIP passes)
     RoundDesc rounds[kPassMaxOps];
     RegOp ops[kPassMaxOps];

@@ -564,6 +564,17 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             }
         }
         // the basis offset of each run of 8 (tile bits 3..m-1), copied into shared memory per tile
+        for (int b = 0; b < n;) {  // runs of bits outside the tile
+            if (pp.tile >> b & 1) {
+                ++b;
+                continue;
+            }
+            int e = b;
+            while (e < n && !(pp.tile >> e & 1)) ++e;
+            P.run_pos[P.nruns] = std::uint8_t(b);
+            P.run_len[P.nruns++] = std::uint8_t(e - b);
+            b = e;
+        }
         if (out.tables.size() & 1) out.tables.push_back(0);  // 16-byte aligned (cp.async)
         P.hi_off = std::uint32_t(out.tables.size());
         for (unsigned k = 0; k < (1u << (P.m - 3)); ++k) {

@@ -262,16 +262,21 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
     u64* hi_tab = reinterpret_cast<u64*>(sm + sz);  // basis offset of local bits 3..m-1 (host table)
     const unsigned t = threadIdx.x, bt = blockDim.x;
     for (unsigned j = 2 * t; j < ngroups; j += 2 * bt) cp_async16(hi_tab + j, tables + P.hi_off + j);
-    u64 base = P.list_cnt ? __ldg(tables + P.list_off + blockIdx.x) : u64(blockIdx.x), tile_mask = 0;
-    for (int b = 0; b < m; ++b) {  // bits[] ascending: insert zeros from the lowest position up
-        const int pos = P.bits[b];
-        base = ((base >> pos) << (pos + 1)) | (base & ((u64(1) << pos) - 1));
-        tile_mask |= u64(1) << pos;
+    // basis offset of the tile: its index deposited into the bits outside the tile (host-listed runs)
+    u64 base = 0;
+    {
+        u64 tile = P.list_cnt ? __ldg(tables + P.list_off + blockIdx.x) : u64(blockIdx.x);
+        for (int i = 0; i < P.nruns; ++i) {
+            base |= (tile & ((u64(1) << P.run_len[i]) - 1)) << P.run_pos[i];
+            tile >>= P.run_len[i];
+        }
     }
     // sign steps whose listed indices miss this tile act uniformly (negate all or nothing):
     // decide that once per tile (bit s = sign op s has a listed index inside the tile)
     unsigned sign_hit = 0;
     if (F & F_SIGN) {
+        u64 tile_mask = 0;
+        for (int b = 0; b < m; ++b) tile_mask |= u64(1) << P.bits[b];
         for (int oi = 0; oi < P.nops; ++oi) {
             const RegOp& o = P.ops[oi];
             if ((o.kind & KF_KIND) != TOP_SIGN) continue;
