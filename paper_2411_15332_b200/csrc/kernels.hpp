@@ -113,7 +113,7 @@ struct RoundDesc {
 };
 
 constexpr int kPassMaxOps = 200;
-constexpr int kPassPool = 528;    // double2 slots for gate bundles (12 per bundle)
+constexpr int kPassPool = 512;    // double2 slots for gate bundles (12 per bundle)
 enum : std::uint8_t { ALT_NONE = 0, ALT_ROUNDS = 1, ALT_SKIP = 2 };
 struct PassParams {           // <= 32 KB: the kernel parameter limit
     int m;                    // tile bits (3..12)
@@ -125,6 +125,8 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
     std::uint8_t alt_mode;
     std::uint16_t alt_begin, alt_nrounds;
     std::uint32_t hi_off;     // this pass's table of run offsets (tile bits 3..m-1) in the plan's tables
+    int tma_rank;             // > 0: the tile moves as one TMA box of this rank (set at launch)
+    std::uint8_t tma_gap_pos[5], tma_gap_len[5];  // box dims over bits outside the tile: coordinate bits
     int nruns;                // the basis bits outside the tile, as runs: a tile index deposits into them
     std::uint8_t run_pos[16], run_len[16];
     std::uint32_t list_off, list_cnt;  // list_cnt > 0: run only these tiles (ALT_SKIP passes)
@@ -132,10 +134,12 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
     RegOp ops[kPassMaxOps];
     double2 pool[kPassPool];
 };
-static_assert(sizeof(PassParams) <= 32764, "kernel parameter space");
+// the kernel's parameters: PassParams, four pointers and a 128-byte tensor map in 32764 bytes
+static_assert(sizeof(PassParams) + 4 * 8 + 128 + 64 <= 32764, "kernel parameter space");
 
 // tables_dev: the plan's u64 tables (Lowered::tables): run offsets and tile lists
-void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* big_dev,
+// sets p.tma_* for the launch
+void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev,
                       const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, cudaStream_t st);
 int tile_max_bits();
 

@@ -25,6 +25,8 @@
 #include <algorithm>
 #include <cstdint>
 
+#include <cuda.h>
+
 #include "common.hpp"
 #include "kernels.hpp"
 
@@ -65,6 +67,82 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// ---- TMA: the whole tile as one tensor-map box (cp.async.bulk.tensor), 128-byte swizzle
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, const int (&c)[5], int rank,
+                                         unsigned long long* bar) {
+    const unsigned d = smem_u32(dst), b = smem_u32(bar);
+    const auto m = reinterpret_cast<unsigned long long>(map);
+    switch (rank) {
+        case 2:
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                         " [%0], [%1, {%2, %3}], [%4];" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(b) : "memory");
+            break;
+        case 3:
+            asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b)
+                         : "memory");
+            break;
+        case 4:
+            asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                         " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]),
+                         "r"(c[3]), "r"(b)
+                         : "memory");
+            break;
+        default:
+            asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                         " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]),
+                         "r"(c[3]), "r"(c[4]), "r"(b)
+                         : "memory");
+            break;
+    }
+}
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, const int (&c)[5], int rank, const void* src) {
+    const unsigned s_ = smem_u32(src);
+    const auto m = reinterpret_cast<unsigned long long>(map);
+    switch (rank) {
+        case 2:
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(m),
+                         "r"(c[0]), "r"(c[1]), "r"(s_)
+                         : "memory");
+            break;
+        case 3:
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(m),
+                         "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(s_)
+                         : "memory");
+            break;
+        case 4:
+            asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                             m),
+                         "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(s_)
+                         : "memory");
+            break;
+        default:
+            asm volatile(
+                "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(m),
+                "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(s_)
+                : "memory");
+            break;
+    }
+    asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\nfence.mbarrier_init.release.cluster;\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(unsigned long long* bar) {
+    asm volatile(
+        "{\n.reg .pred done;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n"
+        "@!done bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
 
 // Fused passes are held to the 1e-12 tolerance (their operation order already differs from the
 // reference's per-step fold), so their complex products use fused multiply-adds: half the
@@ -239,12 +317,20 @@ constexpr int kThreads = 256;
 #ifndef QCS_TILE_MINB
 #define QCS_TILE_MINB 2
 #endif
+#ifndef QCS_TILE_TMA  // tiles move as one tensor-map TMA box where the bit layout allows
+#define QCS_TILE_TMA 1
+#endif
 #ifndef QCS_TILE_IO  // bit 1: last register round straight to HBM (bit 0, loads, measured slower: removed)
 #define QCS_TILE_IO 2
 #endif
 constexpr int kMaxBits = 12;
 
 enum : unsigned { F_GATE = 1, F_DIAG = 2, F_SIGN = 4, F_SMEM = 8 };
+
+// dynamic shared memory: 1 KB alignment slack, the tile, its run offsets (>= 16 bytes), mbarrier
+constexpr std::size_t tile_smem(int m) {
+    return 1024 + (std::size_t(1) << m) * 16 + std::max<std::size_t>(16, (std::size_t(1) << (m - 3)) * 8) + 16;
+}
 
 // F: the operation kinds present in the pass (the host picks the instantiation), so a pass
 // without gates or diagonals compiles to the lean butterfly/sign kernel.
@@ -253,13 +339,18 @@ template <unsigned F>
 // passes with gates or diagonals trade residency for registers (QCS_TILE_MINB)
 __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_MINB : (F & F_SMEM) ? 2 : 3)
     k_tile(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,
-           const u64* __restrict__ flipped, const u64* __restrict__ tables) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+           const u64* __restrict__ flipped, const u64* __restrict__ tables, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int m = P.m;
     const unsigned sz = 1u << m;
     const unsigned ngroups = sz >> 3;  // 8 amplitudes per group
-    double2* sm = reinterpret_cast<double2*>(smem_raw);
+    // 1024-byte aligned tile (the TMA 128-byte swizzle repeats every 1 KB), then the run offsets
+    // and the tile's mbarrier
+    // (offset from smem_raw, not an integer-cast pointer: keeps the accesses in the shared space)
+    const unsigned align_pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    double2* sm = reinterpret_cast<double2*>(smem_raw + align_pad);
     u64* hi_tab = reinterpret_cast<u64*>(sm + sz);  // basis offset of local bits 3..m-1 (host table)
+    auto* bar = reinterpret_cast<unsigned long long*>(hi_tab + (ngroups < 2 ? 2 : ngroups));
     const unsigned t = threadIdx.x, bt = blockDim.x;
     for (unsigned j = 2 * t; j < ngroups; j += 2 * bt) cp_async16(hi_tab + j, tables + P.hi_off + j);
     // basis offset of the tile: its index deposited into the bits outside the tile (host-listed runs)
@@ -297,17 +388,33 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
     // round trip less); only when bits 0..2 are not register bits, so a warp stores whole runs
     const RoundDesc& RL = P.rounds[re - 1];
     const bool io_last = (QCS_TILE_IO & 2) && !((F & F_SMEM) && (RL.flags & RD_SMEM)) && RL.r[0] >= 3;
+    // TMA: the tile is one box of the host's tensor map over the state; the coordinates of the
+    // bit runs outside the tile come from the tile base (runs inside start at 0)
+    int tc[5] = {0, 0, 0, 0, 0};
+    if (P.tma_rank) {
+        for (int d = 1; d < P.tma_rank; ++d)
+            if (P.tma_gap_len[d]) tc[d] = int((base >> P.tma_gap_pos[d]) & ((u64(1) << P.tma_gap_len[d]) - 1));
+        if (t == 0) {
+            mbar_init(bar);
+            mbar_expect_tx(bar, sz * 16u);
+            tma_load(sm, &tmap, tc, P.tma_rank, bar);
+        }
+    }
     cp_async_wait_all();  // the run-offset table
     __syncthreads();
-    // j = t + k * bt: with bt a power of two >= 8, the run offset splits into the thread part
-    // hi_tab[t >> 3] and the CTA-uniform part hi_tab[k * bt / 8] (deposit is linear on disjoint bits)
-    if (t < sz) {
-        const u64 gt = base | (t & 7u) | hi_tab[t >> 3];
-        const unsigned rs = bt >> 3;
-        for (unsigned j = t, k = 0; j < sz; j += bt, k += rs) cp_async16(sm + swz(j), a + (gt | hi_tab[k]));
+    if (P.tma_rank) {
+        mbar_wait0(bar);
+    } else {
+        // j = t + k * bt: with bt a power of two >= 8, the run offset splits into the thread part
+        // hi_tab[t >> 3] and the CTA-uniform part hi_tab[k * bt / 8] (deposit is linear on disjoint bits)
+        if (t < sz) {
+            const u64 gt = base | (t & 7u) | hi_tab[t >> 3];
+            const unsigned rs = bt >> 3;
+            for (unsigned j = t, k = 0; j < sz; j += bt, k += rs) cp_async16(sm + swz(j), a + (gt | hi_tab[k]));
+        }
+        cp_async_wait_all();
+        __syncthreads();
     }
-    cp_async_wait_all();
-    __syncthreads();
     for (int ri = rb; ri < re; ++ri) {
         const RoundDesc& R = P.rounds[ri];
         if ((F & F_SMEM) && (R.flags & RD_SMEM)) {
@@ -454,7 +561,11 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
         }
         __syncthreads();
     }
-    if (!io_last && t < sz) {
+    if (!io_last && P.tma_rank) {  // the tile back as one TMA box
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (t == 0) tma_store(&tmap, tc, P.tma_rank, sm);
+    } else if (!io_last && t < sz) {
         const u64 gt = base | (t & 7u) | hi_tab[t >> 3];
         const unsigned rs = bt >> 3;
         for (unsigned j = t, k = 0; j < sz; j += bt, k += rs) __stcs(a + (gt | hi_tab[k]), sm[swz(j)]);
@@ -463,28 +574,93 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
 
 template <unsigned F>
 void launch_f(double2* amps, const PassParams& p, const TileOp* big_dev, const std::uint64_t* flipped_dev, unsigned tiles,
-              const std::uint64_t* tables_dev, int threads, std::size_t smem, cudaStream_t st) {
+              const std::uint64_t* tables_dev, const CUtensorMap& tmap, int threads, std::size_t smem, cudaStream_t st) {
     static bool attr_set[64] = {};  // per device and instantiation
     int dev = 0;
     QCS_CUDA(cudaGetDevice(&dev));
     if (dev < 64 && !attr_set[dev]) {
-        const int max_smem = (1 << kMaxBits) * 16 + (1 << (kMaxBits - 3)) * 8;
-        QCS_CUDA(cudaFuncSetAttribute(k_tile<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+        QCS_CUDA(cudaFuncSetAttribute(k_tile<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tile_smem(kMaxBits))));
         QCS_CUDA(cudaFuncSetAttribute(k_tile<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr_set[dev] = true;
     }
-    k_tile<F><<<tiles, threads, smem, st>>>(amps, p, big_dev, flipped_dev, tables_dev);
+    k_tile<F><<<tiles, threads, smem, st>>>(amps, p, big_dev, flipped_dev, tables_dev, tmap);
+}
+
+// The tensor map that moves a pass's tile as one TMA box: the state as <= 5 dims in ascending
+// bit order -- the 8 amplitudes of bits 0..2 (16 doubles, 128 bytes, swizzled like swz), then
+// each run of tile bits (<= 8 bits per dim: box = the whole run) and each run of other bits
+// (box 1, the coordinate selects the tile).  False when the bit layout needs more dims.
+bool tile_tensor_map(double2* amps, int n, PassParams& p, CUtensorMap* map) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode encode = nullptr;
+    static bool looked = false;
+    if (!looked) {
+        looked = true;
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<Encode>(fn);
+        else
+            cudaGetLastError();
+    }
+    if (!encode || n > 36 || p.m < 3) return false;
+    u64 tile = 0;
+    for (int b = 0; b < p.m; ++b) tile |= u64(1) << p.bits[b];
+    cuuint64_t gdim[5], gstride[4];
+    cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+    int rank = 1;
+    gdim[0] = 16;
+    box[0] = 16;
+    std::uint8_t gpos[5] = {}, glen[5] = {};
+    for (int b = 3; b < n;) {
+        const bool in = tile >> b & 1;
+        int e = b;
+        while (e < n && bool(tile >> e & 1) == in) ++e;
+        for (int c = b; c < e;) {
+            const int len = in ? std::min(8, e - c) : e - c;
+            if (rank >= 5 || (!in && len > 31)) return false;
+            gdim[rank] = cuuint64_t(1) << len;
+            box[rank] = in ? cuuint32_t(1) << len : 1;
+            gstride[rank - 1] = cuuint64_t(16) << c;
+            gpos[rank] = std::uint8_t(in ? 0 : c);
+            glen[rank] = std::uint8_t(in ? 0 : len);
+            ++rank;
+            c += len;
+        }
+        b = e;
+    }
+    if (rank < 2) {  // a 3-bit state: one more (unit) dim keeps the 2d..5d forms
+        gdim[1] = 1;
+        box[1] = 1;
+        gstride[0] = 128;
+        rank = 2;
+    }
+    if (encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(rank), amps, gdim, gstride, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    p.tma_rank = rank;
+    for (int d = 0; d < 5; ++d) {
+        p.tma_gap_pos[d] = gpos[d];
+        p.tma_gap_len[d] = glen[d];
+    }
+    return true;
 }
 
 }  // namespace
 
 int tile_max_bits() { return kMaxBits; }
 
-void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* big_dev, const std::uint64_t* flipped_dev,
+void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev, const std::uint64_t* flipped_dev,
                       const std::uint64_t* tables_dev, cudaStream_t st) {
     if (p.m < 3 || p.m > kMaxBits || p.m > n) raise(QCS_ERR_ARG, "tile bits out of range");
-    // the tile, then its run-offset table (copied in 16-byte pieces)
-    const std::size_t smem = (std::size_t(1) << p.m) * sizeof(double2) + std::max<std::size_t>(16, (std::size_t(1) << (p.m - 3)) * sizeof(u64));
+    const std::size_t smem = tile_smem(p.m);
+    CUtensorMap tmap{};
+    p.tma_rank = 0;
+    if (QCS_TILE_TMA) tile_tensor_map(amps, n, p, &tmap);
     const u64 tiles = p.list_cnt ? u64(p.list_cnt) : u64(1) << (n - p.m);
     if (tiles > 0x7fffffffull) raise(QCS_ERR_CAPACITY, "too many tiles for one launch");
     const int threads = std::min(kThreads, std::max(32, 1 << (p.m - 3)));
@@ -500,7 +676,7 @@ void launch_tile_pass(double2* amps, int n, const PassParams& p, const TileOp* b
     TimedLaunch tl("tile_pass", 32.0 * double(tiles) * double(1u << p.m), st);
     switch (f) {
 #define QCS_TILE_CASE(x) \
-    case x: launch_f<x>(amps, p, big_dev, flipped_dev, unsigned(tiles), tables_dev, threads, smem, st); break;
+    case x: launch_f<x>(amps, p, big_dev, flipped_dev, unsigned(tiles), tables_dev, tmap, threads, smem, st); break;
         QCS_TILE_CASE(0) QCS_TILE_CASE(1) QCS_TILE_CASE(2) QCS_TILE_CASE(3) QCS_TILE_CASE(4) QCS_TILE_CASE(5)
         QCS_TILE_CASE(6) QCS_TILE_CASE(7) QCS_TILE_CASE(8) QCS_TILE_CASE(9) QCS_TILE_CASE(10) QCS_TILE_CASE(11)
         QCS_TILE_CASE(12) QCS_TILE_CASE(13) QCS_TILE_CASE(14) QCS_TILE_CASE(15)
