@@ -320,9 +320,6 @@ constexpr int kThreads = 256;
 #ifndef QCS_TILE_TMA  // tiles move as one tensor-map TMA box where the bit layout allows
 #define QCS_TILE_TMA 1
 #endif
-#ifndef QCS_TILE_IO  // bit 1: last register round straight to HBM (bit 0, loads, measured slower: removed)
-#define QCS_TILE_IO 2
-#endif
 constexpr int kMaxBits = 12;
 
 enum : unsigned { F_GATE = 1, F_DIAG = 2, F_SIGN = 4, F_SMEM = 8 };
@@ -384,10 +381,6 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
         rb = P.alt_begin;
         re = rb + P.alt_nrounds;
     }
-    // a register round at the end writes its amplitudes straight back to HBM (one shared-memory
-    // round trip less); only when bits 0..2 are not register bits, so a warp stores whole runs
-    const RoundDesc& RL = P.rounds[re - 1];
-    const bool io_last = (QCS_TILE_IO & 2) && !((F & F_SMEM) && (RL.flags & RD_SMEM)) && RL.r[0] >= 3;
     // TMA: the tile is one box of the host's tensor map over the state; the coordinates of the
     // bit runs outside the tile come from the tile base (runs inside start at 0)
     int tc[5] = {0, 0, 0, 0, 0};
@@ -543,29 +536,20 @@ __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_M
                 }
             }
             if ((F & F_DIAG) && (R.flags & RD_SIGNS)) flip_signs<NG>(v, negacc);
-            const bool to_hbm = io_last && ri == re - 1;
 #pragma unroll
             for (int r = 0; r < NG; ++r) {
                 if (!ok[r]) continue;
-                if (to_hbm) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const unsigned j = lb[r] | off[q];
-                        __stcs(a + (base | (j & 7u) | hi_tab[j >> 3]), v[r][q]);
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) sm[swz(lb[r]) ^ soff[q]] = v[r][q];
-                }
+                for (int q = 0; q < 8; ++q) sm[swz(lb[r]) ^ soff[q]] = v[r][q];
             }
         }
         __syncthreads();
     }
-    if (!io_last && P.tma_rank) {  // the tile back as one TMA box
+    if (P.tma_rank) {  // the tile back as one TMA box
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();
         if (t == 0) tma_store(&tmap, tc, P.tma_rank, sm);
-    } else if (!io_last && t < sz) {
+    } else if (t < sz) {
         const u64 gt = base | (t & 7u) | hi_tab[t >> 3];
         const unsigned rs = bt >> 3;
         for (unsigned j = t, k = 0; j < sz; j += bt, k += rs) __stcs(a + (gt | hi_tab[k]), sm[swz(j)]);
