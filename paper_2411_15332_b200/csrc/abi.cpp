@@ -352,7 +352,7 @@ int qcs_step_dax(int n, const qcs_placement* placements, int num_placements, int
         }
         *count = qcs::step_encode(n, placements, num_placements, device, false, capacity, rows, cols, values, nullptr,
                                   nullptr, mem == QCS_MEM_DEVICE);
-        if (*count > capacity) qcs::raise(QCS_ERR_CAPACITY, "output capacity below the entry count");
+        if (capacity && *count > capacity) qcs::raise(QCS_ERR_CAPACITY, "output capacity below the entry count");
     });
 }
 
@@ -367,7 +367,7 @@ int qcs_step_das(int n, const qcs_placement* placements, int num_placements, int
         }
         *count = qcs::step_encode(n, placements, num_placements, device, true, capacity, nullptr, nullptr, values, dis,
                                   last_in_row, mem == QCS_MEM_DEVICE);
-        if (*count > capacity) qcs::raise(QCS_ERR_CAPACITY, "output capacity below the entry count");
+        if (capacity && *count > capacity) qcs::raise(QCS_ERR_CAPACITY, "output capacity below the entry count");
     });
 }
 

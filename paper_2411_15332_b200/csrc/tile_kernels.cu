@@ -202,8 +202,40 @@ __device__ __forceinline__ void butterfly(double2 (&v)[8]) {
 
 // Diagonal phase: entry index g from up to three basis bits; bits held in registers vary with
 // q, the others are constant over the thread's group (taken from the group's first element).
+// One-bit diagonal on register bit T: entry 0 on the registers with bit T clear, entry 1 on the
+// others; an entry that is exactly 1 (skip bit) is not applied.
+template <int T>
+__device__ __forceinline__ void diag_reg(double2 (&v)[8], double2 c0, double2 c1, unsigned skip) {
+    if (!(skip & 1u)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (!(q >> T & 1)) v[q] = cmul_f(c0, v[q]);
+    }
+    if (!(skip & 2u)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q >> T & 1) v[q] = cmul_f(c1, v[q]);
+    }
+}
+
 __device__ __forceinline__ void diag_op(double2 (&v)[8], const RegOp& o, const TileOp* big, u64 g0) {
     const int dk = o.dk;
+    if (dk == 1) {  // S, T, RZ, phase gates: no per-register entry selection
+        const unsigned skip = o.dskip;
+        if (o.dreg[0] == 0xff) {  // the bit is constant over the group: one entry for all 8
+            const int g = int((g0 >> o.dpos[0]) & 1);
+            if (skip >> g & 1) return;
+            const double2 d = g ? o.c[1] : o.c[0];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = cmul_f(d, v[q]);
+            return;
+        }
+        const int rb = o.dreg[0];
+        if (rb == 0) diag_reg<0>(v, o.c[0], o.c[1], skip);
+        else if (rb == 1) diag_reg<1>(v, o.c[0], o.c[1], skip);
+        else diag_reg<2>(v, o.c[0], o.c[1], skip);
+        return;
+    }
     if (dk <= 2) {  // the host tabulated the register part of g for every q (2 bits each)
         int cg = 0;
         if (o.dreg[0] == 0xff && dk >= 1) cg |= int((g0 >> o.dpos[0]) & 1) << (dk - 1);
