@@ -697,7 +697,7 @@ void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev
         QCS_TILE_CASE(6) QCS_TILE_CASE(7) QCS_TILE_CASE(8) QCS_TILE_CASE(9) QCS_TILE_CASE(10) QCS_TILE_CASE(11)
         QCS_TILE_CASE(12) QCS_TILE_CASE(13) QCS_TILE_CASE(14) QCS_TILE_CASE(15)
 #undef QCS_TILE_CASE
-        default: break;
+        default: raise(QCS_ERR_SIM, "internal: no tile kernel for this operation mix");
     }
     check_launch("k_tile");
 }
