@@ -61,7 +61,15 @@ __device__ u64 row_entries(const EncodeStep& st, u64 r, Visit&& visit) {
         double2 v = make_double2(1.0, 0.0);
         for (int f = 0; f < st.nfold; ++f) {
             const int j = st.fold_gate[f];
-            const double2 fv = j < 0 ? make_double2(1.0, 0.0) : st.p[j].val[g[j]][idx[slot[j]]];
+            if (j < 0) {
+                // an identity factor (1 + 0i) returns v bit for bit unless a component is -0
+                // (x - (-0*0) / (+0) + (-0) can turn -0 into +0): only then multiply
+                const bool neg_zero = (v.x == 0.0 && signbit(v.x)) || (v.y == 0.0 && signbit(v.y));
+                if (f > 0 && !neg_zero) continue;
+                v = f == 0 ? make_double2(1.0, 0.0) : cmul(v, make_double2(1.0, 0.0));
+                continue;
+            }
+            const double2 fv = st.p[j].val[g[j]][idx[slot[j]]];
             v = f == 0 ? fv : cmul(v, fv);
         }
         (void)n;
@@ -95,7 +103,7 @@ __global__ void k_encode_emit(const EncodeStep* __restrict__ stp, u64 dim, const
     for (u64 r = u64(blockIdx.x) * blockDim.x + threadIdx.x; r < dim; r += stride) {
         const u64 o = offsets[r];
         row_entries(st, r, [&](u64 i, u64 col, double2 v) {
-            rows[o + i] = r;
+            if (rows) rows[o + i] = r;
             cols[o + i] = col;
             vals[o + i] = v;
         });
@@ -231,11 +239,33 @@ inline unsigned grid_for(u64 work, int threads) {
     return unsigned(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
+// One memory pool per device for the encoder / MVM scratch; it keeps up to 8 GiB mapped
+// between calls, so repeated encodes do not pay for mapping fresh memory.
+cudaMemPool_t scratch_pool() {
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    QCS_CUDA(cudaGetDevice(&dev));
+    if (dev >= 64) raise(QCS_ERR_ARG, "device index out of range");
+    if (!pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        QCS_CUDA(cudaMemPoolCreate(&pools[dev], &props));
+        std::uint64_t keep = std::uint64_t(8) << 30;
+        QCS_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep));
+    }
+    return pools[dev];
+}
+
 template <class T>
-struct DevBuf {
+struct DevBuf {  // stream-ordered scratch from scratch_pool(): no cudaMalloc / unmap per call
     T* p = nullptr;
-    explicit DevBuf(u64 n) { if (n) QCS_CUDA(cudaMalloc(&p, n * sizeof(T))); }
-    ~DevBuf() { if (p) cudaFree(p); }
+    cudaStream_t s = nullptr;
+    DevBuf(u64 n, cudaStream_t st) : s(st) {
+        if (n) QCS_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), n * sizeof(T), scratch_pool(), s));
+    }
+    ~DevBuf() { if (p) cudaFreeAsync(p, s); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
 };
@@ -243,7 +273,7 @@ struct DevBuf {
 void exclusive_scan(const u64* in, u64* out, u64 n, cudaStream_t s) {
     std::size_t bytes = 0;
     QCS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
-    DevBuf<unsigned char> tmp(bytes);
+    DevBuf<unsigned char> tmp(bytes, s);
     QCS_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s));
     note_launch();
     QCS_CUDA(cudaStreamSynchronize(s));
@@ -255,9 +285,9 @@ void exclusive_scan(const u64* in, u64* out, u64 n, cudaStream_t s) {
 u64 encode_step(const EncodeStep& host_step, bool das, u64 capacity, u64* rows_out, u64* cols_out,
                 double2* vals_out, u64* dis_out, std::uint8_t* last_out, bool out_on_device, cudaStream_t s) {
     const u64 dim = u64(1) << host_step.n;
-    DevBuf<EncodeStep> st(1);
+    DevBuf<EncodeStep> st(1, s);
     QCS_CUDA(cudaMemcpyAsync(st.p, &host_step, sizeof(EncodeStep), cudaMemcpyHostToDevice, s));
-    DevBuf<u64> counts(dim + 1), offsets(dim + 1);
+    DevBuf<u64> counts(dim + 1, s), offsets(dim + 1, s);
     QCS_CUDA(cudaMemsetAsync(counts.p + dim, 0, sizeof(u64), s));
     k_encode_count<<<grid_for(dim, 128), 128, 0, s>>>(st.p, dim, counts.p);
     check_launch("k_encode_count");
@@ -266,11 +296,13 @@ u64 encode_step(const EncodeStep& host_step, bool das, u64 capacity, u64* rows_o
     QCS_CUDA(cudaMemcpyAsync(&total, offsets.p + dim, sizeof(u64), cudaMemcpyDeviceToHost, s));
     QCS_CUDA(cudaStreamSynchronize(s));
     if (total > capacity) return total;
-    DevBuf<u64> rows(total), cols(total);
-    DevBuf<double2> vals(out_on_device ? 0 : total);
+    // scratch only where the outputs cannot take the entries directly (DAS needs no rows)
+    const bool direct = out_on_device && !das;
+    DevBuf<u64> rows(direct || das ? 0 : total, s), cols(direct ? 0 : total, s);
+    DevBuf<double2> vals(out_on_device ? 0 : total, s);
     double2* v = out_on_device ? vals_out : vals.p;
-    u64* rr = (out_on_device && !das) ? rows_out : rows.p;
-    u64* cc = (out_on_device && !das) ? cols_out : cols.p;
+    u64* rr = direct ? rows_out : rows.p;
+    u64* cc = direct ? cols_out : cols.p;
     k_encode_emit<<<grid_for(dim, 128), 128, 0, s>>>(st.p, dim, offsets.p, rr, cc, v);
     check_launch("k_encode_emit");
     if (!host_step.sorted) {
@@ -278,10 +310,10 @@ u64 encode_step(const EncodeStep& host_step, bool das, u64 capacity, u64* rows_o
         check_launch("k_sort_segments");
     }
     if (das) {
-        DevBuf<int> err(1);
+        DevBuf<int> err(1, s);
         QCS_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
-        DevBuf<u64> dis(out_on_device ? 0 : total);
-        DevBuf<std::uint8_t> last(out_on_device ? 0 : total);
+        DevBuf<u64> dis(out_on_device ? 0 : total, s);
+        DevBuf<std::uint8_t> last(out_on_device ? 0 : total, s);
         u64* dd = out_on_device ? dis_out : dis.p;
         std::uint8_t* ll = out_on_device ? last_out : last.p;
         k_das_from_dax<<<grid_for(dim, 128), 128, 0, s>>>(dim, offsets.p, cc, dd, ll, err.p);
@@ -321,7 +353,7 @@ void dax_mvm(const u64* rows, const u64* cols, const double2* vals, u64 count, c
 
 void das_mvm(const u64* dis, const std::uint8_t* last, const double2* vals, u64 count, const double2* in,
              double2* out, u64 dim, int* err_dev, cudaStream_t s) {
-    DevBuf<u64> flag(count + 1), step(count + 1), rowid(count + 1), cum(count + 1), rb(dim), re(dim);
+    DevBuf<u64> flag(count + 1, s), step(count + 1, s), rowid(count + 1, s), cum(count + 1, s), rb(dim, s), re(dim, s);
     QCS_CUDA(cudaMemsetAsync(err_dev, 0, sizeof(int), s));
     QCS_CUDA(cudaMemsetAsync(rb.p, 0, dim * sizeof(u64), s));
     QCS_CUDA(cudaMemsetAsync(re.p, 0, dim * sizeof(u64), s));
