@@ -89,6 +89,10 @@ int qcs_state_set_basis(qcs_state* s, uint64_t basis_index);
 /* Copy amplitudes [first, first+count) from / to host memory (pinned memory is fastest). */
 int qcs_state_upload(qcs_state* s, const double* host, uint64_t first, uint64_t count);
 int qcs_state_download(qcs_state* s, double* host, uint64_t first, uint64_t count);
+/* The same read-back enqueued on the state's stream without waiting: `host` must be pinned
+ * (qcs_host_alloc) and is complete after qcs_state_sync.  Lets a caller keep several states
+ * (requests) in flight, as bench.py's end-to-end arm does. */
+int qcs_state_download_async(qcs_state* s, double* host, uint64_t first, uint64_t count);
 int qcs_state_copy(qcs_state* dst, const qcs_state* src);
 int qcs_state_sync(qcs_state* s);
 /* Seeded i.i.d. Gaussian re/im, L2-normalised (a synthetic-input generator on the device). */

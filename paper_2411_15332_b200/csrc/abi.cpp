@@ -173,6 +173,21 @@ int qcs_state_download(qcs_state* s, double* host, uint64_t first, uint64_t coun
     });
 }
 
+int qcs_state_download_async(qcs_state* s, double* host, uint64_t first, uint64_t count) {
+    return guarded([&] {
+        need(s, "state");
+        need(host, "host");
+        check_range(s, first, count);
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, host) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+            cudaGetLastError();
+            qcs::raise(QCS_ERR_ARG, "asynchronous download needs pinned host memory (qcs_host_alloc)");
+        }
+        qcs::DeviceGuard g(s->device);
+        QCS_CUDA(cudaMemcpyAsync(host, s->amps + first, count * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
+    });
+}
+
 int qcs_state_copy(qcs_state* dst, const qcs_state* src) {
     return guarded([&] {
         need(dst, "dst");
