@@ -347,7 +347,7 @@ constexpr int kThreads = 256;
 #define QCS_TILE_NG 1
 #endif
 #ifndef QCS_TILE_MINB
-#define QCS_TILE_MINB 2
+#define QCS_TILE_MINB 3
 #endif
 #ifndef QCS_TILE_TMA  // tiles move as one tensor-map TMA box where the bit layout allows
 #define QCS_TILE_TMA 1
@@ -365,7 +365,8 @@ constexpr std::size_t tile_smem(int m) {
 // without gates or diagonals compiles to the lean butterfly/sign kernel.
 template <unsigned F>
 // butterfly / sign-only passes are lean enough for 3 resident tiles per SM (the smem limit);
-// passes with gates or diagonals trade residency for registers (QCS_TILE_MINB)
+// passes with gates or diagonals: QCS_TILE_MINB resident tiles (3 measured best on B200: C4
+// 1.74 -> 1.42 s, C5-shaped 3.52 -> 3.08 s, despite some spilling at 85 registers)
 __global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_MINB : (F & F_SMEM) ? 2 : 3)
     k_tile(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,
            const u64* __restrict__ flipped, const u64* __restrict__ tables, const __grid_constant__ CUtensorMap tmap) {
