@@ -352,7 +352,10 @@ constexpr int kThreads = 256;
 #ifndef QCS_TILE_TMA  // tiles move as one tensor-map TMA box where the bit layout allows
 #define QCS_TILE_TMA 1
 #endif
-constexpr int kMaxBits = 12;
+#ifndef QCS_TILE_BITS  // tile size (log2 amplitudes): 12 = 64 KB of shared memory per tile
+#define QCS_TILE_BITS 12
+#endif
+constexpr int kMaxBits = QCS_TILE_BITS;
 
 enum : unsigned { F_GATE = 1, F_DIAG = 2, F_SIGN = 4, F_SMEM = 8 };
 
