@@ -369,8 +369,9 @@ constexpr std::size_t tile_smem(int m) {
 template <unsigned F>
 // butterfly / sign-only passes are lean enough for 3 resident tiles per SM (the smem limit);
 // passes with gates or diagonals: QCS_TILE_MINB resident tiles (3 measured best on B200: C4
-// 1.74 -> 1.42 s, C5-shaped 3.52 -> 3.08 s, despite some spilling at 85 registers)
-__global__ void __launch_bounds__(kThreads, (F & (F_GATE | F_DIAG)) ? QCS_TILE_MINB : (F & F_SMEM) ? 2 : 3)
+// 1.74 -> 1.42 s, C5-shaped 3.52 -> 3.08 s; 80 registers, no spills); passes with shared-memory
+// gate rounds (a non-inlined call) keep 2 tiles and 128 registers
+__global__ void __launch_bounds__(kThreads, (F & F_SMEM) ? 2 : (F & (F_GATE | F_DIAG)) ? QCS_TILE_MINB : 3)
     k_tile(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,
            const u64* __restrict__ flipped, const u64* __restrict__ tables, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
