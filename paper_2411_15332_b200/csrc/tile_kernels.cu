@@ -1,27 +1,32 @@
 // tile_kernels.cu -- fused shared-memory passes (sm_100a).
 //
-// A pass owns a set S of m basis-bit positions, the tile bits (S always holds bits 0..2, so
-// warp accesses are 128-byte runs).  Each CTA copies the 2^m amplitudes of one tile -- the
-// indices that agree outside S -- from HBM into shared memory with cp.async (16 B per
-// request, the whole tile in flight at once), runs the pass's operations, and streams the tile
-// back: one HBM round trip, 32 B per amplitude, for the whole operation list.
+// A pass owns a set S of m basis-bit positions, the tile bits (S always holds bits 0..2, so a
+// tile is made of 128-byte runs).  Each CTA moves the 2^m amplitudes of one tile -- the indices
+// that agree outside S -- from HBM into shared memory, runs the pass's operations, and writes
+// the tile back: one HBM round trip, 32 B per amplitude, for the whole operation list.  Where
+// the bit layout fits a <= 5-dim tensor map the tile moves as ONE TMA box each way
+// (cp.async.bulk.tensor + mbarrier; the 128-byte TMA swizzle is exactly the layout below);
+// otherwise every thread issues 16-byte cp.async copies.
 //
 // Operations execute in rounds: in a round each thread holds 8 amplitudes in registers that
 // differ exactly in three tile bits (the round bits) and applies every operation of the round
 // to them; rounds are separated by one shared-memory exchange and a barrier.  Shared memory is
-// XOR-swizzled (position = j ^ ((j >> 3) & 7)) so 16-byte accesses are bank-conflict free
+// XOR-swizzled (position = j ^ ((j >> 3) & 7)) so 16-byte accesses spread over the banks
 // whichever three bits a round owns.  The pass description -- rounds and compact operations --
 // travels in the kernel parameter space (<= 32 KB), i.e. the constant bank: every thread
 // reads the same operation at the same time, which the constant cache broadcasts.
 //
-// Register operations: a one-target gate (controls anywhere; tile-bit controls are tested per
-// element group, controls outside the tile once per CTA), a diagonal phase on up to three
-// basis bits (bits outside the round are constant over a group: resolved once per group), a
-// diagonal sign step (Grover oracle / Z0, engine.cpp:62-80), unnormalised Walsh-Hadamard
-// butterflies (the RH structure, rh.cpp:92-156: scale by 2^{-n/2} first, then +-1 sums) and a
-// real scale.  Gates on 2-3 targets run straight on shared memory in rounds of their own.
-// Gate rows use dax_mvm's arithmetic (acc = 0; acc += v * x in ascending column order, each
-// operation separately rounded), so a single-gate pass reproduces the reference bit for bit.
+// Register operations: a one-target gate as a dense 2x2 (controls anywhere; tile-bit controls
+// per register, controls outside the tile once per CTA), up to three consecutive uncontrolled
+// gates bundled into one operation, a diagonal phase on up to three basis bits, +-1 diagonals
+// as pending sign flips, a diagonal sign step (Grover oracle / Z0, engine.cpp:62-80),
+// unnormalised Walsh-Hadamard butterflies (rh.cpp:92-156: scale by 2^{-n/2}, then +-1 sums)
+// and a real scale.  Gates on 2-3 targets run straight on shared memory in rounds of their
+// own.  Tiles no sign step reaches run the pass's simplified program, or nothing.
+//
+// Arithmetic: a fused pass reorders the reference's per-step fold anyway, so it is held to the
+// 1e-12 bar and uses fused multiply-adds (half the FP64 instructions).  Passes of a single
+// operation never come here: the engine runs them with the bit-exact gate kernels.
 #include <algorithm>
 #include <cstdint>
 
