@@ -79,6 +79,15 @@ struct TileOp {
 
 // RegOp::kind flags above the kind bits
 constexpr int KF_KIND = 0x0f;
+// KF_BUNDLE on a +-1 diagonal (KF_SIGNED): a run of them; smask low byte = the flips of the ones
+// with no group-constant bit, pool[ref .. ref + t) = SignEntry for the others
+struct SignEntry {
+    std::uint32_t smask;      // byte cg = registers that flip when the constant bits spell cg
+    std::uint8_t dk, p0, p1;  // phase bits; basis positions of the constant ones
+    std::uint8_t cmask;       // bit 0: phase bit 0 is constant over a group, bit 1: phase bit 1
+    std::uint64_t pad;
+};
+static_assert(sizeof(SignEntry) == 16, "one pool slot");
 constexpr int KF_BUNDLE = 0x10;  // TOP_GATE: dense gates on the register bits of mask t, coefficients
                                  // in PassParams::pool[ref + 4 * bit] (m00 m01 m10 m11 per bit)
 constexpr int KF_FLUSH = 0x20;   // apply the pending +-1 sign flips before this op (set by the planner)

@@ -519,6 +519,40 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                     o.kind = std::uint8_t(o.kind | KF_FLUSH);
                     pending_signs = false;
                 }
+                // consecutive +-1 diagonals (CZ rings, Z): one bundled operation; the ones with
+                // no group-constant bit fold into one flip byte at plan time
+                if (o.kind == (TOP_DIAG | KF_SIGNED) && nops > rd.op_begin) {
+                    RegOp& prev = P.ops[nops - 1];
+                    auto add_entry = [&](const RegOp& x, RegOp& b) {
+                        const bool c0 = x.dreg[0] == 0xff, c1 = x.dk == 2 && x.dreg[1] == 0xff;
+                        if (!c0 && !c1) {
+                            b.smask ^= x.smask & 0xffu;
+                            return;
+                        }
+                        SignEntry e{};
+                        e.smask = x.smask;
+                        e.dk = x.dk;
+                        e.p0 = x.dpos[0];
+                        e.p1 = x.dpos[1];
+                        e.cmask = std::uint8_t((c0 ? 1u : 0u) | (c1 ? 2u : 0u));
+                        std::memcpy(&P.pool[npool++], &e, sizeof(e));
+                        b.t = std::uint8_t(b.t + 1);
+                    };
+                    const bool prev_sign = (prev.kind & ~KF_BUNDLE) == (TOP_DIAG | KF_SIGNED);
+                    if (prev_sign && npool + 2 <= kPassPool && prev.t < 250) {
+                        if (!(prev.kind & KF_BUNDLE)) {
+                            RegOp b = prev;
+                            b.kind = std::uint8_t(b.kind | KF_BUNDLE);
+                            b.smask = 0;
+                            b.t = 0;
+                            b.ref = std::uint16_t(npool);
+                            add_entry(prev, b);
+                            prev = b;
+                        }
+                        add_entry(o, prev);
+                        continue;
+                    }
+                }
                 // consecutive uncontrolled one-qubit gates on different register bits: one
                 // bundled operation (one dispatch per group instead of up to three)
                 if (f.kind == TOP_GATE && !(rd.flags & RD_SMEM) && o.kind == TOP_GATE && !o.lctrl_mask &&

@@ -496,6 +496,24 @@ __global__ void __launch_bounds__(kThreads, (F & F_SMEM) ? 2 : (F & (F_GATE | F_
                 const int kb = o.kind;  // low bits: kind; KF_GCTRL: controls outside the tile
                 if ((F & F_DIAG) && (kb & KF_FLUSH)) flip_signs<NG>(v, negacc);  // before a butterfly / gate
                 if ((kb & KF_GCTRL) && (base & o.gctrl_mask) != o.gctrl_val) continue;
+                if ((F & F_DIAG) && (kb & KF_SIGNED) && (kb & KF_BUNDLE)) {
+                    const auto* e = reinterpret_cast<const SignEntry*>(P.pool + o.ref);
+                    const int ne = o.t;
+                    const unsigned cst = o.smask & 0xffu;
+#pragma unroll
+                    for (int r = 0; r < NG; ++r) {
+                        unsigned acc = cst;
+                        for (int i = 0; i < ne; ++i) {
+                            const unsigned sm_ = e[i].smask, cmk = e[i].cmask, dk = e[i].dk;
+                            int cg = 0;
+                            if (cmk & 1u) cg |= int((g0[r] >> e[i].p0) & 1) << (dk - 1);
+                            if (cmk & 2u) cg |= int((g0[r] >> e[i].p1) & 1);
+                            acc ^= (sm_ >> (8 * cg)) & 0xffu;
+                        }
+                        negacc[r] ^= acc;
+                    }
+                    continue;
+                }
                 if ((F & F_DIAG) && (kb & KF_SIGNED)) {
                     // +-1 diagonal: the host tabulated, for each value of the bits that are
                     // constant over the group, which registers flip (one byte per value)
