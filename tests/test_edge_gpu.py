@@ -1,0 +1,112 @@
+"""Edge cases through the B200 engine against the oracle: empty and one-qubit circuits,
+non-zero initial basis states, degenerate sign steps, and fused random circuits over the whole
+catalog on multi-tile states (shared-memory gate rounds, controls inside and outside the
+tile, bundles, missed-tile programs).  Bars as in test_parity_gpu.py."""
+import numpy as np
+import pytest
+
+from conftest import bits_equal, canon_zero
+
+pytestmark = pytest.mark.gpu
+
+TOL_AMP = 1e-12
+TOL_L2 = 1e-10
+
+
+@pytest.fixture(scope="module")
+def Q():
+    from paper_2411_15332_b200 import qcsim
+    return qcsim
+
+
+def oracle_run(oracle, c):
+    x = np.zeros(1 << c.n, np.complex128)
+    x[c.initial] = 1
+    for st in c.steps:
+        if int(st.kind) == 1:
+            x = oracle.apply_diag(c.n, sorted(set(st.diag.flipped)), st.diag.flip_rest, x)
+        elif st.is_hadamard_all(c.n):
+            x = oracle.wht(c.n, x)
+        else:
+            x = oracle.apply_step(c.n, [(p.qubit_list(), p.gate.matrix) for p in st.placements], x)
+    return x
+
+
+def test_empty_circuit_is_the_basis_state(Q):
+    for n, init in ((1, 0), (1, 1), (9, 300), (13, 8191)):
+        rep = Q.simulate(Q.Circuit(n, [], init), Q.Engine.rh_dax)
+        want = np.zeros(1 << n, np.complex128)
+        want[init] = 1
+        assert bits_equal(rep.final.download(), want)
+        assert rep.steps == [] and rep.total_madd_count == 0
+
+
+@pytest.mark.parametrize("engine", ["dense", "dax", "das", "rh_dax"])
+def test_one_qubit_circuits(Q, oracle, engine):
+    G = Q.gate_catalog_lookup
+    for init in (0, 1):
+        c = Q.Circuit(1, [Q.hadamard_all(1), Q.CircuitStep.of_gates([Q.Placement(G("T"), 0)]),
+                          Q.CircuitStep.of_diag(Q.DiagSign([1], False)), Q.hadamard_all(1),
+                          Q.CircuitStep.of_gates([Q.Placement(G("RY", [0.4]), 0)])], init)
+        want = oracle_run(oracle, c)
+        for fuse in (False, True):
+            got = Q.simulate(c, getattr(Q.Engine, engine), Q.SimOptions(fuse=fuse)).final.download()
+            assert np.abs(got - want).max() <= TOL_AMP, (engine, init, fuse)
+
+
+def test_degenerate_sign_steps(Q, oracle):
+    """Duplicated indices flip once, an empty list without flip_rest is the identity, an empty
+    list with flip_rest negates everything: bit-exact one step at a time, within the bar fused
+    between other steps."""
+    from conftest import random_state
+    n = 14
+    rng = np.random.default_rng(9)
+    signs = [Q.DiagSign([5, 5, 77, 5], False), Q.DiagSign([], False), Q.DiagSign([], True),
+             Q.DiagSign([int(i) for i in rng.choice(1 << n, 200, replace=False)], True)]
+    x = random_state(n, 21)
+    s = Q.DeviceState.from_numpy(x)
+    want = x
+    for d in signs:
+        s.apply_diag(d)
+        want = oracle.apply_diag(n, sorted(set(d.flipped)), d.flip_rest, want)
+        assert bits_equal(s.download(), want)
+    steps = [Q.hadamard_all(n)] + [Q.CircuitStep.of_diag(d) for d in signs[:3]]
+    steps += [Q.CircuitStep.of_gates([Q.Placement(Q.gate_catalog_lookup("RX", [0.9]), 3)]),
+              Q.CircuitStep.of_diag(signs[3]), Q.hadamard_all(n)]
+    c = Q.Circuit(n, steps, 17)
+    want = oracle_run(oracle, c)
+    for fuse in (True, False):
+        got = Q.simulate(c, Q.Engine.rh_dax, Q.SimOptions(fuse=fuse)).final.download()
+        assert np.abs(got - want).max() <= TOL_AMP, fuse
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_catalog_circuits_fused(Q, oracle, seed):
+    """Random circuits over all 38 catalog gates (any arity, reversed / non-adjacent qubits) on
+    n = 13..17: several 12-bit tiles, so every kind of tile operation and round meets tile
+    boundaries.  Fused and stepwise against the oracle."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(13, 18))
+    infos = Q.gate_catalog()
+    steps = [Q.hadamard_all(n)]
+    for _ in range(40):
+        used, pl = set(), []
+        for _ in range(int(rng.integers(1, 4))):
+            info = infos[int(rng.integers(0, len(infos)))]
+            free = [q for q in range(n) if q not in used]
+            if len(free) < info.arity:
+                break
+            qs = [int(q) for q in rng.choice(free, info.arity, replace=False)]
+            used.update(qs)
+            g = Q.gate_catalog_lookup(info.name, list(rng.uniform(0, 2 * np.pi, info.param_count)))
+            pl.append(Q.Placement(g, qubits=qs))
+        if pl:
+            steps.append(Q.CircuitStep.of_gates(pl))
+        if rng.random() < 0.15:
+            steps.append(Q.CircuitStep.of_diag(Q.DiagSign([int(rng.integers(0, 1 << n))], bool(rng.random() < 0.5))))
+    c = Q.Circuit(n, steps, int(rng.integers(0, 1 << n)))
+    want = oracle_run(oracle, c)
+    for fuse in (True, False):
+        got = Q.simulate(c, Q.Engine.rh_dax, Q.SimOptions(fuse=fuse)).final.download()
+        assert np.abs(got - want).max() <= TOL_AMP, fuse
+        assert np.linalg.norm(got - want) <= TOL_L2, fuse
