@@ -181,3 +181,67 @@ def test_gloo_ranks_match_full_state(oracle, tmp_path, world, name):
                        start_method="spawn")
     want = oracle_full(oracle, circuits()[name])
     assert np.abs(np.load(path) - want).max() < 1e-12
+
+
+class _SharedPeerTransport:
+    """gloo processes whose shards live in shared memory: peer_buffer maps the partner's shard
+    (the CPU stand-in for NVLink peer memory), barrier is the gloo barrier."""
+
+    def __init__(self, shards):
+        from paper_2411_15332_b200.partition import DistTransport
+        self.inner = DistTransport()
+        self.shards = shards
+
+    def exchange(self, send, recv, peer):
+        self.inner.exchange(send, recv, peer)
+
+    def peer_buffer(self, peer):
+        return self.shards[peer]
+
+    def barrier(self):
+        dist.barrier()
+
+
+def _gloo_peer_worker(rank, world, port, name, shards, result_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle_py import Oracle
+    from paper_2411_15332_b200.partition import ShardedState
+    Oracle.lib()
+    c = circuits()[name]
+    g = world.bit_length() - 1
+    backend = OracleBackend(c.n - g, Oracle)
+    backend.tensor = shards[rank]  # this rank's shard is the shared one the partners map
+    st = ShardedState(c.n, world, rank, backend, _SharedPeerTransport(shards), initial=c.initial, chunk_elems=5)
+    assert st.peer
+    run_ops(st, circuit_ops(c))
+    st.flush()
+    dist.barrier()
+    amap = torch.from_numpy(st.logical_amplitude_map())
+    maps = [torch.zeros_like(amap) for _ in range(world)] if rank == 0 else None
+    dist.gather(amap, maps, dst=0)
+    if rank == 0:
+        full = np.zeros(1 << c.n, dtype=np.complex128)
+        for r, mp_ in enumerate(maps):
+            full[mp_.numpy()] = shards[r].numpy()
+        np.save(result_path, np.array([full, st.splits], dtype=object), allow_pickle=True)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,name", [(2, "c4"), (4, "grover"), (2, "c5")])
+def test_gloo_peer_mode_match_full_state(oracle, tmp_path, world, name):
+    """World 2 / 4 processes over gloo in peer mode: gates mixing one global qubit run on the
+    partner's shard directly (mapped through shared memory here, NVLink on the GPU box)."""
+    c = circuits()[name]
+    g = world.bit_length() - 1
+    shards = [torch.zeros(1 << (c.n - g), dtype=torch.complex128).share_memory_() for _ in range(world)]
+    path = str(tmp_path / "full.npy")
+    mp.start_processes(_gloo_peer_worker, args=(world, _free_port(), name, shards, path), nprocs=world, join=True,
+                       start_method="spawn")
+    full, splits = np.load(path, allow_pickle=True)
+    assert np.abs(full - oracle_full(oracle, c)).max() < 1e-12
+    assert splits > 0
