@@ -110,3 +110,30 @@ def test_random_catalog_circuits_fused(Q, oracle, seed):
         got = Q.simulate(c, Q.Engine.rh_dax, Q.SimOptions(fuse=fuse)).final.download()
         assert np.abs(got - want).max() <= TOL_AMP, fuse
         assert np.linalg.norm(got - want) <= TOL_L2, fuse
+
+
+def test_abi_argument_errors(Q):
+    """The B200-only entry points fail loudly on bad arguments (status codes, no crash)."""
+    import ctypes as C
+    L = Q.L
+    lib = L.lib()
+    s = Q.DeviceState(6)
+    buf = np.zeros(2 << 6)
+    rc = lib.qcs_state_download_async(s.handle, buf.ctypes.data_as(C.c_void_p), 0, 1 << 6)
+    assert rc == L.QCS_ERR_ARG  # pageable memory: only pinned buffers may be read back asynchronously
+    hp = C.c_void_p()
+    Q._check(lib.qcs_host_alloc(16 << 6, C.byref(hp)))
+    try:
+        Q._check(lib.qcs_state_download_async(s.handle, hp, 0, 1 << 6))
+        s.sync()
+    finally:
+        lib.qcs_host_free(hp)
+    blocks = np.eye(2, dtype=np.complex128).reshape(1, 2, 2)
+    bp = blocks.ctypes.data_as(C.POINTER(C.c_double))
+    assert lib.qcs_apply_split(s.handle, None, 0, 0, None, bp, 0) == L.QCS_ERR_ARG
+    import torch
+    t = torch.zeros(1 << 6, dtype=torch.complex128, device="cuda")  # a partner shard
+    assert lib.qcs_apply_split(s.handle, C.c_void_p(t.data_ptr()), 2, 0, None, bp, 0) == L.QCS_ERR_ARG
+    sel = (C.c_int * 1)(9)
+    assert lib.qcs_apply_split(s.handle, C.c_void_p(t.data_ptr()), 0, 1, sel, bp, 0) == L.QCS_ERR_DIMENSION
+    assert lib.qcs_apply_split(s.handle, C.c_void_p(t.data_ptr()), 0, 3, sel, bp, 0) == L.QCS_ERR_ARG
