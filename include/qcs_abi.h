@@ -209,6 +209,11 @@ typedef struct qcs_plan_info {
 } qcs_plan_info;
 int qcs_plan_stats(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
                    qcs_plan_info* out);
+/* Generate and compile (NVRTC, host only) the specialised kernel of every tile pass of that
+ * plan -- the kernels qcs_simulate runs for passes with enough work (QCS_JIT=force: all).
+ * *kernels = passes compiled, *cubin_bytes = total code size.  B200-specific check/tool. */
+int qcs_plan_compile(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
+                     int64_t* kernels, int64_t* cubin_bytes);
 
 /* ------------------------------------------------------------------ compressed structures
  * The device gate encoder: materialise step_matrix_dax / step_matrix_das (engine.hpp:38-39)

@@ -26,7 +26,10 @@ COMMON = ["-O3", "-std=c++20", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC"
 COMMON += os.environ.get("QCS_EXTRA_NVCC", "").split()
 
 SOURCES = ["gates.cpp", "ops.cpp", "planner.cpp", "engine.cpp", "abi.cpp", "timing.cpp",
-           "gate_kernels.cu", "tile_kernels.cu", "state_kernels.cu", "encode_kernels.cu", "peer_kernels.cu"]
+           "gate_kernels.cu", "tile_kernels.cu", "state_kernels.cu", "encode_kernels.cu", "peer_kernels.cu",
+           "jit.cpp"]
+# embedded into the library for the run-time (NVRTC) pass kernels, jit.cpp
+JIT_HEADERS = [("kJitSrcKernels", "kernels.hpp"), ("kJitSrcDevice", "tile_device.cuh")]
 
 
 def _hash(paths):
@@ -38,8 +41,24 @@ def _hash(paths):
     return h.hexdigest()[:16]
 
 
+def _embed_jit_sources() -> str:
+    """_build/jit_src.cpp: the device headers as string constants for NVRTC (jit.cpp)."""
+    path = os.path.join(OBJ, "jit_src.cpp")
+    parts = ["namespace qcs {"]
+    for sym, name in JIT_HEADERS:
+        with open(os.path.join(CSRC, name)) as f:
+            text = f.read()
+        if ")qcsjit\"" in text:
+            raise RuntimeError(f"{name} contains the raw-string delimiter")
+        parts.append(f'extern const char* const {sym};\nconst char* const {sym} = R"qcsjit({text})qcsjit";')
+    parts.append("}  // namespace qcs\n")
+    with open(path, "w") as f:
+        f.write("\n".join(parts))
+    return path
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".hpp")]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "qcs_abi.h"))
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     stamp = os.path.join(OBJ, "stamp")
@@ -47,6 +66,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if not force and os.path.exists(OUT) and os.path.exists(stamp) and open(stamp).read() == digest:
         return OUT
     os.makedirs(OBJ, exist_ok=True)
+    srcs = srcs + [_embed_jit_sources()]
     objs = []
     procs = []
     for s in srcs:
@@ -67,7 +87,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if failed:
         msg = "\n".join(f"--- {s}\n{o}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    link = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-Xcompiler", "-fPIC"]
+    cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+    link = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-Xcompiler", "-fPIC", "-lnvrtc", "-L" + cudalib,
+            "-Xlinker", "-rpath=" + cudalib]
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.run(link, check=True)

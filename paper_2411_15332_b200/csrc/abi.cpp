@@ -354,6 +354,15 @@ int qcs_plan_stats(int n, const qcs_step* steps, int num_steps, int engine, cons
     });
 }
 
+int qcs_plan_compile(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
+                     int64_t* kernels, int64_t* cubin_bytes) {
+    return guarded([&] {
+        need(kernels, "kernels");
+        need(cubin_bytes, "cubin_bytes");
+        qcs::plan_compile(n, steps, num_steps, engine, opts, kernels, cubin_bytes);
+    });
+}
+
 // ---------------------------------------------------------------- compressed structures
 
 int qcs_step_dax(int n, const qcs_placement* placements, int num_placements, int device, uint64_t* rows,

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -469,6 +470,7 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
     }
     if (o.fuse) {
         merge_single_qubit(n, ops);
+        split_phases(ops);
         run_fused(s, ops);
     }
 }
@@ -484,7 +486,9 @@ void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out) {
     }
     Lowered low;
     lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
+    const bool dump = std::getenv("QCS_PLAN_DUMP") != nullptr;  // planner debugging: rounds and ops
     for (std::size_t i = 0; i < low.passes.size(); ++i) {
+        if (dump) dump_pass(stderr, low.passes[i], low.pass_ops[i].size());
         ++out->passes;
         if (low.pass_ops[i].size() == 1) {
             ++out->single_passes;
@@ -521,7 +525,39 @@ void plan_stats(int n, const qcs_step* steps, int nsteps, int engine, const qcs_
     }
     if (o.fuse) {
         merge_single_qubit(n, ops);
+        split_phases(ops);
         add_plan_stats(n, ops, out);
+    }
+}
+
+void plan_compile(int n, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
+                  std::int64_t* kernels, std::int64_t* cubin_bytes) {
+    validate_circuit(n, steps, nsteps);
+    if (engine < QCS_ENGINE_DENSE || engine > QCS_ENGINE_RH_DAX) raise(QCS_ERR_ARG, "unknown engine");
+    qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1};
+    if (opts) o = *opts;
+    *kernels = 0;
+    *cubin_bytes = 0;
+    std::vector<FOp> ops;
+    auto flush = [&] {
+        if (ops.empty() || n < 3) return;
+        Lowered low;
+        lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
+        for (std::size_t i = 0; i < low.passes.size(); ++i) {
+            if (low.pass_ops[i].size() == 1) continue;
+            *cubin_bytes += std::int64_t(jit_compile_only(low.passes[i]));
+            ++*kernels;
+        }
+        ops.clear();
+    };
+    for (int i = 0; i < nsteps; ++i) {
+        append_step_ops(n, steps[i], engine == QCS_ENGINE_RH_DAX && is_hadamard_all(steps[i], n), ops);
+        if (!o.fuse) flush();
+    }
+    if (o.fuse) {
+        merge_single_qubit(n, ops);
+        split_phases(ops);
+        flush();
     }
 }
 

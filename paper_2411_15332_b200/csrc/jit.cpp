@@ -1,0 +1,314 @@
+// jit.cpp -- per-pass specialised tile kernels, generated and compiled at run time (NVRTC).
+//
+// The interpreter kernel k_tile (tile_kernels.cu) walks each pass's operation list from the
+// kernel parameter space: every group of 8 amplitudes pays for the operation dispatch, the
+// coefficient loads and -- because all operation kinds share one register assignment -- the
+// register moves that reconcile the kinds' code paths.  Gate-heavy passes (C4, C5) are issue
+// bound on exactly that overhead (profiles/r01_ncu_full_tile_c4.json).  Here the pass's
+// STRUCTURE -- rounds, register bits, operation kinds, target bits, control masks, sign tables --
+// becomes straight-line CUDA source built from the same device building blocks
+// (tile_device.cuh), so the generated kernel does exactly the interpreter's arithmetic in the
+// same order (bit-identical results) without any of the dispatch.  Coefficients stay in the
+// kernel parameters, so one compiled kernel serves every pass of the same structure (the layers
+// of a circuit, circuits with new angles).  Kernels are cached by their source text.
+#include <cuda.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace qcs {
+
+extern const char* const kJitSrcKernels;  // kernels.hpp and tile_device.cuh, embedded by build.py
+extern const char* const kJitSrcDevice;
+
+namespace {
+
+struct Out {
+    std::string s;
+    void operator()(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
+        char buf[1024];
+        va_list ap;
+        va_start(ap, fmt);
+        const int k = std::vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        if (k >= int(sizeof(buf))) raise(QCS_ERR_SIM, "internal: generated line too long");
+        s += buf;
+    }
+};
+
+// the cg (value of the group-constant phase bits) expression of a +-1 diagonal, as source
+std::string const_bits(bool c0, bool c1, int dk, int p0, int p1) {
+    std::string e = "0";
+    char buf[128];
+    if (c0) {
+        std::snprintf(buf, sizeof(buf), " | (int((g0 >> %d) & 1) << %d)", p0, dk - 1);
+        e += buf;
+    }
+    if (c1) {
+        std::snprintf(buf, sizeof(buf), " | int((g0 >> %d) & 1)", p1);
+        e += buf;
+    }
+    return e;
+}
+
+// One register round: the interpreter's round loop (tile_kernels.cu) with every structural
+// field of the operations as a literal.
+void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) {
+    const RoundDesc& R = P.rounds[ri];
+    const unsigned ngroups = (1u << P.m) >> 3;
+    unsigned off[8];
+    for (int q = 0; q < 8; ++q)
+        off[q] = ((q & 1) ? 1u << R.r[0] : 0u) | ((q & 2) ? 1u << R.r[1] : 0u) | ((q & 4) ? 1u << R.r[2] : 0u);
+    auto swz = [](unsigned j) { return j ^ ((j >> 3) & 7u); };
+    o("  {  // round %d: register bits %d %d %d\n", ri, R.r[0], R.r[1], R.r[2]);
+    o("#pragma unroll 1\n");
+    o("    for (unsigned gb = t; gb < %uu; gb += %uu) {\n", ngroups, threads);
+    o("      const unsigned lb = insert_zero(insert_zero(insert_zero(gb, %d), %d), %d);\n", R.r[0], R.r[1], R.r[2]);
+    o("      const unsigned slb = swz(lb);\n");
+    o("      double2 v[8];\n");
+    for (int q = 0; q < 8; ++q) o("      v[%d] = sm[slb ^ %uu];\n", q, swz(off[q]));
+    o("      const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];\n");
+    o("      unsigned negacc = 0;\n");
+    o("      (void)g0;\n");
+    for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
+        const RegOp& op = P.ops[oi];
+        const int kb = op.kind, kind = kb & KF_KIND;
+        if (kb & KF_FLUSH) o("      flip_signs1(v, negacc);\n");
+        const bool gc = kb & KF_GCTRL;
+        if (gc) o("      if ((base & 0x%llxull) == 0x%llxull) {\n", (unsigned long long)op.gctrl_mask,
+                  (unsigned long long)op.gctrl_val);
+        if ((kb & KF_SIGNED) && (kb & KF_BUNDLE)) {
+            o("      { unsigned acc = 0x%xu;\n", op.smask & 0xffu);
+            for (int i = 0; i < op.t; ++i) {
+                SignEntry e;
+                std::memcpy(&e, &P.pool[op.ref + i], sizeof(e));
+                o("        acc ^= (0x%xu >> (8 * (%s))) & 0xffu;\n", e.smask,
+                  const_bits(e.cmask & 1u, e.cmask & 2u, e.dk, e.p0, e.p1).c_str());
+            }
+            o("        negacc ^= acc; }\n");
+        } else if (kb & KF_SIGNED) {
+            const bool c0 = op.dreg[0] == 0xff, c1 = op.dk == 2 && op.dreg[1] == 0xff;
+            o("      negacc ^= (0x%xu >> (8 * (%s))) & 0xffu;\n", op.smask,
+              const_bits(c0, c1, op.dk, op.dpos[0], op.dpos[1]).c_str());
+        } else if (kind == TOP_WHT) {
+            for (int b = 0; b < 3; ++b)
+                if (op.t >> b & 1) o("      butterfly<%d>(v);\n", b);
+        } else if (kind == TOP_SCALE) {
+            o("      { const double sc = P.ops[%d].c[0].x;\n", oi);
+            o("        for (int q = 0; q < 8; ++q) v[q] = make_double2(v[q].x * sc, v[q].y * sc); }\n");
+        } else if (kind == TOP_GATE && (kb & KF_BUNDLE)) {
+            for (int b = 0; b < 3; ++b)
+                if (op.t >> b & 1)
+                    o("      %s<%d, false>(v, P.pool + %d, 0xffu);\n", (kb & KF_REAL) ? "gate1r" : "gate1", b,
+                      op.ref + 4 * b);
+        } else if (kind == TOP_GATE) {
+            const char* g = (kb & KF_REAL) ? "gate1r" : "gate1";
+            if (op.lctrl_mask) {
+                o("      { unsigned en = 0;\n");
+                for (int q = 0; q < 8; ++q)
+                    o("        en |= unsigned(((lb | %uu) & %uu) == %uu) << %d;\n", off[q], op.lctrl_mask, op.lctrl_val, q);
+                o("        %s<%d, true>(v, P.ops[%d].c, en); }\n", g, op.t, oi);
+            } else {
+                o("      %s<%d, false>(v, P.ops[%d].c, 0xffu);\n", g, op.t, oi);
+            }
+        } else if (kind == TOP_DTAB) {
+            for (int q = 0; q < 8; ++q)
+                if (!(op.dskip >> q & 1)) o("      v[%d] = cmul_f(P.pool[%d], v[%d]);\n", q, op.ref + q, q);
+        } else if (kind == TOP_DIAG) {
+            if (op.dk == 1 && op.dreg[0] == 0xff) {
+                o("      { const int g = int((g0 >> %d) & 1);\n", op.dpos[0]);
+                o("        if (!((%uu >> g) & 1u)) { const double2 d = g ? P.ops[%d].c[1] : P.ops[%d].c[0];\n",
+                  unsigned(op.dskip), oi, oi);
+                o("          for (int q = 0; q < 8; ++q) v[q] = cmul_f(d, v[q]); } }\n");
+            } else if (op.dk == 1) {
+                o("      diag_reg<%d>(v, P.ops[%d].c[0], P.ops[%d].c[1], %uu);\n", op.dreg[0], oi, oi, unsigned(op.dskip));
+            } else {
+                o("      diag_op(v, P.ops[%d], big, g0);\n", oi);
+            }
+        } else if (kind == TOP_SIGN) {
+            o("      { const TileOp& so = big[%d];\n", op.ref);
+            o("        if (!(sign_hit >> %u & 1u)) {\n", op.sidx & 31u);
+            o("          if (so.flip_rest) { for (int q = 0; q < 8; ++q) v[q] = neg_exact(v[q]); }\n");
+            o("        } else {\n");
+            o("          const u64* f = flipped + so.flip_off;\n");
+            for (int q = 0; q < 8; ++q) {
+                o("          { const unsigned j = lb | %uu; const u64 gi = base | (j & 7u) | hi_tab[j >> 3];\n", off[q]);
+                o("            if (listed(f, so.flip_cnt, gi) != (so.flip_rest != 0)) v[%d] = neg_exact(v[%d]); }\n", q, q);
+            }
+            o("        } }\n");
+        } else {
+            raise(QCS_ERR_SIM, "internal: operation kind without a generated form");
+        }
+        if (gc) o("      }\n");
+    }
+    if (R.flags & RD_SIGNS) o("      flip_signs1(v, negacc);\n");
+    for (int q = 0; q < 8; ++q) o("      sm[slb ^ %uu] = v[%d];\n", swz(off[q]), q);
+    o("    }\n    __syncthreads();\n  }\n");
+}
+
+void emit_smem_round(Out& o, const PassParams& P, int ri, unsigned threads) {
+    const RoundDesc& R = P.rounds[ri];
+    o("  {  // round %d: gates on 2-3 targets in shared memory\n", ri);
+    for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
+        o("    { const TileOp& o = big[%d];\n", P.ops[oi].ref);
+        o("      if (!(o.gctrl_mask && (base & o.gctrl_mask) != o.gctrl_val)) {\n");
+        o("        if (o.gcase == 2) smem_gate<2>(sm, o, %d, %uu); else smem_gate<3>(sm, o, %d, %uu);\n", P.m, threads,
+          P.m, threads);
+        o("      }\n      __syncthreads(); }\n");
+    }
+    o("  }\n");
+}
+
+void emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threads) {
+    for (int ri = begin; ri < end; ++ri) {
+        if (P.rounds[ri].flags & RD_SMEM) emit_smem_round(o, P, ri, threads);
+        else emit_register_round(o, P, ri, threads);
+    }
+}
+
+std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
+    Out o;
+    const int minb = (F & 8u) ? 2 : 3;
+    o("#include \"tile_device.cuh\"\n");
+    o("using namespace qcs;\nusing namespace qcs::tile;\n");
+    o("extern \"C\" __global__ void __launch_bounds__(%u, %d)\n", threads, minb);
+    o("qcs_pass(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,\n");
+    o("         const u64* __restrict__ flipped, const u64* __restrict__ tables, const __grid_constant__ TmapParam tmap) {\n");
+    o("  extern __shared__ __align__(1024) unsigned char smem_raw[];\n");
+    o("  TileCtx c;\n");
+    o("  if (!tile_begin<%uu>(a, P, big, flipped, tables, tmap, smem_raw, c)) return;\n", F);
+    o("  double2* const sm = c.sm;\n  const u64* const hi_tab = c.hi_tab;\n  const u64 base = c.base;\n");
+    o("  const unsigned sign_hit = c.sign_hit;\n  const unsigned t = threadIdx.x;\n");
+    o("  (void)sign_hit; (void)hi_tab;\n");
+    if (P.alt_mode == ALT_ROUNDS) {
+        o("  if (c.rb == 0 && c.re == %d) {\n", P.nrounds);
+        emit_rounds(o, P, 0, P.nrounds, threads);
+        o("  } else {\n");
+        emit_rounds(o, P, P.alt_begin, P.alt_begin + P.alt_nrounds, threads);
+        o("  }\n");
+    } else {
+        emit_rounds(o, P, 0, P.nrounds, threads);
+    }
+    o("  tile_end(a, P, tmap, c);\n}\n");
+    return o.s;
+}
+
+void nvrtc_check(nvrtcResult r, const char* what) {
+    if (r != NVRTC_SUCCESS) raise(QCS_ERR_SIM, std::string(what) + ": " + nvrtcGetErrorString(r));
+}
+
+struct JitKernel {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kernel = nullptr;
+    std::set<int> attr_devices;  // devices whose dynamic shared-memory limit is raised
+};
+
+std::mutex g_mu;
+std::map<std::string, std::unique_ptr<JitKernel>> g_cache;
+std::atomic<unsigned long long> g_compiles{0};
+
+std::vector<char> compile_cubin(const std::string& src) {
+    nvrtcProgram prog;
+    const char* headers[] = {kJitSrcKernels, kJitSrcDevice};
+    const char* names[] = {"kernels.hpp", "tile_device.cuh"};
+    nvrtc_check(nvrtcCreateProgram(&prog, src.c_str(), "qcs_pass.cu", 2, headers, names), "nvrtcCreateProgram");
+    const char* opts[] = {"-arch=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo", "-default-device"};
+    const nvrtcResult rc = nvrtcCompileProgram(prog, 5, opts);
+    if (rc != NVRTC_SUCCESS) {
+        std::size_t n = 0;
+        nvrtcGetProgramLogSize(prog, &n);
+        std::string log(n, '\0');
+        nvrtcGetProgramLog(prog, log.data());
+        nvrtcDestroyProgram(&prog);
+        raise(QCS_ERR_SIM, "pass kernel compilation failed: " + log.substr(0, 2000));
+    }
+    std::size_t n = 0;
+    nvrtc_check(nvrtcGetCUBINSize(prog, &n), "nvrtcGetCUBINSize");
+    std::vector<char> cubin(n);
+    nvrtc_check(nvrtcGetCUBIN(prog, cubin.data()), "nvrtcGetCUBIN");
+    nvrtcDestroyProgram(&prog);
+    return cubin;
+}
+
+JitKernel& compile(const std::string& src) {
+    // callers hold g_mu
+    auto it = g_cache.find(src);
+    if (it != g_cache.end()) return *it->second;
+    const std::vector<char> cubin = compile_cubin(src);
+    const std::size_t n = cubin.size();
+    auto k = std::make_unique<JitKernel>();
+    QCS_CUDA(cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    QCS_CUDA(cudaLibraryGetKernel(&k->kernel, k->lib, "qcs_pass"));
+    ++g_compiles;
+    if (std::getenv("QCS_JIT_DUMP")) std::fprintf(stderr, "---- qcs_pass (%zu bytes cubin)\n%s", n, src.c_str());
+    auto& ref = *k;
+    g_cache.emplace(src, std::move(k));
+    return ref;
+}
+
+}  // namespace
+
+int jit_mode() {
+    static const int mode = [] {
+        const char* v = std::getenv("QCS_JIT");
+        if (!v || !*v) return 1;                       // default: passes with enough work
+        if (!std::strcmp(v, "force")) return 2;        // every tile pass (tests)
+        return std::atoi(v) != 0 ? 1 : 0;
+    }();
+    return mode;
+}
+
+unsigned long long jit_compiles() { return g_compiles.load(); }
+
+std::size_t jit_compile_only(const PassParams& p) {
+    unsigned F = 0, threads = 0;
+    tile_pass_shape(p, F, threads);
+    return compile_cubin(pass_source(p, F, threads)).size();
+}
+
+bool launch_tile_pass_jit(double2* amps, const PassParams& p, unsigned F, const TileOp* big_dev,
+                          const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, const TmapParam& tmap,
+                          unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st) {
+    const int mode = jit_mode();
+    if (mode == 0) return false;
+    // worth a compile (~0.5 s, once per structure): enough tiles x rounds of work
+    if (mode == 1 && (double(tiles) * double(p.nrounds) < 32768.0 || p.nrounds < 2)) return false;
+    const std::string src = pass_source(p, F, threads);
+    int dev = 0;
+    QCS_CUDA(cudaGetDevice(&dev));
+    cudaKernel_t kern;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        JitKernel& k = compile(src);
+        if (!k.attr_devices.count(dev)) {
+            QCS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k.kernel),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)));
+            QCS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k.kernel),
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            k.attr_devices.insert(dev);
+        }
+        kern = k.kernel;
+    }
+    void* a = amps;
+    const void* b = big_dev;
+    const void* f = flipped_dev;
+    const void* tb = tables_dev;
+    void* args[] = {&a, const_cast<PassParams*>(&p), &b, &f, &tb, const_cast<TmapParam*>(&tmap)};
+    QCS_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(kern), dim3(tiles), dim3(threads), args, smem, st));
+    return true;
+}
+
+}  // namespace qcs

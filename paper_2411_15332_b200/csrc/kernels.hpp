@@ -2,9 +2,21 @@
 // the launch entry points of every kernel in this library.
 #pragma once
 
+#ifdef __CUDACC_RTC__  // NVRTC build of the per-pass specialised kernels (jit.cpp): no host headers
+namespace std {
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long uint64_t;
+typedef int int32_t;
+typedef unsigned long size_t;
+}  // namespace std
+typedef struct CUstream_st* cudaStream_t;
+#else
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#endif
 
 namespace qcs {
 
@@ -51,6 +63,8 @@ enum TileOpKind : std::int32_t {
     TOP_SIGN = 2,    // diag sign step: flipped list (global memory) XOR flip_rest
     TOP_WHT = 3,     // unnormalised butterflies (a+b, a-b) over round bits (wht_mask)
     TOP_SCALE = 4,   // multiply by a real scalar (the RH magnitude, rh.cpp:99-100)
+    TOP_DTAB = 5,    // register round: diagonal given per register, pool[ref + q] (q = 0..7); dskip bit q
+                     // = entry q is exactly 1 (the round's diagonals on its register bits, combined)
 };
 
 struct TileOp {
@@ -78,7 +92,8 @@ struct TileOp {
 };
 
 // RegOp::kind flags above the kind bits
-constexpr int KF_KIND = 0x0f;
+constexpr int KF_KIND = 0x07;
+constexpr int KF_REAL = 0x08;    // TOP_GATE (bundled or not): every coefficient is real (c[k].y == 0)
 // KF_BUNDLE on a +-1 diagonal (KF_SIGNED): a run of them; smask low byte = the flips of the ones
 // with no group-constant bit, pool[ref .. ref + t) = SignEntry for the others
 struct SignEntry {
@@ -145,6 +160,23 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
 };
 // the kernel's parameters: PassParams, four pointers and a 128-byte tensor map in 32764 bytes
 static_assert(sizeof(PassParams) + 4 * 8 + 128 + 64 <= 32764, "kernel parameter space");
+
+// The pass's TMA tensor map (a CUtensorMap, cuda.h) as opaque kernel-parameter bytes
+struct alignas(64) TmapParam {
+    unsigned long long w[16];
+};
+
+#ifndef __CUDACC_RTC__
+// The pass as a kernel specialised to its operation list (jit.cpp); false when the pass is not
+// worth a compile (or QCS_JIT=0), and the interpreter k_tile runs it.
+bool launch_tile_pass_jit(double2* amps, const struct PassParams& p, unsigned F, const struct TileOp* big_dev,
+                          const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, const TmapParam& tmap,
+                          unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st);
+int jit_mode();                      // 0 off, 1 passes with enough work (default), 2 every tile pass
+std::size_t jit_compile_only(const struct PassParams& p);  // NVRTC only (no device): cubin bytes
+void tile_pass_shape(const struct PassParams& p, unsigned& F, unsigned& threads);  // kernel variant, CTA size
+unsigned long long jit_compiles();   // pass kernels compiled so far
+#endif
 
 // tables_dev: the plan's u64 tables (Lowered::tables): run offsets and tile lists
 // sets p.tma_* for the launch

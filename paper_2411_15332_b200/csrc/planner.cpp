@@ -7,6 +7,7 @@
 // supports, or both diagonal.  A pass keeps basis bits 0..2 in its tile for coalescing.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.hpp"
@@ -15,6 +16,13 @@
 namespace qcs {
 
 namespace {
+// planner A/B switches for measurements (host side, read once)
+bool knob(const char* name) {
+    const char* v = std::getenv(name);
+    return v && *v && *v != '0';
+}
+const bool kNoTables = knob("QCS_NO_DTAB");
+const bool kNoReal = knob("QCS_NO_REAL");
 inline bool is_zero(const cplx& v) { return v.real() == 0.0 && v.imag() == 0.0; }
 inline bool is_one(const cplx& v) { return v.real() == 1.0 && v.imag() == 0.0; }
 }  // namespace
@@ -186,6 +194,64 @@ void merge_single_qubit(int n, std::vector<FOp>& ops) {
     ops.clear();
     for (FOp& f : out)
         if (f.kind >= 0) ops.push_back(std::move(f));
+}
+
+// Phase splitting for fused passes: a one-qubit gate whose rows each carry one common phase is
+// D_L * R with R real, one whose columns do is R * D_R.  The real factor costs half the FP64
+// instructions of a complex 2x2 and the diagonal joins its round's diagonal table (lower_plan):
+// C4's merged RZ * RY, Y = diag(-i, i) * X.  The factors reproduce the gate to ~1e-16; fused
+// passes are held to 1e-12.
+void split_phases(std::vector<FOp>& ops) {
+    if (knob("QCS_NO_SPLIT")) return;
+    std::vector<FOp> out;
+    out.reserve(ops.size());
+    auto one_qubit = [](int bit, const cplx (&m)[4], FOp& f) {
+        GateOp g;
+        g.k = 1;
+        g.pos[0] = bit;
+        g.m.assign(m, m + 4);
+        return make_fop(g, f);
+    };
+    for (FOp& f : ops) {
+        bool split = false;
+        if (f.kind == TOP_GATE && f.src.k == 1 && f.K == 1 && f.ctrl_mask == 0) {
+            const cplx* m = f.src.m.data();
+            bool real = true;
+            for (int i = 0; i < 4; ++i) real &= m[i].imag() == 0.0;
+            // factor by rows (by_rows) or columns: entry (r, c) = d[line] * R(r, c), R real
+            for (int by_rows = 1; !real && !split && by_rows >= 0; --by_rows) {
+                cplx d[2];
+                cplx R[4];
+                bool ok = true;
+                for (int l = 0; l < 2 && ok; ++l) {
+                    const int i0 = by_rows ? 2 * l : l, i1 = by_rows ? 2 * l + 1 : l + 2;
+                    const cplx big = std::abs(m[i0]) >= std::abs(m[i1]) ? m[i0] : m[i1];
+                    if (std::abs(big) == 0.0) { ok = false; break; }
+                    d[l] = big / std::abs(big);
+                    for (int i : {i0, i1}) {
+                        const cplx x = m[i] * std::conj(d[l]);
+                        if (std::fabs(x.imag()) > 1e-15) ok = false;
+                        R[i] = cplx(x.real(), 0.0);
+                    }
+                }
+                if (!ok) continue;
+                const cplx D[4] = {d[0], cplx(0.0, 0.0), cplx(0.0, 0.0), d[1]};
+                cplx Rm[4] = {R[0], R[1], R[2], R[3]};
+                FOp fr, fd;
+                const bool has_r = one_qubit(f.tpos[0], Rm, fr), has_d = one_qubit(f.tpos[0], D, fd);
+                if (by_rows) {  // D_L * R: R first
+                    if (has_r) out.push_back(std::move(fr));
+                    if (has_d) out.push_back(std::move(fd));
+                } else {
+                    if (has_d) out.push_back(std::move(fd));
+                    if (has_r) out.push_back(std::move(fr));
+                }
+                split = true;
+            }
+        }
+        if (!split) out.push_back(std::move(f));
+    }
+    ops.swap(out);
 }
 
 Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
@@ -395,8 +461,36 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 return -1;
             };
             rd.op_begin = std::uint16_t(nops);
+            // diagonals on the round's register bits that commute to the end of the round (no
+            // later operation targets their bits) combine into one table of 8 entries (TOP_DTAB)
+            std::vector<int> seq, tab;
+            if (!r.smem) {
+                for (std::size_t i = 0; i < r.ops.size(); ++i) {
+                    const FOp& f = src[std::size_t(r.ops[i])];
+                    bool movable = !kNoTables && f.kind == TOP_DIAG && npool + 8 <= kPassPool - 12;
+                    for (int j = 0; movable && j < f.dk; ++j) movable = loc[f.dpos[j]] >= 0 && reg(f.dpos[j]) >= 0;
+                    if (movable) {  // +-1 diagonals stay pending sign flips (cheaper)
+                        bool signed_only = true;
+                        for (int g = 0; g < (1 << f.dk); ++g) {
+                            const double2 d = f.dval[g];
+                            if (d.y != 0.0 || (d.x != 1.0 && d.x != -1.0)) signed_only = false;
+                        }
+                        movable = !signed_only;
+                    }
+                    for (std::size_t j = i + 1; movable && j < r.ops.size(); ++j) {
+                        const FOp& g = src[std::size_t(r.ops[j])];
+                        if (g.kind != TOP_GATE && g.kind != TOP_WHT) continue;
+                        u64 tg = 0;
+                        for (int k = 0; k < g.K; ++k) tg |= u64(1) << g.tpos[k];
+                        if (tg & f.touch) movable = false;
+                    }
+                    (movable ? tab : seq).push_back(r.ops[i]);
+                }
+            } else {
+                seq = r.ops;
+            }
             bool pending_signs = false;  // a +-1 diagonal since the last butterfly / gate
-            for (int idx : r.ops) {
+            for (int idx : seq) {
                 const FOp& f = src[std::size_t(idx)];
                 if (nops >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many operations in a pass");
                 RegOp o{};
@@ -440,6 +534,8 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                                 o.c[2 * rm] = o.c[2 * rm + 1] = make_double2(0.0, 0.0);
                                 for (int z = 0; z < f.nnz[row]; ++z) o.c[2 * rm + f.col_member[row][z]] = f.val[row][z];
                             }
+                            if (!kNoReal && o.c[0].y == 0.0 && o.c[1].y == 0.0 && o.c[2].y == 0.0 && o.c[3].y == 0.0)
+                                o.kind = std::uint8_t(o.kind | KF_REAL);
                         }
                         break;
                     case TOP_WHT: {  // a run of single-bit butterflies becomes one masked op
@@ -555,10 +651,11 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 }
                 // consecutive uncontrolled one-qubit gates on different register bits: one
                 // bundled operation (one dispatch per group instead of up to three)
-                if (f.kind == TOP_GATE && !(rd.flags & RD_SMEM) && o.kind == TOP_GATE && !o.lctrl_mask &&
+                if (f.kind == TOP_GATE && !(rd.flags & RD_SMEM) && (o.kind & ~KF_REAL) == TOP_GATE && !o.lctrl_mask &&
                     nops > rd.op_begin) {
                     RegOp& prev = P.ops[nops - 1];
-                    const bool prev_gate = (prev.kind & ~(KF_BUNDLE | KF_FLUSH)) == TOP_GATE && !prev.lctrl_mask;
+                    const bool prev_gate = (prev.kind & ~(KF_BUNDLE | KF_FLUSH | KF_REAL)) == TOP_GATE &&
+                                           !prev.lctrl_mask && (prev.kind & KF_REAL) == (o.kind & KF_REAL);
                     const unsigned pmask = (prev.kind & KF_BUNDLE) ? prev.t : (1u << prev.t);
                     if (prev_gate && !(pmask & (1u << o.t)) && ((prev.kind & KF_BUNDLE) || npool + 12 <= kPassPool)) {
                         if (!(prev.kind & KF_BUNDLE)) {
@@ -573,6 +670,25 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                         continue;
                     }
                 }
+                P.ops[nops++] = o;
+            }
+            if (!tab.empty()) {
+                if (nops >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many operations in a pass");
+                RegOp o{};
+                o.kind = TOP_DTAB;
+                o.ref = std::uint16_t(npool);
+                for (int q = 0; q < 8; ++q) {
+                    cplx t(1.0, 0.0);
+                    for (int idx : tab) {
+                        const FOp& f = src[std::size_t(idx)];
+                        int g = 0;
+                        for (int i = 0; i < f.dk; ++i) g |= ((q >> reg(f.dpos[i])) & 1) << (f.dk - 1 - i);
+                        if (!f.dskip[g]) t *= cplx(f.dval[g].x, f.dval[g].y);
+                    }
+                    P.pool[npool + q] = make_double2(t.real(), t.imag());
+                    if (t == cplx(1.0, 0.0)) o.dskip = std::uint8_t(o.dskip | (1u << q));
+                }
+                npool += 8;
                 P.ops[nops++] = o;
             }
             rd.op_count = std::uint16_t(nops - rd.op_begin);
@@ -643,6 +759,30 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
         out.pass_ops.push_back(lists[pi]);
         out.single_flip_off.push_back(flip_off);
         out.single_flip_cnt.push_back(flip_cnt);
+    }
+}
+
+void dump_pass(std::FILE* f, const PassParams& p, std::size_t nsrc) {
+    std::fprintf(f, "pass m=%d src_ops=%zu rounds=%d ops=%d alt=%d list=%u bits=", p.m, nsrc, p.nrounds, p.nops,
+                 int(p.alt_mode), p.list_cnt);
+    for (int b = 0; b < p.m; ++b) std::fprintf(f, "%d%s", p.bits[b], b + 1 < p.m ? "," : "\n");
+    if (nsrc == 1) return;
+    const int nr = p.alt_mode == ALT_ROUNDS ? p.alt_begin + p.alt_nrounds : p.nrounds;
+    for (int r = 0; r < nr; ++r) {
+        const RoundDesc& R = p.rounds[r];
+        std::fprintf(f, "  round%s%s regs=%d,%d,%d:", (R.flags & RD_SMEM) ? " smem" : "", r >= p.nrounds ? " alt" : "",
+                     R.r[0], R.r[1], R.r[2]);
+        for (int i = R.op_begin; i < R.op_begin + R.op_count; ++i) {
+            const RegOp& o = p.ops[i];
+            static const char* names[] = {"G", "D", "SIGN", "WHT", "SC", "DTAB"};
+            const int k = o.kind & KF_KIND;
+            std::fprintf(f, " %s%s%s%s%s%s", k <= 5 ? names[k] : "?", (o.kind & KF_BUNDLE) ? "b" : "",
+                         (o.kind & KF_SIGNED) ? "s" : "", (o.kind & KF_GCTRL) ? "g" : "", (o.kind & KF_FLUSH) ? "f" : "", (o.kind & KF_REAL) ? "r" : "");
+            if (k == TOP_GATE || k == TOP_WHT) std::fprintf(f, "[t%d%s]", o.t, o.lctrl_mask ? " c" : "");
+            if (k == TOP_DIAG) std::fprintf(f, "[dk%d r%d,%d]", o.dk, o.dreg[0] == 0xff ? -1 : o.dreg[0],
+                                            o.dk > 1 ? (o.dreg[1] == 0xff ? -1 : o.dreg[1]) : -2);
+        }
+        std::fprintf(f, "\n");
     }
 }
 

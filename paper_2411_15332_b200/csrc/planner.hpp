@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <vector>
 
 #include "common.hpp"
@@ -53,6 +54,7 @@ struct Plan {
 };
 Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits);
 void merge_single_qubit(int n, std::vector<FOp>& ops);
+void split_phases(std::vector<FOp>& ops);
 
 struct Lowered {
     std::vector<PassParams> passes;
@@ -63,5 +65,7 @@ struct Lowered {
     std::vector<u64> single_flip_off, single_flip_cnt;  // sign step of a single-op pass
 };
 void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& out);
+// one line per round and operation (planner debugging, QCS_PLAN_DUMP)
+void dump_pass(std::FILE* f, const PassParams& p, std::size_t nsrc);
 
 }  // namespace qcs

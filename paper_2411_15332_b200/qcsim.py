@@ -603,6 +603,17 @@ def plan_stats(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOpt
     return {f: int(getattr(info, f)) for f, _ in L.qcs_plan_info._fields_}
 
 
+def plan_compile(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOptions] = None) -> dict:
+    """Generate and compile (NVRTC, host only) the specialised kernel of every tile pass of the
+    plan of `c`.  B200-specific check/tool: {"kernels": passes compiled, "cubin_bytes": code size}."""
+    opts = opts or SimOptions()
+    arr, keep = _steps(c.steps)
+    o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)))
+    k, b = C.c_int64(), C.c_int64()
+    _check(L.lib().qcs_plan_compile(c.n, arr, len(c.steps), int(engine), C.byref(o), C.byref(k), C.byref(b)))
+    return {"kernels": int(k.value), "cubin_bytes": int(b.value)}
+
+
 # ---------------------------------------------------------------- compressed structures
 @dataclass
 class DaxMatrix:  # dax.hpp:22-28

@@ -16,13 +16,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--which", default="c1,c3,c4")
 ap.add_argument("--n3", type=int, default=30)
 ap.add_argument("--n4", type=int, default=32)
+ap.add_argument("--n5", type=int, default=32)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--fuse", type=int, default=1)
 a = ap.parse_args()
 
 jobs = {"c1": (lambda: configs.c1_circuit(), configs.c1_updates()),
         "c3": (lambda: configs.c3_circuit(a.n3), configs.c3_updates(a.n3)),
-        "c4": (lambda: configs.c4_circuit(a.n4), configs.c4_updates(a.n4))}
+        "c4": (lambda: configs.c4_circuit(a.n4), configs.c4_updates(a.n4)),
+        "c5": (lambda: configs.c5_circuit(a.n5), configs.c5_updates(a.n5))}
 for key in a.which.split(","):
     build, updates = jobs[key]
     c = build()
