@@ -212,6 +212,11 @@ int qcs_plan_stats(int n, const qcs_step* steps, int num_steps, int engine, cons
 /* Generate and compile (NVRTC, host only) the specialised kernel of every tile pass of that
  * plan -- the kernels qcs_simulate runs for passes with enough work (QCS_JIT=force: all).
  * *kernels = passes compiled, *cubin_bytes = total code size.  B200-specific check/tool. */
+/* Which tile passes run as specialised kernels: 0 none (the interpreter kernel runs every
+ * pass), 1 passes with enough work (default), 2 all.  Initial value from QCS_JIT (0/1/force).
+ * Both forms compute bit-identical results; process-wide. */
+int qcs_set_jit_mode(int mode);
+int qcs_get_jit_mode(void);
 int qcs_plan_compile(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
                      int64_t* kernels, int64_t* cubin_bytes);
 

@@ -90,6 +90,8 @@ SIGNATURES = {
     "qcs_apply_split": (C.c_int, [_P, _P, C.c_int, C.c_int, _I, _D, C.c_uint32]),
     "qcs_plan_stats": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
                                  C.POINTER(qcs_plan_info)]),
+    "qcs_set_jit_mode": (C.c_int, [C.c_int]),
+    "qcs_get_jit_mode": (C.c_int, []),
     "qcs_plan_compile": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "qcs_step_dax": (C.c_int, [C.c_int, C.POINTER(qcs_placement), C.c_int, C.c_int, _P, _P, _P, C.c_uint64,

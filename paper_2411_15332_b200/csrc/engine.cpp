@@ -273,6 +273,7 @@ void run_fused(qcs_state* s, const std::vector<FOp>& ops) {
     Lowered low;
     if (n >= 3) {
         lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
+        jit_prepare(n, low.passes, low.pass_ops);
     } else {  // no 3-bit tile: one operation per pass
         for (std::size_t i = 0; i < ops.size(); ++i) {
             low.pass_ops.push_back({int(i)});

@@ -14,7 +14,9 @@
 #include <cuda.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -24,6 +26,7 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.hpp"
@@ -74,7 +77,8 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
         off[q] = ((q & 1) ? 1u << R.r[0] : 0u) | ((q & 2) ? 1u << R.r[1] : 0u) | ((q & 4) ? 1u << R.r[2] : 0u);
     auto swz = [](unsigned j) { return j ^ ((j >> 3) & 7u); };
     o("  {  // round %d: register bits %d %d %d\n", ri, R.r[0], R.r[1], R.r[2]);
-    o("#pragma unroll 1\n");
+    static const int unroll = [] { const char* v = std::getenv("QCS_JIT_UNROLL"); return v ? std::atoi(v) : 1; }();
+    o("#pragma unroll %d\n", unroll);
     o("    for (unsigned gb = t; gb < %uu; gb += %uu) {\n", ngroups, threads);
     o("      const unsigned lb = insert_zero(insert_zero(insert_zero(gb, %d), %d), %d);\n", R.r[0], R.r[1], R.r[2]);
     o("      const unsigned slb = swz(lb);\n");
@@ -181,7 +185,8 @@ void emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threa
 
 std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
     Out o;
-    const int minb = (F & 8u) ? 2 : 3;
+    static const int minb_env = [] { const char* v = std::getenv("QCS_JIT_MINB"); return v ? std::atoi(v) : 0; }();
+    const int minb = minb_env > 0 ? minb_env : (F & 8u) ? 2 : 3;  // resident tiles per SM
     o("#include \"tile_device.cuh\"\n");
     o("using namespace qcs;\nusing namespace qcs::tile;\n");
     o("extern \"C\" __global__ void __launch_bounds__(%u, %d)\n", threads, minb);
@@ -243,11 +248,8 @@ std::vector<char> compile_cubin(const std::string& src) {
     return cubin;
 }
 
-JitKernel& compile(const std::string& src) {
+JitKernel& load(const std::string& src, const std::vector<char>& cubin) {
     // callers hold g_mu
-    auto it = g_cache.find(src);
-    if (it != g_cache.end()) return *it->second;
-    const std::vector<char> cubin = compile_cubin(src);
     const std::size_t n = cubin.size();
     auto k = std::make_unique<JitKernel>();
     QCS_CUDA(cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
@@ -259,19 +261,82 @@ JitKernel& compile(const std::string& src) {
     return ref;
 }
 
+JitKernel& compile(const std::string& src) {
+    // callers hold g_mu
+    auto it = g_cache.find(src);
+    if (it != g_cache.end()) return *it->second;
+    return load(src, compile_cubin(src));
+}
+
+// worth a compile (~0.5 s, once per structure): enough tiles x rounds of work
+bool wanted(const PassParams& p, double tiles) {
+    const int mode = jit_mode();
+    if (mode == 0) return false;
+    return mode == 2 || (tiles * double(p.nrounds) >= 32768.0 && p.nrounds >= 2);
+}
+
 }  // namespace
 
-int jit_mode() {
-    static const int mode = [] {
-        const char* v = std::getenv("QCS_JIT");
-        if (!v || !*v) return 1;                       // default: passes with enough work
-        if (!std::strcmp(v, "force")) return 2;        // every tile pass (tests)
-        return std::atoi(v) != 0 ? 1 : 0;
-    }();
-    return mode;
+namespace {
+std::atomic<int> g_mode{[] {
+    const char* v = std::getenv("QCS_JIT");
+    if (!v || !*v) return 1;                 // default: passes with enough work
+    if (!std::strcmp(v, "force")) return 2;  // every tile pass
+    return std::atoi(v) != 0 ? 1 : 0;
+}()};
+}  // namespace
+
+int jit_mode() { return g_mode.load(std::memory_order_relaxed); }
+void set_jit_mode(int mode) {
+    if (mode < 0 || mode > 2) raise(QCS_ERR_ARG, "jit mode must be 0, 1 or 2");
+    g_mode.store(mode);
 }
 
 unsigned long long jit_compiles() { return g_compiles.load(); }
+
+void jit_prepare(int n, const std::vector<PassParams>& passes, const std::vector<std::vector<int>>& pass_ops) {
+    std::vector<std::string> todo;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        std::set<std::string> seen;
+        for (std::size_t i = 0; i < passes.size(); ++i) {
+            const PassParams& p = passes[i];
+            if (pass_ops[i].size() < 2 || p.m < 3 || p.m > n) continue;
+            const double tiles = p.list_cnt ? double(p.list_cnt) : std::ldexp(1.0, n - p.m);
+            if (!wanted(p, tiles)) continue;
+            unsigned F = 0, threads = 0;
+            tile_pass_shape(p, F, threads);
+            std::string src = pass_source(p, F, threads);
+            if (g_cache.count(src) || !seen.insert(src).second) continue;
+            todo.push_back(std::move(src));
+        }
+    }
+    if (todo.size() < 2) return;  // a single kernel compiles at its launch
+    // NVRTC programs compile concurrently; modules load afterwards under the cache lock
+    std::vector<std::vector<char>> cubins(todo.size());
+    std::vector<std::string> errors(todo.size());
+    std::atomic<std::size_t> next{0};
+    auto worker = [&] {
+        for (std::size_t i; (i = next.fetch_add(1)) < todo.size();) {
+            try {
+                cubins[i] = compile_cubin(todo[i]);
+            } catch (const std::exception& e) {
+                errors[i] = e.what();
+            }
+        }
+    };
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const std::size_t nthreads = std::min<std::size_t>(todo.size(), std::min(hw, 32u));
+    std::vector<std::thread> pool;
+    for (std::size_t i = 1; i < nthreads; ++i) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    for (const auto& e : errors)
+        if (!e.empty()) raise(QCS_ERR_SIM, e);
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (std::size_t i = 0; i < todo.size(); ++i)
+        if (!g_cache.count(todo[i])) load(todo[i], cubins[i]);
+}
 
 std::size_t jit_compile_only(const PassParams& p) {
     unsigned F = 0, threads = 0;
@@ -282,10 +347,7 @@ std::size_t jit_compile_only(const PassParams& p) {
 bool launch_tile_pass_jit(double2* amps, const PassParams& p, unsigned F, const TileOp* big_dev,
                           const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, const TmapParam& tmap,
                           unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st) {
-    const int mode = jit_mode();
-    if (mode == 0) return false;
-    // worth a compile (~0.5 s, once per structure): enough tiles x rounds of work
-    if (mode == 1 && (double(tiles) * double(p.nrounds) < 32768.0 || p.nrounds < 2)) return false;
+    if (!wanted(p, double(tiles))) return false;
     const std::string src = pass_source(p, F, threads);
     int dev = 0;
     QCS_CUDA(cudaGetDevice(&dev));

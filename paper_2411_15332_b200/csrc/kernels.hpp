@@ -173,6 +173,7 @@ bool launch_tile_pass_jit(double2* amps, const struct PassParams& p, unsigned F,
                           const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, const TmapParam& tmap,
                           unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st);
 int jit_mode();                      // 0 off, 1 passes with enough work (default), 2 every tile pass
+void set_jit_mode(int mode);
 std::size_t jit_compile_only(const struct PassParams& p);  // NVRTC only (no device): cubin bytes
 void tile_pass_shape(const struct PassParams& p, unsigned& F, unsigned& threads);  // kernel variant, CTA size
 unsigned long long jit_compiles();   // pass kernels compiled so far

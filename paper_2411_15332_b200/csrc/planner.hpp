@@ -65,6 +65,8 @@ struct Lowered {
     std::vector<u64> single_flip_off, single_flip_cnt;  // sign step of a single-op pass
 };
 void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& out);
+// compile (in parallel, NVRTC) the specialised kernels of the plan's passes that will use one (jit.cpp)
+void jit_prepare(int n, const std::vector<PassParams>& passes, const std::vector<std::vector<int>>& pass_ops);
 // one line per round and operation (planner debugging, QCS_PLAN_DUMP)
 void dump_pass(std::FILE* f, const PassParams& p, std::size_t nsrc);
 

@@ -603,6 +603,17 @@ def plan_stats(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOpt
     return {f: int(getattr(info, f)) for f, _ in L.qcs_plan_info._fields_}
 
 
+def set_jit_mode(mode: int) -> None:
+    """0: every fused pass runs on the interpreter kernel; 1 (default): passes with enough work
+    run as kernels specialised to their operation list (compiled once per structure, NVRTC);
+    2: all.  Results are bit-identical.  B200-specific."""
+    _check(L.lib().qcs_set_jit_mode(int(mode)))
+
+
+def jit_mode() -> int:
+    return int(L.lib().qcs_get_jit_mode())
+
+
 def plan_compile(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOptions] = None) -> dict:
     """Generate and compile (NVRTC, host only) the specialised kernel of every tile pass of the
     plan of `c`.  B200-specific check/tool: {"kernels": passes compiled, "cubin_bytes": code size}."""
