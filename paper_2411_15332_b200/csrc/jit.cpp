@@ -52,6 +52,17 @@ struct Out {
     }
 };
 
+
+int knob_unroll() {
+    static const int u = [] { const char* v = std::getenv("QCS_JIT_UNROLL"); return v ? std::atoi(v) : 1; }();
+    return u;
+}
+
+bool knob_bankswap() {
+    static const bool on = [] { const char* v = std::getenv("QCS_JIT_BANKSWAP"); return !v || std::atoi(v) != 0; }();
+    return on;
+}
+
 // the cg (value of the group-constant phase bits) expression of a +-1 diagonal, as source
 std::string const_bits(bool c0, bool c1, int dk, int p0, int p1) {
     std::string e = "0";
@@ -68,25 +79,61 @@ std::string const_bits(bool c0, bool c1, int dk, int p0, int p1) {
 }
 
 // One register round: the interpreter's round loop (tile_kernels.cu) with every structural
-// field of the operations as a literal.
+// field of the operations as a literal.  (16-amplitude rounds -- 4 register bits, 22% fewer
+// rounds for C4 -- were measured no faster at 2 resident tiles per SM and slower for C3.)
 void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) {
     const RoundDesc& R = P.rounds[ri];
-    const unsigned ngroups = (1u << P.m) >> 3;
-    unsigned off[8];
-    for (int q = 0; q < 8; ++q)
-        off[q] = ((q & 1) ? 1u << R.r[0] : 0u) | ((q & 2) ? 1u << R.r[1] : 0u) | ((q & 4) ? 1u << R.r[2] : 0u);
+    constexpr int W = 3, G = 1 << W;
+    const unsigned long long gmask = (1ull << G) - 1;
+    const unsigned ngroups = (1u << P.m) >> W;
+    unsigned off[16] = {};
+    unsigned regmask = 0;
+    for (int i = 0; i < W; ++i) regmask |= 1u << R.r[i];
+    for (int q = 0; q < G; ++q)
+        for (int i = 0; i < W; ++i)
+            if (q >> i & 1) off[q] |= 1u << R.r[i];
     auto swz = [](unsigned j) { return j ^ ((j >> 3) & 7u); };
-    o("  {  // round %d: register bits %d %d %d\n", ri, R.r[0], R.r[1], R.r[2]);
-    static const int unroll = [] { const char* v = std::getenv("QCS_JIT_UNROLL"); return v ? std::atoi(v) : 1; }();
-    o("#pragma unroll %d\n", unroll);
+    o("  {  // round %d: register bits", ri);
+    for (int i = 0; i < W; ++i) o(" %d", R.r[i]);
+    o("\n#pragma unroll %d\n", knob_unroll());
     o("    for (unsigned gb = t; gb < %uu; gb += %uu) {\n", ngroups, threads);
-    o("      const unsigned lb = insert_zero(insert_zero(insert_zero(gb, %d), %d), %d);\n", R.r[0], R.r[1], R.r[2]);
+    // Thread order: the 8 threads of one 16-byte shared-memory phase differ in gb's low 3 bits,
+    // i.e. in the round's lowest 3 non-register tile bits.  Their bank group is bits 0..2 XOR
+    // bits 3..5 of the (swizzled) position; when those three bits do not map to 8 distinct
+    // groups, swap one of them with a higher non-register bit that does (same groups, another
+    // thread order: the accesses become conflict-free).
+    auto bank = [](int b) { return (b < 3 ? 1u << b : 0u) ^ (b >= 3 && b < 6 ? 1u << (b - 3) : 0u); };
+    auto independent = [&](int a, int b, int c) {
+        const unsigned x = bank(a), y = bank(b), z = bank(c);
+        return x && y && z && x != y && x != z && y != z && (x ^ y) != z;
+    };
+    std::vector<int> nonreg;
+    for (int b = 0; b < P.m; ++b)
+        if (!(regmask >> b & 1)) nonreg.push_back(b);
+    int swap_a = -1, swap_b = -1;
+    if (knob_bankswap() && nonreg.size() >= 4 && !independent(nonreg[0], nonreg[1], nonreg[2])) {
+        for (int i = 0; i < 3 && swap_a < 0; ++i)
+            for (std::size_t j = 3; j < nonreg.size() && swap_a < 0; ++j) {
+                int c[3] = {nonreg[0], nonreg[1], nonreg[2]};
+                c[i] = nonreg[j];
+                if (independent(c[0], c[1], c[2])) {
+                    swap_a = nonreg[std::size_t(i)];
+                    swap_b = nonreg[j];
+                }
+            }
+    }
+    std::string lbx = "gb";
+    for (int i = 0; i < W; ++i) lbx = "insert_zero(" + lbx + ", " + std::to_string(R.r[i]) + ")";
+    o("      %sunsigned lb = %s;\n", swap_a < 0 ? "const " : "", lbx.c_str());
+    if (swap_a >= 0)
+        o("      { const unsigned d = ((lb >> %d) ^ (lb >> %d)) & 1u; lb ^= (d << %d) | (d << %d); }\n", swap_a, swap_b,
+          swap_a, swap_b);
     o("      const unsigned slb = swz(lb);\n");
-    o("      double2 v[8];\n");
-    for (int q = 0; q < 8; ++q) o("      v[%d] = sm[slb ^ %uu];\n", q, swz(off[q]));
+    o("      double2 v[%d];\n", G);
+    for (int q = 0; q < G; ++q) o("      v[%d] = sm[slb ^ %uu];\n", q, swz(off[q]));
     o("      const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];\n");
     o("      unsigned negacc = 0;\n");
-    o("      (void)g0;\n");
+    o("      (void)g0; (void)negacc;\n");
     for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
         const RegOp& op = P.ops[oi];
         const int kb = op.kind, kind = kb & KF_KIND;
@@ -95,48 +142,49 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
         if (gc) o("      if ((base & 0x%llxull) == 0x%llxull) {\n", (unsigned long long)op.gctrl_mask,
                   (unsigned long long)op.gctrl_val);
         if ((kb & KF_SIGNED) && (kb & KF_BUNDLE)) {
-            o("      { unsigned acc = 0x%xu;\n", op.smask & 0xffu);
+            o("      { unsigned acc = 0x%llxu;\n", (unsigned long long)(op.smask & gmask));
             for (int i = 0; i < op.t; ++i) {
                 SignEntry e;
                 std::memcpy(&e, &P.pool[op.ref + i], sizeof(e));
-                o("        acc ^= (0x%xu >> (8 * (%s))) & 0xffu;\n", e.smask,
-                  const_bits(e.cmask & 1u, e.cmask & 2u, e.dk, e.p0, e.p1).c_str());
+                o("        acc ^= unsigned(0x%llxull >> (%d * (%s))) & 0x%llxu;\n", (unsigned long long)e.smask, G,
+                  const_bits(e.cmask & 1u, e.cmask & 2u, e.dk, e.p0, e.p1).c_str(), gmask);
             }
             o("        negacc ^= acc; }\n");
         } else if (kb & KF_SIGNED) {
             const bool c0 = op.dreg[0] == 0xff, c1 = op.dk == 2 && op.dreg[1] == 0xff;
-            o("      negacc ^= (0x%xu >> (8 * (%s))) & 0xffu;\n", op.smask,
-              const_bits(c0, c1, op.dk, op.dpos[0], op.dpos[1]).c_str());
+            o("      negacc ^= unsigned(0x%llxull >> (%d * (%s))) & 0x%llxu;\n", (unsigned long long)op.smask, G,
+              const_bits(c0, c1, op.dk, op.dpos[0], op.dpos[1]).c_str(), gmask);
         } else if (kind == TOP_WHT) {
-            for (int b = 0; b < 3; ++b)
+            for (int b = 0; b < W; ++b)
                 if (op.t >> b & 1) o("      butterfly<%d>(v);\n", b);
         } else if (kind == TOP_SCALE) {
             o("      { const double sc = P.ops[%d].c[0].x;\n", oi);
-            o("        for (int q = 0; q < 8; ++q) v[q] = make_double2(v[q].x * sc, v[q].y * sc); }\n");
+            o("        for (int q = 0; q < %d; ++q) v[q] = make_double2(v[q].x * sc, v[q].y * sc); }\n", G);
         } else if (kind == TOP_GATE && (kb & KF_BUNDLE)) {
-            for (int b = 0; b < 3; ++b)
+            for (int b = 0; b < W; ++b)
                 if (op.t >> b & 1)
-                    o("      %s<%d, false>(v, P.pool + %d, 0xffu);\n", (kb & KF_REAL) ? "gate1r" : "gate1", b,
+                    o("      %s<%d, false>(v, P.pool + %d, 0xffffu);\n", (kb & KF_REAL) ? "gate1r" : "gate1", b,
                       op.ref + 4 * b);
         } else if (kind == TOP_GATE) {
             const char* g = (kb & KF_REAL) ? "gate1r" : "gate1";
             if (op.lctrl_mask) {
                 o("      { unsigned en = 0;\n");
-                for (int q = 0; q < 8; ++q)
-                    o("        en |= unsigned(((lb | %uu) & %uu) == %uu) << %d;\n", off[q], op.lctrl_mask, op.lctrl_val, q);
+                for (int q = 0; q < G; ++q)
+                    o("        en |= unsigned(((lb | %uu) & %uu) == %uu) << %d;\n", off[q], unsigned(op.lctrl_mask),
+                      unsigned(op.lctrl_val), q);
                 o("        %s<%d, true>(v, P.ops[%d].c, en); }\n", g, op.t, oi);
             } else {
-                o("      %s<%d, false>(v, P.ops[%d].c, 0xffu);\n", g, op.t, oi);
+                o("      %s<%d, false>(v, P.ops[%d].c, 0xffffu);\n", g, op.t, oi);
             }
         } else if (kind == TOP_DTAB) {
-            for (int q = 0; q < 8; ++q)
+            for (int q = 0; q < G; ++q)
                 if (!(op.dskip >> q & 1)) o("      v[%d] = cmul_f(P.pool[%d], v[%d]);\n", q, op.ref + q, q);
         } else if (kind == TOP_DIAG) {
             if (op.dk == 1 && op.dreg[0] == 0xff) {
                 o("      { const int g = int((g0 >> %d) & 1);\n", op.dpos[0]);
                 o("        if (!((%uu >> g) & 1u)) { const double2 d = g ? P.ops[%d].c[1] : P.ops[%d].c[0];\n",
                   unsigned(op.dskip), oi, oi);
-                o("          for (int q = 0; q < 8; ++q) v[q] = cmul_f(d, v[q]); } }\n");
+                o("          for (int q = 0; q < %d; ++q) v[q] = cmul_f(d, v[q]); } }\n", G);
             } else if (op.dk == 1) {
                 o("      diag_reg<%d>(v, P.ops[%d].c[0], P.ops[%d].c[1], %uu);\n", op.dreg[0], oi, oi, unsigned(op.dskip));
             } else {
@@ -144,11 +192,11 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
             }
         } else if (kind == TOP_SIGN) {
             o("      { const TileOp& so = big[%d];\n", op.ref);
-            o("        if (!(sign_hit >> %u & 1u)) {\n", op.sidx & 31u);
-            o("          if (so.flip_rest) { for (int q = 0; q < 8; ++q) v[q] = neg_exact(v[q]); }\n");
+            o("        if (!(sign_hit >> %u & 1u)) {\n", unsigned(op.sidx) & 31u);
+            o("          if (so.flip_rest) { for (int q = 0; q < %d; ++q) v[q] = neg_exact(v[q]); }\n", G);
             o("        } else {\n");
             o("          const u64* f = flipped + so.flip_off;\n");
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < G; ++q) {
                 o("          { const unsigned j = lb | %uu; const u64 gi = base | (j & 7u) | hi_tab[j >> 3];\n", off[q]);
                 o("            if (listed(f, so.flip_cnt, gi) != (so.flip_rest != 0)) v[%d] = neg_exact(v[%d]); }\n", q, q);
             }
@@ -159,7 +207,7 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
         if (gc) o("      }\n");
     }
     if (R.flags & RD_SIGNS) o("      flip_signs1(v, negacc);\n");
-    for (int q = 0; q < 8; ++q) o("      sm[slb ^ %uu] = v[%d];\n", swz(off[q]), q);
+    for (int q = 0; q < G; ++q) o("      sm[slb ^ %uu] = v[%d];\n", swz(off[q]), q);
     o("    }\n    __syncthreads();\n  }\n");
 }
 
@@ -226,12 +274,22 @@ std::map<std::string, std::unique_ptr<JitKernel>> g_cache;
 std::atomic<unsigned long long> g_compiles{0};
 
 std::vector<char> compile_cubin(const std::string& src) {
+    if (std::getenv("QCS_JIT_DUMP")) std::fprintf(stderr, "---- qcs_pass\n%s", src.c_str());
     nvrtcProgram prog;
     const char* headers[] = {kJitSrcKernels, kJitSrcDevice};
     const char* names[] = {"kernels.hpp", "tile_device.cuh"};
     nvrtc_check(nvrtcCreateProgram(&prog, src.c_str(), "qcs_pass.cu", 2, headers, names), "nvrtcCreateProgram");
-    const char* opts[] = {"-arch=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo", "-default-device"};
-    const nvrtcResult rc = nvrtcCompileProgram(prog, 5, opts);
+    static const bool verbose = std::getenv("QCS_JIT_VERBOSE") != nullptr;  // ptxas register / spill report
+    const char* opts[] = {"-arch=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo", "-default-device",
+                          "--ptxas-options=-v"};
+    const nvrtcResult rc = nvrtcCompileProgram(prog, verbose ? 6 : 5, opts);
+    if (verbose && rc == NVRTC_SUCCESS) {
+        std::size_t n = 0;
+        nvrtcGetProgramLogSize(prog, &n);
+        std::string log(n, '\0');
+        nvrtcGetProgramLog(prog, log.data());
+        std::fprintf(stderr, "%s", log.c_str());
+    }
     if (rc != NVRTC_SUCCESS) {
         std::size_t n = 0;
         nvrtcGetProgramLogSize(prog, &n);
@@ -255,7 +313,6 @@ JitKernel& load(const std::string& src, const std::vector<char>& cubin) {
     QCS_CUDA(cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     QCS_CUDA(cudaLibraryGetKernel(&k->kernel, k->lib, "qcs_pass"));
     ++g_compiles;
-    if (std::getenv("QCS_JIT_DUMP")) std::fprintf(stderr, "---- qcs_pass (%zu bytes cubin)\n%s", n, src.c_str());
     auto& ref = *k;
     g_cache.emplace(src, std::move(k));
     return ref;
@@ -267,6 +324,7 @@ JitKernel& compile(const std::string& src) {
     if (it != g_cache.end()) return *it->second;
     return load(src, compile_cubin(src));
 }
+
 
 // worth a compile (~0.5 s, once per structure): enough tiles x rounds of work
 bool wanted(const PassParams& p, double tiles) {

@@ -25,7 +25,8 @@ def digest(st):
     """sha256 of the whole state up to 2^24 amplitudes, else of 2^20 strided amplitudes."""
     if st.n <= 24:
         return hashlib.sha256(st.download().tobytes()).hexdigest()[:16]
-    idx = np.arange(0, 1 << st.n, 1 << (st.n - 20), dtype=np.uint64) + np.uint64(12345)
+    stride = 1 << (st.n - 20)
+    idx = np.arange(0, 1 << st.n, stride, dtype=np.uint64) + np.uint64(12345 % stride)
     return hashlib.sha256(st.gather(idx).tobytes()).hexdigest()[:16]
 for arg in sys.argv[1:]:
     key, n = arg.split(":")
