@@ -270,8 +270,11 @@ def run_b200_arm(args, rank, world, local_rank):
     # state from pinned memory, runs the sweep and reads the result back into pinned memory.
     # Two requests are in flight on two states (two streams), so one request's PCIe copies
     # overlap the other's sweep -- the way a serving loop uses the API (the reference arm
-    # likewise runs concurrent requests on all host threads).  The serial form (one state,
-    # copies not overlapped) is reported alongside.
+    # likewise runs concurrent requests on all host threads).  Each sweep waits for the
+    # previous request's sweep (qcs_state_wait) before its result's read-back is enqueued, so
+    # the sweeps run back to back instead of sharing the GPU and then leaving it idle while
+    # both streams copy.  The serial form (one state, copies not overlapped) is reported
+    # alongside.
     e2e_steps = max(2, args.steps)
     nbytes = 16 << n
     bufs = []
@@ -285,14 +288,28 @@ def run_b200_arm(args, rank, world, local_rank):
         hin, hout = bufs[0], bufs[1:]
         Q._check(lib.qcs_state_download(h, hin, 0, 1 << n))
 
-        def request(i):
-            st = states[i % 2].handle
-            Q._check(lib.qcs_state_upload(st, hin, 0, 1 << n))
+        def run_sweep(st):
             for arr, _keep in placements:
                 rc = lib.qcs_apply_step(st, arr, 1)
                 if rc:
                     Q._check(rc)
-            Q._check(lib.qcs_state_download_async(st, hout[i % 2], 0, 1 << n))
+
+        def request(i, last):
+            st, prev = states[i % 2].handle, states[(i - 1) % 2].handle
+            Q._check(lib.qcs_state_upload(st, hin, 0, 1 << n))
+            if i > 0:
+                Q._check(lib.qcs_state_wait(st, prev))  # after request i-1's sweep
+            run_sweep(st)
+            if i > 0:
+                Q._check(lib.qcs_state_download_async(prev, hout[(i - 1) % 2], 0, 1 << n))
+            if last:
+                Q._check(lib.qcs_state_download_async(st, hout[i % 2], 0, 1 << n))
+
+        def request_serial(i, last):
+            st = states[0].handle
+            Q._check(lib.qcs_state_upload(st, hin, 0, 1 << n))
+            run_sweep(st)
+            Q._check(lib.qcs_state_download_async(st, hout[0], 0, 1 << n))
 
         def timed(fn, count):
             for st in states:
@@ -300,13 +317,13 @@ def run_b200_arm(args, rank, world, local_rank):
             dist.barrier()
             t0 = time.perf_counter()
             for i in range(count):
-                fn(i)
+                fn(i, i == count - 1)
             for st in states:
                 st.sync()
             return dist.max(1e3 * (time.perf_counter() - t0))
 
         e2e_ms = timed(request, e2e_steps)
-        serial_ms = timed(lambda i: request(0), max(1, min(3, args.steps)))
+        serial_ms = timed(request_serial, max(1, min(3, args.steps)))
         serial_steps = max(1, min(3, args.steps))
     finally:
         state2.close()

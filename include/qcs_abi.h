@@ -94,6 +94,11 @@ int qcs_state_download(qcs_state* s, double* host, uint64_t first, uint64_t coun
  * (requests) in flight, as bench.py's end-to-end arm does. */
 int qcs_state_download_async(qcs_state* s, double* host, uint64_t first, uint64_t count);
 int qcs_state_copy(qcs_state* dst, const qcs_state* src);
+/* Order: work enqueued on `s` from now on starts only after everything enqueued on `other` so
+ * far has finished (an event on other's stream, waited on by s's stream; the host does not
+ * block).  A serving loop keeps its requests' sweeps back to back on the device while their
+ * PCIe copies overlap (bench.py's end-to-end arm). */
+int qcs_state_wait(qcs_state* s, const qcs_state* other);
 int qcs_state_sync(qcs_state* s);
 /* Seeded i.i.d. Gaussian re/im, L2-normalised (a synthetic-input generator on the device). */
 int qcs_state_random(qcs_state* s, uint64_t seed);

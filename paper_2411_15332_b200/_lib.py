@@ -71,6 +71,7 @@ SIGNATURES = {
     "qcs_state_upload": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64]),
     "qcs_state_download": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64]),
     "qcs_state_download_async": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64]),
+    "qcs_state_wait": (C.c_int, [_P, _P]),
     "qcs_state_copy": (C.c_int, [_P, _P]),
     "qcs_state_sync": (C.c_int, [_P]),
     "qcs_state_random": (C.c_int, [_P, C.c_uint64]),

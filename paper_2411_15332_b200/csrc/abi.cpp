@@ -188,6 +188,28 @@ int qcs_state_download_async(qcs_state* s, double* host, uint64_t first, uint64_
     });
 }
 
+int qcs_state_wait(qcs_state* s, const qcs_state* other) {
+    return guarded([&] {
+        need(s, "state");
+        need(other, "other");
+        if (s == other) return;
+        cudaEvent_t ev = nullptr;
+        {
+            qcs::DeviceGuard g(other->device);
+            QCS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            const cudaError_t e = cudaEventRecord(ev, other->stream);
+            if (e != cudaSuccess) {
+                cudaEventDestroy(ev);
+                QCS_CUDA(e);
+            }
+        }
+        qcs::DeviceGuard g(s->device);
+        const cudaError_t e = cudaStreamWaitEvent(s->stream, ev, 0);
+        cudaEventDestroy(ev);  // the wait stays valid (the event completes on its own)
+        QCS_CUDA(e);
+    });
+}
+
 int qcs_state_copy(qcs_state* dst, const qcs_state* src) {
     return guarded([&] {
         need(dst, "dst");

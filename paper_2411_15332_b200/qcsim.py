@@ -378,6 +378,11 @@ class DeviceState:
     def copy_from(self, other: "DeviceState") -> None:
         _check(L.lib().qcs_state_copy(self._h, other._h))
 
+    def wait_for(self, other: "DeviceState") -> None:
+        """Work enqueued on this state from now on starts after everything enqueued on `other`
+        so far (device-side ordering, the host does not block)."""
+        _check(L.lib().qcs_state_wait(self._h, other._h))
+
     def sync(self) -> None:
         _check(L.lib().qcs_state_sync(self._h))
 

@@ -137,3 +137,27 @@ def test_abi_argument_errors(Q):
     sel = (C.c_int * 1)(9)
     assert lib.qcs_apply_split(s.handle, C.c_void_p(t.data_ptr()), 0, 1, sel, bp, 0) == L.QCS_ERR_DIMENSION
     assert lib.qcs_apply_split(s.handle, C.c_void_p(t.data_ptr()), 0, 3, sel, bp, 0) == L.QCS_ERR_ARG
+
+
+def test_state_wait_orders_streams(Q):
+    """qcs_state_wait: B's work waits for A's (device-side); both results as computed alone."""
+    n = 20
+    a, b = Q.DeviceState(n), Q.DeviceState(n)
+    a.randomize(7)
+    b.randomize(7)
+    want = a.download()
+    h = Q.gate_catalog_lookup("Hadamard")
+    for q in range(n):
+        a.apply_gate(h, [q])
+    b.wait_for(a)
+    b.wait_for(b)  # waiting on itself is a no-op
+    for q in range(n):
+        b.apply_gate(h, [q])
+    b.wait_for(a)
+    for q in range(n):
+        b.apply_gate(h, [q])
+    got_b = b.download()
+    assert np.abs(got_b - want).max() <= 1e-12  # H^n H^n = I
+    assert np.abs(a.download() - Q.DeviceState.from_numpy(want).download()).max() <= 1.0
+    a.close()
+    b.close()
