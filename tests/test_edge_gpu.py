@@ -139,7 +139,7 @@ def test_abi_argument_errors(Q):
     assert lib.qcs_apply_split(s.handle, C.c_void_p(t.data_ptr()), 0, 3, sel, bp, 0) == L.QCS_ERR_ARG
 
 
-def test_state_wait_orders_streams(Q):
+def test_state_wait_orders_streams(Q, oracle):
     """qcs_state_wait: B's work waits for A's (device-side); both results as computed alone."""
     n = 20
     a, b = Q.DeviceState(n), Q.DeviceState(n)
@@ -158,6 +158,6 @@ def test_state_wait_orders_streams(Q):
         b.apply_gate(h, [q])
     got_b = b.download()
     assert np.abs(got_b - want).max() <= 1e-12  # H^n H^n = I
-    assert np.abs(a.download() - Q.DeviceState.from_numpy(want).download()).max() <= 1.0
+    assert np.abs(a.download() - oracle.wht(n, want)).max() <= 1e-12
     a.close()
     b.close()
