@@ -53,6 +53,11 @@ struct Out {
 };
 
 
+bool knob_swaps() {
+    static const bool on = [] { const char* v = std::getenv("QCS_JIT_SWAPS"); return !v || std::atoi(v) != 0; }();
+    return on;
+}
+
 int knob_unroll() {
     static const int u = [] { const char* v = std::getenv("QCS_JIT_UNROLL"); return v ? std::atoi(v) : 1; }();
     return u;
@@ -76,6 +81,25 @@ std::string const_bits(bool c0, bool c1, int dk, int p0, int p1) {
         e += buf;
     }
     return e;
+}
+
+// A one-target gate on register bit t of the registers in `en` (a literal mask): X-like gates
+// (exactly [[0, 1], [1, 0]]) are register swaps -- no arithmetic, value-identical to the
+// interpreter's 0*x0 + 1*x1 up to the sign of an exact zero -- the others the real or complex
+// 2x2 forms of tile_device.cuh.
+void emit_gate(Out& o, int kb, int t, const double2* c, const std::string& coef, unsigned en, int G) {
+    const bool swap = c[0].x == 0.0 && c[0].y == 0.0 && c[3].x == 0.0 && c[3].y == 0.0 && c[1].x == 1.0 &&
+                      c[1].y == 0.0 && c[2].x == 1.0 && c[2].y == 0.0 && knob_swaps();
+    const unsigned all = (1u << G) - 1;
+    if (swap) {
+        for (int q = 0; q < G; ++q)
+            if (!(q >> t & 1) && (en >> q & 1))
+                o("      { const double2 x = v[%d]; v[%d] = v[%d]; v[%d] = x; }\n", q, q, q | (1 << t), q | (1 << t));
+        return;
+    }
+    const char* g = (kb & KF_REAL) ? "gate1r" : "gate1";
+    if ((en & all) == all) o("      %s<%d, false>(v, %s, 0xffffu);\n", g, t, coef.c_str());
+    else if (en) o("      %s<%d, true>(v, %s, 0x%xu);\n", g, t, coef.c_str(), en);
 }
 
 // One register round: the interpreter's round loop (tile_kernels.cu) with every structural
@@ -162,20 +186,19 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
             o("        for (int q = 0; q < %d; ++q) v[q] = make_double2(v[q].x * sc, v[q].y * sc); }\n", G);
         } else if (kind == TOP_GATE && (kb & KF_BUNDLE)) {
             for (int b = 0; b < W; ++b)
-                if (op.t >> b & 1)
-                    o("      %s<%d, false>(v, P.pool + %d, 0xffffu);\n", (kb & KF_REAL) ? "gate1r" : "gate1", b,
-                      op.ref + 4 * b);
+                if (op.t >> b & 1) emit_gate(o, kb, b, P.pool + op.ref + 4 * b, "P.pool + " + std::to_string(op.ref + 4 * b),
+                                             (1u << G) - 1, G);
         } else if (kind == TOP_GATE) {
-            const char* g = (kb & KF_REAL) ? "gate1r" : "gate1";
-            if (op.lctrl_mask) {
-                o("      { unsigned en = 0;\n");
-                for (int q = 0; q < G; ++q)
-                    o("        en |= unsigned(((lb | %uu) & %uu) == %uu) << %d;\n", off[q], unsigned(op.lctrl_mask),
-                      unsigned(op.lctrl_val), q);
-                o("        %s<%d, true>(v, P.ops[%d].c, en); }\n", g, op.t, oi);
-            } else {
-                o("      %s<%d, false>(v, P.ops[%d].c, 0xffffu);\n", g, op.t, oi);
-            }
+            // controls on register bits select registers (a literal mask); controls on the other
+            // tile bits are one condition per group
+            const unsigned cmr = unsigned(op.lctrl_mask) & regmask, cvr = unsigned(op.lctrl_val) & regmask;
+            const unsigned cmn = unsigned(op.lctrl_mask) & ~regmask, cvn = unsigned(op.lctrl_val) & ~regmask;
+            unsigned en = 0;
+            for (int q = 0; q < G; ++q)
+                if ((off[q] & cmr) == cvr) en |= 1u << q;
+            if (cmn) o("      if ((lb & %uu) == %uu) {\n", cmn, cvn);
+            emit_gate(o, kb, op.t, op.c, "P.ops[" + std::to_string(oi) + "].c", en, G);
+            if (cmn) o("      }\n");
         } else if (kind == TOP_DTAB) {
             for (int q = 0; q < G; ++q)
                 if (!(op.dskip >> q & 1)) o("      v[%d] = cmul_f(P.pool[%d], v[%d]);\n", q, op.ref + q, q);
