@@ -58,6 +58,12 @@ bool knob_swaps() {
     return on;
 }
 
+bool has_pivot(const PassParams& p) {
+    for (int i = 0; i < p.nops; ++i)
+        if ((p.ops[i].kind & KF_KIND) == TOP_GATE && (p.ops[i].kind & KF_PIVOT)) return true;
+    return false;
+}
+
 int knob_unroll() {
     static const int u = [] { const char* v = std::getenv("QCS_JIT_UNROLL"); return v ? std::atoi(v) : 1; }();
     return u;
@@ -87,10 +93,16 @@ std::string const_bits(bool c0, bool c1, int dk, int p0, int p1) {
 // (exactly [[0, 1], [1, 0]]) are register swaps -- no arithmetic, value-identical to the
 // interpreter's 0*x0 + 1*x1 up to the sign of an exact zero -- the others the real or complex
 // 2x2 forms of tile_device.cuh.
-void emit_gate(Out& o, int kb, int t, const double2* c, const std::string& coef, unsigned en, int G) {
+void emit_gate(Out& o, int kb, int t, const double2* c, const std::string& coef, unsigned en, int G, unsigned piv) {
+    const unsigned all = (1u << G) - 1;
+    if (kb & KF_PIVOT) {  // piv: this bit's 4 pivot flags
+        if (en & all)
+            o("      gate1p<%d, %d, %d, %d, %d, %d, 0x%xu>(v, (%s)[0], (%s)[1]);\n", t, int(piv & 1), int(piv >> 1 & 1),
+              int(piv >> 2 & 1), int(piv >> 3 & 1), (kb & KF_REAL) ? 1 : 0, en & all, coef.c_str(), coef.c_str());
+        return;
+    }
     const bool swap = c[0].x == 0.0 && c[0].y == 0.0 && c[3].x == 0.0 && c[3].y == 0.0 && c[1].x == 1.0 &&
                       c[1].y == 0.0 && c[2].x == 1.0 && c[2].y == 0.0 && knob_swaps();
-    const unsigned all = (1u << G) - 1;
     if (swap) {
         for (int q = 0; q < G; ++q)
             if (!(q >> t & 1) && (en >> q & 1))
@@ -165,7 +177,7 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
         const bool gc = kb & KF_GCTRL;
         if (gc) o("      if ((base & 0x%llxull) == 0x%llxull) {\n", (unsigned long long)op.gctrl_mask,
                   (unsigned long long)op.gctrl_val);
-        if ((kb & KF_SIGNED) && (kb & KF_BUNDLE)) {
+        if (kind == TOP_DIAG && (kb & KF_SIGNED) && (kb & KF_BUNDLE)) {
             o("      { unsigned acc = 0x%llxu;\n", (unsigned long long)(op.smask & gmask));
             for (int i = 0; i < op.t; ++i) {
                 SignEntry e;
@@ -174,7 +186,7 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
                   const_bits(e.cmask & 1u, e.cmask & 2u, e.dk, e.p0, e.p1).c_str(), gmask);
             }
             o("        negacc ^= acc; }\n");
-        } else if (kb & KF_SIGNED) {
+        } else if (kind == TOP_DIAG && (kb & KF_SIGNED)) {
             const bool c0 = op.dreg[0] == 0xff, c1 = op.dk == 2 && op.dreg[1] == 0xff;
             o("      negacc ^= unsigned(0x%llxull >> (%d * (%s))) & 0x%llxu;\n", (unsigned long long)op.smask, G,
               const_bits(c0, c1, op.dk, op.dpos[0], op.dpos[1]).c_str(), gmask);
@@ -187,7 +199,7 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
         } else if (kind == TOP_GATE && (kb & KF_BUNDLE)) {
             for (int b = 0; b < W; ++b)
                 if (op.t >> b & 1) emit_gate(o, kb, b, P.pool + op.ref + 4 * b, "P.pool + " + std::to_string(op.ref + 4 * b),
-                                             (1u << G) - 1, G);
+                                             (1u << G) - 1, G, (op.dtab >> (4 * b)) & 15u);
         } else if (kind == TOP_GATE) {
             // controls on register bits select registers (a literal mask); controls on the other
             // tile bits are one condition per group
@@ -197,11 +209,17 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
             for (int q = 0; q < G; ++q)
                 if ((off[q] & cmr) == cvr) en |= 1u << q;
             if (cmn) o("      if ((lb & %uu) == %uu) {\n", cmn, cvn);
-            emit_gate(o, kb, op.t, op.c, "P.ops[" + std::to_string(oi) + "].c", en, G);
+            emit_gate(o, kb, op.t, op.c, "P.ops[" + std::to_string(oi) + "].c", en, G, op.dtab & 15u);
             if (cmn) o("      }\n");
         } else if (kind == TOP_DTAB) {
-            for (int q = 0; q < G; ++q)
-                if (!(op.dskip >> q & 1)) o("      v[%d] = cmul_f(P.pool[%d], v[%d]);\n", q, op.ref + q, q);
+            for (int q = 0; q < G; ++q) {
+                if (op.dskip >> q & 1) continue;
+                if (P.pool[op.ref + q].y == 0.0)  // real entry (e.g. only gate row scales): 2 FP64
+                    o("      { const double s = P.pool[%d].x; v[%d] = make_double2(v[%d].x * s, v[%d].y * s); }\n", op.ref + q,
+                      q, q, q);
+                else
+                    o("      v[%d] = cmul_f(P.pool[%d], v[%d]);\n", q, op.ref + q, q);
+            }
         } else if (kind == TOP_DIAG) {
             if (op.dk == 1 && op.dreg[0] == 0xff) {
                 o("      { const int g = int((g0 >> %d) & 1);\n", op.dpos[0]);
@@ -353,7 +371,7 @@ JitKernel& compile(const std::string& src) {
 bool wanted(const PassParams& p, double tiles) {
     const int mode = jit_mode();
     if (mode == 0) return false;
-    return mode == 2 || (tiles * double(p.nrounds) >= 32768.0 && p.nrounds >= 2);
+    return mode >= 2 || has_pivot(p) || (tiles * double(p.nrounds) >= 32768.0 && p.nrounds >= 2);
 }
 
 }  // namespace
@@ -363,14 +381,24 @@ std::atomic<int> g_mode{[] {
     const char* v = std::getenv("QCS_JIT");
     if (!v || !*v) return 1;                 // default: passes with enough work
     if (!std::strcmp(v, "force")) return 2;  // every tile pass
+    if (!std::strcmp(v, "pivot")) return 3;  // every tile pass, pivoted gates
     return std::atoi(v) != 0 ? 1 : 0;
 }()};
 }  // namespace
 
 int jit_mode() { return g_mode.load(std::memory_order_relaxed); }
 void set_jit_mode(int mode) {
-    if (mode < 0 || mode > 2) raise(QCS_ERR_ARG, "jit mode must be 0, 1 or 2");
+    if (mode < 0 || mode > 3) raise(QCS_ERR_ARG, "jit mode must be 0, 1, 2 or 3");
     g_mode.store(mode);
+}
+
+bool jit_pivot(int n, const PassParams& p) {
+    static const bool pivots = [] { const char* v = std::getenv("QCS_JIT_PIVOT"); return !v || std::atoi(v) != 0; }();
+    const int mode = jit_mode();
+    if (mode == 3) return true;
+    if (mode != 1 || !pivots) return false;
+    const double tiles = p.list_cnt ? double(p.list_cnt) : std::ldexp(1.0, n - p.m);
+    return wanted(p, tiles);
 }
 
 unsigned long long jit_compiles() { return g_compiles.load(); }

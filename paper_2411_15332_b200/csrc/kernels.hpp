@@ -108,6 +108,12 @@ constexpr int KF_BUNDLE = 0x10;  // TOP_GATE: dense gates on the register bits o
 constexpr int KF_FLUSH = 0x20;   // apply the pending +-1 sign flips before this op (set by the planner)
 constexpr int KF_SIGNED = 0x40;  // TOP_DIAG with entries in {+1, -1}: dskip holds the -1 entries
 constexpr int KF_GCTRL = 0x80;   // has controls outside the tile (gctrl_mask / gctrl_val)
+// KF_PIVOT on TOP_GATE (the KF_SIGNED bit; that one is TOP_DIAG-only): pivoted form, specialised
+// kernels only.  Per target bit b (single gates: b = 0 in the fields), output row r is
+// x[piv] + rho_r * x[other], with rho_r in coefficient slot r (c[r] / pool[ref + 4b + r]); dtab
+// bits 4b..4b+3 = piv_0, piv_1 (1: the row's pivot is input 1), zero_0, zero_1 (rho_r == 0).  The
+// rows' scales were folded into the round's diagonal table (TOP_DTAB).
+constexpr int KF_PIVOT = KF_SIGNED;
 
 // Compact register-round operation; a pass's list travels in the kernel parameter space.
 struct RegOp {
@@ -172,7 +178,8 @@ struct alignas(64) TmapParam {
 bool launch_tile_pass_jit(double2* amps, const struct PassParams& p, unsigned F, const struct TileOp* big_dev,
                           const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, const TmapParam& tmap,
                           unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st);
-int jit_mode();                      // 0 off, 1 passes with enough work (default), 2 every tile pass
+int jit_mode();                      // 0 off, 1 passes with enough work (default), 2 every tile pass, 3 = 2 + pivots
+bool jit_pivot(int n, const struct PassParams& p);  // lower this pass's gates to the pivoted form
 void set_jit_mode(int mode);
 std::size_t jit_compile_only(const struct PassParams& p);  // NVRTC only (no device): cubin bytes
 void tile_pass_shape(const struct PassParams& p, unsigned& F, unsigned& threads);  // kernel variant, CTA size

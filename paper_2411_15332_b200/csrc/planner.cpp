@@ -356,6 +356,129 @@ bool missed_tile_program(const std::vector<FOp>& ops, const std::vector<int>& li
 
 // Lower planned passes to kernel descriptors: one PassParams (constant-bank operation list) per
 // pass, plus the plan-wide TileOp array (shared-memory gates, sign steps, 3-bit diagonals).
+namespace {
+
+// Pivoted gates for the specialised kernels: a 2x2 row (a, b) with pivot a (the larger entry) is
+// a * (x_piv + (b / a) x_other) -- one fused multiply-add per component for a real ratio, two for
+// a complex one, instead of two / four -- and the row scale a commutes to the end of the round
+// when no later operation of the round targets the gate's bit, where it joins the round's
+// diagonal table (created if the round has none).  Gates qualify without controls outside the
+// registers; controls on register bits select which table entries take the scale.
+void pivot_pass(PassParams& P, int& npool) {
+    const int nr = P.alt_mode == ALT_ROUNDS ? P.alt_begin + P.alt_nrounds : P.nrounds;
+    std::vector<RegOp> ops;
+    std::vector<RoundDesc> rounds(P.rounds, P.rounds + nr);
+    for (int ri = 0; ri < nr; ++ri) {
+        RoundDesc& R = rounds[std::size_t(ri)];
+        const int b0 = R.op_begin, b1 = R.op_begin + R.op_count;
+        R.op_begin = std::uint16_t(ops.size());
+        std::vector<RegOp> rops(P.ops + b0, P.ops + b1);
+        if (R.flags & RD_SMEM) {
+            ops.insert(ops.end(), rops.begin(), rops.end());
+            continue;
+        }
+        unsigned regmask = 0;
+        for (int i = 0; i < 3; ++i) regmask |= 1u << R.r[i];
+        // the round's table: the existing one (the last operation) or a new one
+        int tab = -1;
+        if (!rops.empty() && (rops.back().kind & KF_KIND) == TOP_DTAB) tab = int(rops.size()) - 1;
+        cplx table[8];
+        for (int q = 0; q < 8; ++q)
+            table[q] = tab >= 0 ? cplx(P.pool[rops[std::size_t(tab)].ref + q].x, P.pool[rops[std::size_t(tab)].ref + q].y)
+                                : cplx(1.0, 0.0);
+        const bool room = tab >= 0 || (npool + 8 <= kPassPool && int(ops.size() + rops.size()) + 1 < kPassMaxOps);
+        bool changed = false;
+        for (std::size_t i = 0; i < rops.size() && room; ++i) {
+            RegOp& o = rops[i];
+            if ((o.kind & KF_KIND) != TOP_GATE || (o.kind & KF_GCTRL) || (o.lctrl_mask & ~regmask)) continue;
+
+            const bool bundle = o.kind & KF_BUNDLE;
+            const unsigned bits = bundle ? o.t : 1u << o.t;
+            // the deferred scale is a diagonal on the target and the (register) control bits: no
+            // later operation of the round may target any of them
+            unsigned support = bits;
+            for (int k = 0; k < 3; ++k)
+                if (o.lctrl_mask >> R.r[k] & 1) support |= 1u << k;
+            bool later = false;
+            for (std::size_t j = i + 1; j < rops.size(); ++j) {
+                const int k = rops[j].kind & KF_KIND;
+                const unsigned tj = k == TOP_WHT || (rops[j].kind & KF_BUNDLE) ? rops[j].t
+                                    : k == TOP_GATE ? 1u << rops[j].t : 0u;
+                if ((k == TOP_GATE || k == TOP_WHT) && (tj & support)) later = true;
+            }
+            if (later) continue;
+            // registers the gate acts on (register-bit controls)
+            unsigned en = 0;
+            for (int q = 0; q < 8; ++q) {
+                unsigned lq = 0;
+                for (int k = 0; k < 3; ++k)
+                    if (q >> k & 1) lq |= 1u << R.r[k];
+                if ((lq & o.lctrl_mask) == o.lctrl_val) en |= 1u << q;
+            }
+            // every target bit must pivot (a zero row cannot)
+            double2* cs[3] = {nullptr, nullptr, nullptr};
+            bool ok = true;
+            for (int b = 0; b < 3; ++b)
+                if (bits >> b & 1) {
+                    cs[b] = bundle ? P.pool + o.ref + 4 * b : o.c;
+                    for (int r = 0; r < 2; ++r) ok &= std::abs(cplx(cs[b][2 * r].x, cs[b][2 * r].y)) +
+                                                          std::abs(cplx(cs[b][2 * r + 1].x, cs[b][2 * r + 1].y)) > 0.0;
+                }
+            if (!ok) continue;
+            unsigned piv = 0;
+            for (int b = 0; b < 3; ++b) {
+                if (!(bits >> b & 1)) continue;
+                double2* c = cs[b];
+                const int fb = bundle ? b : 0;
+                cplx scale[2], rho[2];
+                for (int r = 0; r < 2; ++r) {
+                    const cplx a0(c[2 * r].x, c[2 * r].y), a1(c[2 * r + 1].x, c[2 * r + 1].y);
+                    const int pv = std::abs(a1) > std::abs(a0) ? 1 : 0;
+                    scale[r] = pv ? a1 : a0;
+                    rho[r] = (pv ? a0 : a1) / scale[r];
+                    piv |= unsigned(pv) << (4 * fb + r);
+                    if (rho[r] == cplx(0.0, 0.0)) piv |= 1u << (4 * fb + 2 + r);
+                }
+                for (int r = 0; r < 2; ++r) c[r] = make_double2(rho[r].real(), rho[r].imag());
+                c[2] = c[3] = make_double2(0.0, 0.0);
+                const int rb = bundle ? b : o.t;
+                for (int q = 0; q < 8; ++q)
+                    if (en >> q & 1) table[q] *= scale[q >> rb & 1];
+            }
+            bool real = true;
+            for (int b = 0; b < 3; ++b)
+                if (bits >> b & 1) real &= cs[b][0].y == 0.0 && cs[b][1].y == 0.0;
+            o.kind = std::uint8_t((o.kind & ~KF_REAL) | KF_PIVOT | (real ? KF_REAL : 0));
+            o.dtab = std::uint16_t(piv);
+            changed = true;
+        }
+        if (changed) {
+            if (tab < 0) {
+                RegOp t{};
+                t.kind = TOP_DTAB;
+                t.ref = std::uint16_t(npool);
+                npool += 8;
+                rops.push_back(t);
+                tab = int(rops.size()) - 1;
+            }
+            RegOp& t = rops[std::size_t(tab)];
+            t.dskip = 0;
+            for (int q = 0; q < 8; ++q) {
+                P.pool[t.ref + q] = make_double2(table[q].real(), table[q].imag());
+                if (table[q] == cplx(1.0, 0.0)) t.dskip = std::uint8_t(t.dskip | (1u << q));
+            }
+        }
+        ops.insert(ops.end(), rops.begin(), rops.end());
+        R.op_count = std::uint16_t(ops.size() - R.op_begin);
+    }
+    if (int(ops.size()) > kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many operations in a pass");
+    std::copy(ops.begin(), ops.end(), P.ops);
+    std::copy(rounds.begin(), rounds.end(), P.rounds);
+    P.nops = int(ops.size());
+}
+
+}  // namespace
+
 void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered& out) {
     out = Lowered{};
     // Missed-tile programs (tile-kernel passes of >= 2 operations).  One that is only a scalar
@@ -755,6 +878,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             }
         }
         P.nops = nops;
+        if (jit_pivot(n, P)) pivot_pass(P, npool);
         out.passes.push_back(P);
         out.pass_ops.push_back(lists[pi]);
         out.single_flip_off.push_back(flip_off);

@@ -176,6 +176,25 @@ __device__ __forceinline__ void gate1r(double2 (&v)[8], const double2* c, unsign
     }
 }
 
+// Pivoted form (specialised kernels, KF_PIVOT): row r = x[piv_r] + rho_r * x[other] on the
+// register pairs along bit T of the registers in EN; the row scales sit in the round's table.
+template <int T, bool P0, bool P1, bool Z0, bool Z1, bool REAL, unsigned EN>
+__device__ __forceinline__ void gate1p(double2 (&v)[8], double2 rho0, double2 rho1) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if ((q & (1 << T)) || !((EN >> q) & 1u)) continue;
+        const double2 x0 = v[q], x1 = v[q | (1 << T)];
+        const double2 p0 = P0 ? x1 : x0, o0 = P0 ? x0 : x1, p1 = P1 ? x1 : x0, o1 = P1 ? x0 : x1;
+        double2 n0 = p0, n1 = p1;
+        if (!Z0) n0 = REAL ? make_double2(fma(rho0.x, o0.x, p0.x), fma(rho0.x, o0.y, p0.y))
+                           : make_double2(fma(rho0.x, o0.x, fma(-rho0.y, o0.y, p0.x)), fma(rho0.x, o0.y, fma(rho0.y, o0.x, p0.y)));
+        if (!Z1) n1 = REAL ? make_double2(fma(rho1.x, o1.x, p1.x), fma(rho1.x, o1.y, p1.y))
+                           : make_double2(fma(rho1.x, o1.x, fma(-rho1.y, o1.y, p1.x)), fma(rho1.x, o1.y, fma(rho1.y, o1.x, p1.y)));
+        v[q] = n0;
+        v[q | (1 << T)] = n1;
+    }
+}
+
 // Apply and clear the pending +-1 flips (bit q of negacc: negate register q) by xor of the sign
 // bits: straight-line, so the round loop keeps one register assignment.
 template <int NG>

@@ -372,6 +372,9 @@ void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev
         check_launch("qcs_pass");
         return;
     }
+    for (int i = 0; i < p.nops; ++i)
+        if ((p.ops[i].kind & KF_KIND) == TOP_GATE && (p.ops[i].kind & KF_PIVOT))
+            raise(QCS_ERR_SIM, "internal: pivoted gates need the specialised kernel");
     switch (f) {
 #define QCS_TILE_CASE(x) \
     case x: launch_f<x>(amps, p, big_dev, flipped_dev, unsigned(tiles), tables_dev, tmap, threads, smem, st); break;

@@ -2,6 +2,7 @@
 k_tile: the generated source must compile for every kind of tile operation and round (CPU,
 NVRTC only), and on the GPU both forms must give bit-identical states up to the sign of exact
 zeros (same arithmetic, same order; X-like gates become register swaps instead of 0*x0 + 1*x1)
+(mode 2), and with pivoted gates (mode 3, the default for big passes) agree with the oracle,
 on circuits that exercise gates (real / complex, bundled, controls inside and outside
 the tile), diagonal tables and phases on 1-3 bits, sign flips and sign steps with missed-tile
 programs, butterflies, scales and shared-memory gate rounds."""
@@ -73,11 +74,11 @@ def test_generated_sources_compile(Q, cfg):
 def test_jit_mode_switch(Q):
     old = Q.jit_mode()
     try:
-        for m in (0, 2, 1):
+        for m in (0, 2, 3, 1):
             Q.set_jit_mode(m)
             assert Q.jit_mode() == m
         with pytest.raises(ValueError):
-            Q.set_jit_mode(3)
+            Q.set_jit_mode(4)
     finally:
         Q.set_jit_mode(old)
 
@@ -97,11 +98,12 @@ def run_mode(Q, c, mode, fuse=True):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(3))
 def test_specialised_equals_interpreter_random(Q, seed):
+    """(Every pass compiles its own kernel here, ~0.5 s each: the stepwise form only once.)"""
     n = 13 + seed
     c = random_catalog_circuit(Q, seed, n)
-    for fuse in (True, False):
+    for fuse in ((True, False) if seed == 0 else (True,)):
         assert same(run_mode(Q, c, 2, fuse), run_mode(Q, c, 0, fuse)), (seed, fuse)
 
 
@@ -113,9 +115,51 @@ def test_specialised_equals_interpreter_circuits(Q, cfg):
         assert same(run_mode(Q, c, 2), run_mode(Q, c, 0)), c.n
 
 
+TOL_AMP, TOL_L2 = 1e-12, 1e-10
+
+
+def oracle_run(oracle, c):
+    x = np.zeros(1 << c.n, np.complex128)
+    x[c.initial] = 1
+    for st in c.steps:
+        if int(st.kind) == 1:
+            x = oracle.apply_diag(c.n, sorted(set(st.diag.flipped)), st.diag.flip_rest, x)
+        elif st.is_hadamard_all(c.n):
+            x = oracle.wht(c.n, x)
+        else:
+            x = oracle.apply_step(c.n, [(p.qubit_list(), p.gate.matrix) for p in st.placements], x)
+    return x
+
+
+@pytest.mark.gpu
+def test_pivoted_gates_against_oracle(Q, cfg, oracle):
+    """Mode 3: every tile pass specialised, with pivoted gates (row scales folded into the
+    rounds' diagonal tables: a different rounding, so the floating-point bar) against the
+    oracle."""
+    G = Q.gate_catalog_lookup
+    # a deferred row scale of a controlled gate is a diagonal on its control bits too: a later
+    # gate on the control bit in the same round must keep it from moving (regression)
+    ctrl_chain = Q.Circuit(12, [Q.hadamard_all(12)] + [Q.CircuitStep.of_gates([p]) for p in (
+        Q.Placement(G("RX", [5.703]), qubits=[0]),
+        Q.Placement(G("CU", [2.54, 4.966, 2.455, 3.298]), qubits=[11, 9]),
+        Q.Placement(G("CU", [3.229, 1.978, 4.731, 1.819]), qubits=[0, 11]))])
+    # (random whole-catalog circuits compile ~2 s per pass: shared-memory gate rounds)
+    circuits = [random_catalog_circuit(Q, 0, 13), random_catalog_circuit(Q, 5, 14, 16)]
+    circuits += [ctrl_chain, sign_sandwich(Q, 15), cfg.c4_circuit(15, 3), cfg.c5_circuit(15, 3, global_qubits=2),
+                 cfg.c3_circuit(14), cfg.c1_circuit()]
+    for c in circuits:
+        want = oracle_run(oracle, c)
+        for fuse in (True,):
+            got = run_mode(Q, c, 3, fuse)
+            assert np.abs(got - want).max() <= TOL_AMP, (c.n, fuse)
+            assert np.linalg.norm(got - want) <= TOL_L2, (c.n, fuse)
+
+
 @pytest.mark.gpu
 def test_default_mode_specialises_big_passes(Q, cfg):
-    """At n = 22 the C4 passes (1024 tiles x >= 32 rounds) take the specialised kernels in the
-    default mode; same bits as the interpreter."""
+    """At n = 22 the C4 passes (1024 tiles x >= 32 rounds) take the specialised kernels with
+    pivoted gates in the default mode: within the bar of the (oracle-checked) interpreter."""
     c = cfg.c4_circuit(22, 2)
-    assert same(run_mode(Q, c, 1), run_mode(Q, c, 0))
+    got, want = run_mode(Q, c, 1), run_mode(Q, c, 0)
+    assert np.abs(got - want).max() <= TOL_AMP
+    assert np.linalg.norm(got - want) <= TOL_L2
