@@ -145,7 +145,7 @@ def test_pivoted_gates_against_oracle(Q, cfg, oracle):
         Q.Placement(G("CU", [3.229, 1.978, 4.731, 1.819]), qubits=[0, 11]))])
     # (random whole-catalog circuits compile ~2 s per pass: shared-memory gate rounds)
     circuits = [random_catalog_circuit(Q, 0, 13), random_catalog_circuit(Q, 5, 14, 16)]
-    circuits += [ctrl_chain, sign_sandwich(Q, 15), cfg.c4_circuit(15, 3), cfg.c5_circuit(15, 3, global_qubits=2),
+    circuits += [ctrl_chain, sign_sandwich(Q, 15), cfg.c4_circuit(11, 3), cfg.c5_circuit(15, 3, global_qubits=2),
                  cfg.c3_circuit(14), cfg.c1_circuit()]
     for c in circuits:
         want = oracle_run(oracle, c)
