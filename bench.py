@@ -479,9 +479,10 @@ def run_circuit_arm(args, rank, world, local_rank):
                             "frac_nominal_8TBs": achieved / 8000.0, "traffic": None,
                             "passes_per_step": plan["passes"], "skip_passes_per_step": plan["skip_passes"],
                             "kernel_ms_per_step": k_ms / args.steps,
-                            # full sweeps at copy bandwidth (skip passes move only the reached tiles)
-                            "pass_floor_ms": (plan["passes"] - plan["skip_passes"]) * 32.0 * (1 << c.n)
-                            / (peak * 1e9) * 1e3}
+                            # the launched passes' algorithmic bytes at copy bandwidth (skip passes and
+                            # pass pairs move only the tiles they reach)
+                            "pass_floor_ms": k_bytes / args.steps / (peak * 1e9) * 1e3,
+                            "full_sweeps_per_step": k_bytes / args.steps / (32.0 * (1 << c.n))}
         line["kernel_classes"] = {k: {"launches": v[0] / args.steps, "ms": round(v[1] / args.steps, 3),
                                       "GBps": v[2] / (v[1] / 1e3) / 1e9} for k, v in timing.items()}
         line["gpu_launches"] = int(sum(v[0] for v in timing.values()))

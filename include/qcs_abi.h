@@ -211,6 +211,8 @@ typedef struct qcs_plan_info {
     int64_t max_tile_bits;  /* tile size used (log2 amplitudes) */
     int64_t alt_passes;     /* tile passes with a simplified program for tiles no sign step reaches */
     int64_t skip_passes;    /* ... where that program is the identity: only the reached tiles move */
+    int64_t paired_passes;  /* passes of a pair around a skip pass that composes to a scalar: they
+                               run only on the tiles the skip pass reaches */
 } qcs_plan_info;
 int qcs_plan_stats(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
                    qcs_plan_info* out);

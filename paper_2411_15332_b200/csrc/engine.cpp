@@ -499,6 +499,7 @@ void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out) {
         ++out->tile_passes;
         if (p.alt_mode != ALT_NONE) ++out->alt_passes;
         if (p.alt_mode == ALT_SKIP) ++out->skip_passes;
+        if (p.alt_mode == ALT_NONE && p.list_cnt) ++out->paired_passes;
         out->rounds += p.nrounds;
         for (int r = 0; r < p.nrounds; ++r)
             if (p.rounds[r].flags & RD_SMEM) ++out->smem_rounds;

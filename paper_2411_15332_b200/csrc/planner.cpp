@@ -319,12 +319,12 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
 // when the pass has no sign step; alt = the remaining operations (a leading scale if the
 // scalar is not 1), empty when the pass is the identity on those tiles.  Exact: the scalars are
 // +-1, the H^n scales 2^(-n/2) and the factors 2.
-bool missed_tile_program(const std::vector<FOp>& ops, const std::vector<int>& list, std::vector<FOp>& alt) {
-    bool any_sign = false;
-    for (int idx : list) any_sign |= ops[std::size_t(idx)].kind == TOP_SIGN;
-    if (!any_sign) return false;
-    double s = 1.0;
-    std::vector<int> keep;
+// Reduce an operation list with every sign step taken as its missed-tile scalar (-1 when
+// flip_rest, else +1): scales and sign scalars multiply into s, and a butterfly pair on one bit
+// with nothing between them touching that bit is 2 I.  keep = what remains, in order.
+void reduce_scalar(const std::vector<FOp>& ops, const std::vector<int>& list, double& s, std::vector<int>& keep) {
+    s = 1.0;
+    keep.clear();
     for (int idx : list) {
         const FOp& f = ops[std::size_t(idx)];
         if (f.kind == TOP_SIGN) {
@@ -348,6 +348,15 @@ bool missed_tile_program(const std::vector<FOp>& ops, const std::vector<int>& li
         }
         keep.push_back(idx);
     }
+}
+
+bool missed_tile_program(const std::vector<FOp>& ops, const std::vector<int>& list, std::vector<FOp>& alt) {
+    bool any_sign = false;
+    for (int idx : list) any_sign |= ops[std::size_t(idx)].kind == TOP_SIGN;
+    if (!any_sign) return false;
+    double s = 1.0;
+    std::vector<int> keep;
+    reduce_scalar(ops, list, s, keep);
     alt.clear();
     if (s != 1.0) alt.push_back(make_scale(s));
     for (int idx : keep) alt.push_back(ops[std::size_t(idx)]);
@@ -488,11 +497,11 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
     std::vector<std::vector<int>> lists(np);
     std::vector<std::vector<FOp>> alts(np);
     std::vector<char> has_alt(np, 0);
-    int carrier = -1;
+    bool any_plain = false;  // a pass that runs every tile exists (it can carry the scalars)
     for (std::size_t i = 0; i < np; ++i) {
         lists[i] = plan.passes[i].ops;
         if (lists[i].size() >= 2) has_alt[i] = missed_tile_program(ops_in, lists[i], alts[i]);
-        if (!has_alt[i] && carrier < 0) carrier = int(i);
+        any_plain |= !has_alt[i];
     }
     std::vector<FOp> ext;  // ops_in plus the scales the deferral adds
     bool extended = false;
@@ -505,7 +514,8 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
         return int(ext.size()) - 1;
     };
     double carry = 1.0;
-    for (std::size_t i = 0; i < np && carrier >= 0; ++i) {
+    std::vector<char> skip(np, 0);
+    for (std::size_t i = 0; i < np && any_plain; ++i) {
         if (!has_alt[i] || alts[i].size() > 1 || (alts[i].size() == 1 && alts[i][0].kind != TOP_SCALE)) continue;
         const double sc = alts[i].empty() ? 1.0 : alts[i][0].scale;
         if (sc != 1.0) {
@@ -514,8 +524,68 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             carry *= sc;
         }
         alts[i].clear();
+        skip[i] = 1;
     }
+    // Pass pairs around a skip pass.  With Q a skip pass (the identity, after the carried scalar,
+    // on every tile its sign steps miss) between passes P and P' on the same tile bits whose
+    // programs compose to a scalar s (P' P = s I: e.g. the same butterflies twice, Grover's
+    // H_low ... H_low), the triple P' Q P is s I on every P-tile that no tile Q reaches
+    // intersects.  So P and P' run only on the P-tiles that do (one Q-tile meets 2^k P-tiles,
+    // k = the Q-tile bits outside P's tile), s moves to the carrier, and P' appends 1/s on the
+    // tiles it runs.  Exact: s is a power of two (butterfly pairs) times the pass scales.
+    std::vector<std::vector<u64>> forced(np);
+    for (std::size_t i = 0; i + 2 < np && any_plain; ++i) {
+        const std::size_t j = i + 1, k = i + 2;
+        if (!skip[j] || !forced[i].empty() || has_alt[i] || has_alt[k] || lists[i].size() < 2 || lists[k].size() < 2)
+            continue;
+        const u64 S = plan.passes[i].tile, SQ = plan.passes[j].tile;
+        if (plan.passes[k].tile != S) continue;
+        std::vector<int> both = lists[i];
+        both.insert(both.end(), lists[k].begin(), lists[k].end());
+        double s2 = 1.0;
+        std::vector<int> rest;
+        reduce_scalar(extended ? ext : ops_in, both, s2, rest);
+        if (!rest.empty() || s2 == 0.0 || std::fabs(std::log2(std::fabs(carry * s2))) > 400.0) continue;
+        // the P-tiles that the reached Q-tiles meet
+        std::vector<u64> flips;
+        for (int idx : lists[j]) {
+            const FOp& f = (extended ? ext : ops_in)[std::size_t(idx)];
+            if (f.kind == TOP_SIGN) flips.insert(flips.end(), f.flips.begin(), f.flips.end());
+        }
+        const u64 full = n >= 64 ? ~u64(0) : (u64(1) << n) - 1;
+        const u64 outP = full & ~S, freeb = outP & SQ;  // P-tile bits a Q-tile leaves free
+        const int nfree = __builtin_popcountll(freeb), nout = __builtin_popcountll(outP);
+        if (flips.empty() || nfree > 16 || nout >= 63) continue;
+        std::vector<u64> touched;
+        for (u64 e : flips)
+            for (u64 v = 0; v < (u64(1) << nfree); ++v) {
+                u64 x = e & ~freeb, w = v;  // deposit v into the free bits
+                for (int b = 0; b < n; ++b)
+                    if (freeb >> b & 1) {
+                        x = (x & ~(u64(1) << b)) | ((w & 1) << b);
+                        w >>= 1;
+                    }
+                u64 tile = 0;  // x's bits outside P's tile, compressed
+                for (int b = 0, c = 0; b < n; ++b)
+                    if (outP >> b & 1) tile |= ((x >> b) & 1) << c++;
+                touched.push_back(tile);
+            }
+        std::sort(touched.begin(), touched.end());
+        touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+        if (touched.size() > (u64(1) << nout) / 8) continue;  // not worth it
+        if (s2 != 1.0) {
+            lists[k].push_back(add_op(make_scale(1.0 / s2)));
+            carry *= s2;
+        }
+        forced[i] = touched;
+        forced[k] = touched;
+        ++i;  // P' is used up
+    }
+    int carrier = -1;
+    for (std::size_t i = 0; i < np && carrier < 0; ++i)
+        if (!has_alt[i] && forced[i].empty()) carrier = int(i);
     if (carry != 1.0) {
+        if (carrier < 0) raise(QCS_ERR_SIM, "internal: no pass to carry the deferred scalars");
         auto& cl = lists[std::size_t(carrier)];
         cl.insert(cl.begin(), add_op(make_scale(carry)));
     }
@@ -876,6 +946,12 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 P.list_cnt = std::uint32_t(hit.size());
                 out.tables.insert(out.tables.end(), hit.begin(), hit.end());
             }
+        }
+        if (!forced[pi].empty()) {  // one of a pass pair around a skip pass: only the tiles it reaches
+            if (out.tables.size() & 1) out.tables.push_back(0);
+            P.list_off = std::uint32_t(out.tables.size());
+            P.list_cnt = std::uint32_t(forced[pi].size());
+            out.tables.insert(out.tables.end(), forced[pi].begin(), forced[pi].end());
         }
         P.nops = nops;
         if (jit_pivot(n, P)) pivot_pass(P, npool);

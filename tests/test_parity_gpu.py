@@ -357,3 +357,29 @@ def test_c2_full_size_properties(Q, cfg):
         s.apply_gate(hg, [q])
     assert np.abs(s.gather(probe) - before).max() < 1e-15
     assert abs(s.norm() - 1) < 1e-12
+
+
+@pytest.mark.parametrize("n", [22, 23])
+def test_pass_pairs_around_sign_steps_vs_oracle(Q, oracle, n):
+    """Grover-like circuits with several marked indices (one and three per oracle step, flip_rest
+    both ways): the planner pairs the H_low passes around each skip pass (plan_stats
+    paired_passes) and runs them only on the tiles the sign steps reach; against the oracle."""
+    rng = np.random.default_rng(n)
+    H = Q.hadamard_all(n)
+    steps = [H]
+    for it in range(4):
+        marked = [int(i) for i in rng.choice(1 << n, 1 + 2 * (it % 2), replace=False)]
+        steps += [Q.CircuitStep.of_diag(Q.DiagSign(marked, it == 2)), H,
+                  Q.CircuitStep.of_diag(Q.DiagSign([0], True)), H]
+    c = Q.Circuit(n, steps)
+    assert Q.plan_stats(c)["paired_passes"] > 0
+    x = np.zeros(1 << n, np.complex128)
+    x[0] = 1
+    for st in steps:
+        if st.is_hadamard_all(n):
+            x = oracle.wht(n, x)
+        else:
+            x = oracle.apply_diag(n, sorted(set(st.diag.flipped)), st.diag.flip_rest, x)
+    got = Q.simulate(c, Q.Engine.rh_dax).final.download()
+    assert np.abs(got - x).max() <= TOL_AMP
+    assert np.linalg.norm(got - x) <= TOL_L2

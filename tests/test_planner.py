@@ -34,6 +34,17 @@ def test_grover_sign_passes_skip_missed_tiles():
         assert st["skip_passes"] == st["alt_passes"] == 16, n
 
 
+def test_grover_pass_pairs_around_skip_passes():
+    # between two skip passes, the H_low passes come in pairs H_low Q H_low with Q a skip pass:
+    # H_low H_low = 2^12 I, so each pair runs only on the 2^9 H_low tiles that Q's one reached
+    # tile meets; at n = 30 three passes remain full sweeps (the first H^n)
+    st = Q.plan_stats(configs.c3_circuit(30))
+    assert st["paired_passes"] == 16
+    assert st["passes"] - st["skip_passes"] - st["paired_passes"] == 3
+    # no pairs where the middle pass is not a skip pass
+    assert Q.plan_stats(configs.c4_circuit(24, 2))["paired_passes"] == 0
+
+
 def test_rh_is_ceil_passes():
     # H on every qubit: a 12-bit tile takes bits 0..11, later tiles 9 new bits each (0..2 fixed)
     for n, want in [(12, 1), (21, 2), (28, 3), (30, 3), (32, 4)]:
