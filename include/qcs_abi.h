@@ -175,6 +175,10 @@ typedef struct {
     int fuse;            /* 0: one pass per step in circuit order (bit-exact per step);
                             1: fuse consecutive operations into shared-memory passes
                                (within 1e-12); default 1 */
+    int reset;           /* 1: start from the basis state |initial> (Circuit::initial) instead of
+                            the state's content -- folded into the first pass when that pass
+                            sweeps every tile (no separate write of the state); 0 (default): as is */
+    uint64_t initial;
 } qcs_sim_options;
 
 typedef struct {             /* StepReport, engine.hpp:16-24 */
@@ -188,7 +192,7 @@ typedef struct {             /* StepReport, engine.hpp:16-24 */
 } qcs_step_report;
 
 /* simulate(Circuit, Engine, SimOptions) (engine.hpp:46, engine.cpp:153-210) applied to the
- * state `s` in place.  The caller prepares s (normally qcs_state_set_basis(s, initial)).
+ * state `s` in place, from its current content or (opts->reset) from |opts->initial>.
  * reports: num_steps entries or NULL.  Circuit::validate rules apply (circuit.cpp:41-62). */
 int qcs_simulate(qcs_state* s, const qcs_step* steps, int num_steps, int engine,
                  const qcs_sim_options* opts, qcs_step_report* reports);

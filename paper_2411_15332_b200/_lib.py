@@ -30,7 +30,8 @@ class qcs_step(C.Structure):
 
 
 class qcs_sim_options(C.Structure):
-    _fields_ = [("sign_method", C.c_int), ("block_size", C.c_uint64), ("fuse", C.c_int)]
+    _fields_ = [("sign_method", C.c_int), ("block_size", C.c_uint64), ("fuse", C.c_int), ("reset", C.c_int),
+                ("initial", C.c_uint64)]
 
 
 class qcs_step_report(C.Structure):

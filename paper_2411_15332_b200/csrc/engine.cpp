@@ -113,6 +113,10 @@ qcs_state::~qcs_state() {
     if (timer) qcs::destroy_timer(timer);
     if (flip_buf) cudaFree(flip_buf);
     if (plan_buf) cudaFree(plan_buf);
+    for (auto& st : stage) {
+        if (st.host) cudaFreeHost(st.host);
+        if (st.done) cudaEventDestroy(st.done);
+    }
     if (scratch) cudaFree(scratch);
     for (auto& e : events)
         if (e) cudaEventDestroy(e);
@@ -267,7 +271,9 @@ void run_single(qcs_state* s, const FOp& f, const u64* flips_dev, u64 flip_cnt) 
 }
 
 // Plan, lower, upload and launch a list of operations on the state.
-void run_fused(qcs_state* s, const std::vector<FOp>& ops) {
+// init (>= 0): the state is to start from the basis state |init>; consumed (set to -1) by folding
+// it into the first pass when that pass writes every tile, else by a fill kernel first.
+void run_fused(qcs_state* s, const std::vector<FOp>& ops, std::int64_t* init = nullptr) {
     if (ops.empty()) return;
     const int n = s->n;
     Lowered low;
@@ -290,18 +296,43 @@ void run_fused(qcs_state* s, const std::vector<FOp>& ops) {
     const std::size_t f_off = (bb + 255) & ~std::size_t(255);
     const std::size_t t_off = (f_off + fb + 255) & ~std::size_t(255);
     if (bb + fb + tb) {
-        ensure_plan(s, t_off + tb + 8);
-        std::vector<unsigned char> host(t_off + tb);
-        if (bb) std::memcpy(host.data(), low.big.data(), bb);
-        if (fb) std::memcpy(host.data() + f_off, low.flips.data(), fb);
-        if (tb) std::memcpy(host.data() + t_off, low.tables.data(), tb);
-        // pageable copy: staged before the call returns, so `host` may go out of scope
-        QCS_CUDA(cudaMemcpyAsync(s->plan_buf, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
+        const std::size_t bytes = t_off + tb;
+        ensure_plan(s, bytes + 8);
+        // stream order keeps the upload behind the previous plan's kernels; the pinned slot is
+        // reused only once its earlier upload has been read (four calls back: normally long ago)
+        qcs_state::Stage& sg = s->stage[s->stage_next++ & 3];
+        if (sg.done) QCS_CUDA(cudaEventSynchronize(sg.done));
+        else QCS_CUDA(cudaEventCreateWithFlags(&sg.done, cudaEventDisableTiming));
+        if (sg.cap < bytes) {
+            if (sg.host) QCS_CUDA(cudaFreeHost(sg.host));
+            sg.host = nullptr;
+            sg.cap = 0;
+            const std::size_t cap = std::max<std::size_t>(bytes, 1 << 16);
+            QCS_CUDA(cudaHostAlloc(&sg.host, cap, cudaHostAllocDefault));
+            sg.cap = cap;
+        }
+        auto* host = static_cast<unsigned char*>(sg.host);
+        if (bb) std::memcpy(host, low.big.data(), bb);
+        if (fb) std::memcpy(host + f_off, low.flips.data(), fb);
+        if (tb) std::memcpy(host + t_off, low.tables.data(), tb);
+        QCS_CUDA(cudaMemcpyAsync(s->plan_buf, host, bytes, cudaMemcpyHostToDevice, s->stream));
+        QCS_CUDA(cudaEventRecord(sg.done, s->stream));
     }
     auto* base = static_cast<unsigned char*>(s->plan_buf);
     const auto* big_dev = reinterpret_cast<const TileOp*>(base);
     const auto* flips_dev = reinterpret_cast<const u64*>(base + f_off);
     const auto* tables_dev = reinterpret_cast<const u64*>(base + t_off);
+    if (init && *init >= 0) {
+        const bool fold = !low.passes.empty() && low.pass_ops[0].size() >= 2 && n >= 3 && low.passes[0].list_cnt == 0 &&
+                          low.passes[0].alt_mode != ALT_SKIP;
+        if (fold) {
+            low.passes[0].init = 1;
+            low.passes[0].init_index = u64(*init);
+        } else {
+            fill_basis(s->amps, u64(1) << n, u64(*init), s->stream);
+        }
+        *init = -1;
+    }
     for (std::size_t i = 0; i < low.passes.size(); ++i) {
         const auto& po = low.pass_ops[i];
         if (po.size() == 1) run_single(s, ops[std::size_t(po[0])], flips_dev + low.single_flip_off[i], low.single_flip_cnt[i]);
@@ -426,11 +457,13 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
     const int n = s->n;
     validate_circuit(n, steps, nsteps);
     if (engine < QCS_ENGINE_DENSE || engine > QCS_ENGINE_RH_DAX) raise(QCS_ERR_ARG, "unknown engine");
-    qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1};
+    qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1, 0, 0};
     if (opts) o = *opts;
     const u64 dim = u64(1) << n;
+    if (o.reset && o.initial >= dim) raise(QCS_ERR_DIMENSION, "initial basis index out of range");  // circuit.cpp:41-62
     DeviceGuard g(s->device);
     TimerScope ts(s);
+    std::int64_t init = o.reset ? std::int64_t(o.initial) : -1;
     std::vector<FOp> ops;  // fused mode: the whole circuit; stepwise: one step at a time
     for (int i = 0; i < nsteps; ++i) {
         const qcs_step& st = steps[i];
@@ -466,14 +499,15 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
                 r.madd_count = nnz;         // engine.cpp:191, :199
             }
         }
-        if (!o.fuse) run_fused(s, ops);  // one step: fused only within the step
+        if (!o.fuse) run_fused(s, ops, &init);  // one step: fused only within the step
         if (reports) reports[i] = r;
     }
     if (o.fuse) {
         merge_single_qubit(n, ops);
         split_phases(ops);
-        run_fused(s, ops);
+        run_fused(s, ops, &init);
     }
+    if (init >= 0) fill_basis(s->amps, dim, u64(init), s->stream);  // no operation at all
 }
 
 namespace {
@@ -512,7 +546,7 @@ void plan_stats(int n, const qcs_step* steps, int nsteps, int engine, const qcs_
                 qcs_plan_info* out) {
     validate_circuit(n, steps, nsteps);
     if (engine < QCS_ENGINE_DENSE || engine > QCS_ENGINE_RH_DAX) raise(QCS_ERR_ARG, "unknown engine");
-    qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1};
+    qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1, 0, 0};
     if (opts) o = *opts;
     *out = qcs_plan_info{};
     out->max_tile_bits = std::min(tile_max_bits(), n);
@@ -536,7 +570,7 @@ void plan_compile(int n, const qcs_step* steps, int nsteps, int engine, const qc
                   std::int64_t* kernels, std::int64_t* cubin_bytes) {
     validate_circuit(n, steps, nsteps);
     if (engine < QCS_ENGINE_DENSE || engine > QCS_ENGINE_RH_DAX) raise(QCS_ERR_ARG, "unknown engine");
-    qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1};
+    qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1, 0, 0};
     if (opts) o = *opts;
     *kernels = 0;
     *cubin_bytes = 0;

@@ -21,6 +21,14 @@ struct qcs_state {
     std::size_t flip_cap = 0;
     void* plan_buf = nullptr;             // device copy of the current plan (rounds, ops, flips)
     std::size_t plan_cap = 0;
+    // pinned host staging of plan uploads, a ring: a pageable copy would block the host until the
+    // stream drains, so the next call's planning could not overlap the device's work
+    struct Stage {
+        void* host = nullptr;
+        std::size_t cap = 0;
+        cudaEvent_t done = nullptr;       // the upload from this slot has been read
+    } stage[4];
+    int stage_next = 0;
     cudaEvent_t events[8] = {};
     qcs::LaunchTimer* timer = nullptr;   // per-launch timing (qcs_timing_enable)
     ~qcs_state();

@@ -308,7 +308,39 @@ struct JitKernel {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kernel = nullptr;
     std::set<int> attr_devices;  // devices whose dynamic shared-memory limit is raised
+    std::map<int, CUfunction> fn;  // per device: the kernel's function in that device's context
 };
+
+// Driver entry points for launching the library kernels as CUfunctions (cuLaunchKernel).
+struct Driver {
+    CUresult (*kernel_get_function)(CUfunction*, CUkernel) = nullptr;
+    CUresult (*func_set_attribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+    CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
+                       void**, void**) = nullptr;
+    bool ok = false;
+};
+const Driver& driver() {
+    static const Driver d = [] {
+        Driver r;
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q{};
+            if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+                cudaGetLastError();
+                *fn = nullptr;
+            }
+        };
+        get("cuKernelGetFunction", reinterpret_cast<void**>(&r.kernel_get_function));
+        get("cuFuncSetAttribute", reinterpret_cast<void**>(&r.func_set_attribute));
+        get("cuLaunchKernel", reinterpret_cast<void**>(&r.launch));
+        const char* v = std::getenv("QCS_JIT_LAUNCH");  // "rt": cudaLaunchKernel on the cudaKernel_t
+        r.ok = r.kernel_get_function && r.func_set_attribute && r.launch && !(v && !std::strcmp(v, "rt"));
+        return r;
+    }();
+    return d;
+}
+void cu_check(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) raise(QCS_ERR_CUDA, std::string(what) + " failed (CUresult " + std::to_string(int(r)) + ")");
+}
 
 std::mutex g_mu;
 std::map<std::string, std::unique_ptr<JitKernel>> g_cache;
@@ -461,10 +493,23 @@ bool launch_tile_pass_jit(double2* amps, const PassParams& p, unsigned F, const 
     int dev = 0;
     QCS_CUDA(cudaGetDevice(&dev));
     cudaKernel_t kern;
+    CUfunction fn = nullptr;
+    const Driver& drv = driver();
     {
         std::lock_guard<std::mutex> lk(g_mu);
         JitKernel& k = compile(src);
-        if (!k.attr_devices.count(dev)) {
+        if (drv.ok) {
+            auto it = k.fn.find(dev);
+            if (it == k.fn.end()) {
+                cu_check(drv.kernel_get_function(&fn, reinterpret_cast<CUkernel>(k.kernel)), "cuKernelGetFunction");
+                cu_check(drv.func_set_attribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, int(smem_max)),
+                         "cuFuncSetAttribute");
+                cu_check(drv.func_set_attribute(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100),
+                         "cuFuncSetAttribute");
+                it = k.fn.emplace(dev, fn).first;
+            }
+            fn = it->second;
+        } else if (!k.attr_devices.count(dev)) {
             QCS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k.kernel),
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)));
             QCS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k.kernel),
@@ -478,7 +523,8 @@ bool launch_tile_pass_jit(double2* amps, const PassParams& p, unsigned F, const 
     const void* f = flipped_dev;
     const void* tb = tables_dev;
     void* args[] = {&a, const_cast<PassParams*>(&p), &b, &f, &tb, const_cast<TmapParam*>(&tmap)};
-    QCS_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(kern), dim3(tiles), dim3(threads), args, smem, st));
+    if (fn) cu_check(drv.launch(fn, tiles, 1, 1, threads, 1, 1, unsigned(smem), st, args, nullptr), "cuLaunchKernel");
+    else QCS_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(kern), dim3(tiles), dim3(threads), args, smem, st));
     return true;
 }
 

@@ -142,8 +142,14 @@ struct RoundDesc {
     std::uint16_t op_begin, op_count;
 };
 
-constexpr int kPassMaxOps = 200;
-constexpr int kPassPool = 512;    // double2 slots for gate bundles (12 per bundle)
+#ifndef QCS_PASS_MAX_OPS
+#define QCS_PASS_MAX_OPS 200
+#endif
+constexpr int kPassMaxOps = QCS_PASS_MAX_OPS;
+#ifndef QCS_PASS_POOL
+#define QCS_PASS_POOL 512
+#endif
+constexpr int kPassPool = QCS_PASS_POOL;    // double2 slots for gate bundles (12 per bundle)
 enum : std::uint8_t { ALT_NONE = 0, ALT_ROUNDS = 1, ALT_SKIP = 2 };
 struct PassParams {           // <= 32 KB: the kernel parameter limit
     int m;                    // tile bits (3..12)
@@ -160,6 +166,8 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
     int nruns;                // the basis bits outside the tile, as runs: a tile index deposits into them
     std::uint8_t run_pos[16], run_len[16];
     std::uint32_t list_off, list_cnt;  // list_cnt > 0: run only these tiles (ALT_SKIP passes)
+    std::uint32_t init;       // 1: the pass starts from the basis state |init_index> instead of loading
+    std::uint64_t init_index;
     RoundDesc rounds[kPassMaxOps];
     RegOp ops[kPassMaxOps];
     double2 pool[kPassPool];

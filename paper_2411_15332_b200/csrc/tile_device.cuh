@@ -442,12 +442,29 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
         c.rb = P.alt_begin;
         c.re = c.rb + P.alt_nrounds;
     }
-    // TMA: the tile is one box of the host's tensor map over the state; the coordinates of the
-    // bit runs outside the tile come from the tile base (runs inside start at 0)
     for (int d = 0; d < 5; ++d) c.tc[d] = 0;
-    if (P.tma_rank) {
+    if (P.tma_rank)
         for (int d = 1; d < P.tma_rank; ++d)
             if (P.tma_gap_len[d]) c.tc[d] = int((base >> P.tma_gap_pos[d]) & ((u64(1) << P.tma_gap_len[d]) - 1));
+    if (P.init) {  // the pass starts from |init_index>: zeros and at most one 1, nothing to load
+        for (unsigned j = t; j < sz; j += bt) c.sm[j] = make_double2(0.0, 0.0);
+        cp_async_wait_all();  // the run-offset table
+        __syncthreads();
+        if (t == 0) {
+            u64 tile_mask = 0;
+            unsigned local = 0;
+            for (int b = 0; b < m; ++b) {
+                tile_mask |= u64(1) << P.bits[b];
+                local |= unsigned((P.init_index >> P.bits[b]) & 1) << b;
+            }
+            if ((P.init_index & ~tile_mask) == base) c.sm[swz(local)] = make_double2(1.0, 0.0);
+        }
+        __syncthreads();
+        return true;
+    }
+    // TMA: the tile is one box of the host's tensor map over the state; the coordinates of the
+    // bit runs outside the tile come from the tile base (runs inside start at 0)
+    if (P.tma_rank) {
         if (t == 0) {
             mbar_init(c.bar);
             mbar_expect_tx(c.bar, sz * 16u);

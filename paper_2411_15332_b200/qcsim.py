@@ -562,12 +562,11 @@ def simulate(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOptio
     c.validate()
     if state is None:
         state = DeviceState(c.n, c.initial, device)
-    else:
-        if state.n != c.n:
-            raise DimensionError("state qubit count mismatch")
-        state.set_basis(c.initial)
+    elif state.n != c.n:
+        raise DimensionError("state qubit count mismatch")
     arr, keep = _steps(c.steps)
-    o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)))
+    # reset: start from |initial> (folded into the first pass when it sweeps the whole state)
+    o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)), 1, int(c.initial))
     rep = (L.qcs_step_report * max(1, len(c.steps)))()
     _check(L.lib().qcs_simulate(state.handle, arr, len(c.steps), int(engine), C.byref(o), rep))
     steps = _reports(rep, len(c.steps))
