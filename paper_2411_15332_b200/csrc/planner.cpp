@@ -589,6 +589,28 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
         auto& cl = lists[std::size_t(carrier)];
         cl.insert(cl.begin(), add_op(make_scale(carry)));
     }
+    // scalars commute with everything: one scale per pass (the planner pulls every H^n step's
+    // 2^(-n/2) into the first pass, and the carried scalars join them)
+    for (std::size_t i = 0; i < np; ++i) {
+        int first = -1, count = 0;
+        double prod = 1.0;
+        for (std::size_t k = 0; k < lists[i].size(); ++k) {
+            const FOp& f = (extended ? ext : ops_in)[std::size_t(lists[i][k])];
+            if (f.kind != TOP_SCALE) continue;
+            if (first < 0) first = int(k);
+            prod *= f.scale;
+            ++count;
+        }
+        // (a pass of scales only stays as it is: as one operation it would leave the tile kernels)
+        if (count < 2 || count == int(lists[i].size()) || !std::isfinite(prod) || prod == 0.0) continue;
+        std::vector<int> keep;
+        for (std::size_t k = 0; k < lists[i].size(); ++k) {
+            const int idx = lists[i][k];
+            if (int(k) == first) keep.push_back(add_op(make_scale(prod)));
+            else if ((extended ? ext : ops_in)[std::size_t(idx)].kind != TOP_SCALE) keep.push_back(idx);
+        }
+        lists[i].swap(keep);
+    }
     const std::vector<FOp>& ops = extended ? ext : ops_in;
     for (std::size_t pi = 0; pi < np; ++pi) {
         const PlannedPass& pp = plan.passes[pi];
