@@ -58,9 +58,11 @@ bool knob_swaps() {
     return on;
 }
 
-bool has_pivot(const PassParams& p) {
-    for (int i = 0; i < p.nops; ++i)
-        if ((p.ops[i].kind & KF_KIND) == TOP_GATE && (p.ops[i].kind & KF_PIVOT)) return true;
+bool has_pivot(const PassParams& p) {  // pivoted gates or virtual permutations: specialised kernels only
+    for (int i = 0; i < p.nops; ++i) {
+        const int k = p.ops[i].kind & KF_KIND;
+        if ((k == TOP_GATE && (p.ops[i].kind & KF_PIVOT)) || k == TOP_PERM) return true;
+    }
     return false;
 }
 
@@ -114,11 +116,109 @@ void emit_gate(Out& o, int kb, int t, const double2* c, const std::string& coef,
     else if (en) o("      %s<%d, true>(v, %s, 0x%xu);\n", g, t, coef.c_str(), en);
 }
 
+// The layout relabelling of the virtual permutations (TOP_PERM): an affine map over GF(2) on
+// the local index bits, x -> A x ^ b (column i of A = the image of bit i).
+// Gates controlled only outside the tile add a term to the offset on the tiles where their
+// controls hold (a condition on the tile base, uniform over the CTA): `rt`.
+struct Affine {
+    unsigned col[16];
+    unsigned b = 0;
+    std::vector<std::pair<const RegOp*, unsigned>> rt;  // (op whose outside controls gate it, vector)
+    explicit Affine(int m) {
+        for (int i = 0; i < 16; ++i) col[i] = i < m ? 1u << i : 0u;
+    }
+    bool identity(int m) const {
+        for (int i = 0; i < m; ++i)
+            if (col[i] != 1u << i) return false;
+        return b == 0 && rt.empty();
+    }
+    std::string offset_expr() const {  // b and the runtime terms, as source
+        char buf[160];
+        std::snprintf(buf, sizeof(buf), "%uu", b);
+        std::string e = buf;
+        for (const auto& [op, v] : rt) {
+            std::snprintf(buf, sizeof(buf), " ^ (((base & 0x%llxull) == 0x%llxull) ? %uu : 0u)",
+                          (unsigned long long)op->gctrl_mask, (unsigned long long)op->gctrl_val, v);
+            e += buf;
+        }
+        return e;
+    }
+    unsigned apply(unsigned x) const {
+        unsigned y = b;
+        for (int i = 0; i < 16; ++i)
+            if (x >> i & 1) y ^= col[i];
+        return y;
+    }
+    // the permutation of an X-like gate: x -> x ^ (cond(x) ? e_t : 0), cond = (x & cm) == cv
+    // (cm at most one bit): linear part M = I + e_t e_c^T (with a control c), offset d
+    static void perm(const RegOp& op, unsigned& e_t, int& c, unsigned& d) {
+        e_t = 1u << op.t;
+        c = op.lctrl_mask ? __builtin_ctz(unsigned(op.lctrl_mask)) : -1;
+        d = (c < 0 || !(op.lctrl_val >> c & 1)) ? e_t : 0u;
+    }
+    void compose_right(const RegOp& op) {  // this <- this o pi (loads after the permutation)
+        unsigned e_t, d;
+        int c;
+        perm(op, e_t, c, d);
+        const unsigned colt = apply(e_t) ^ b;  // A e_t
+        if (op.gctrl_mask) {  // x ^ e_t on the tiles where the outside controls hold
+            rt.push_back({&op, colt});
+            return;
+        }
+        if (c >= 0) col[c] ^= colt;
+        b ^= apply(d) ^ b;  // A d
+    }
+    void compose_left(const RegOp& op) {  // this <- pi o this (stores of the permuted result)
+        unsigned e_t, d;
+        int c;
+        perm(op, e_t, c, d);
+        if (op.gctrl_mask) {
+            rt.push_back({&op, e_t});
+            return;
+        }
+        auto mul = [&](unsigned v) { return c >= 0 && (v >> c & 1) ? v ^ e_t : v; };
+        for (int i = 0; i < 16; ++i) col[i] = mul(col[i]);
+        for (auto& term : rt) term.second = mul(term.second);
+        b = mul(b) ^ d;
+    }
+};
+
+// source of A x (no offset) for the local group index `var` whose register bits are zero
+std::string affine_expr(const Affine& A, const char* var, unsigned regmask, int m) {
+    unsigned idmask = 0;
+    std::string e;
+    for (int i = 0; i < m; ++i) {
+        if (regmask >> i & 1) continue;
+        if (A.col[i] == 1u << i) {
+            idmask |= 1u << i;
+            continue;
+        }
+        char buf[96];
+        std::snprintf(buf, sizeof(buf), " ^ ((0u - ((%s >> %d) & 1u)) & %uu)", var, i, A.col[i]);
+        e += buf;
+    }
+    char head[64];
+    std::snprintf(head, sizeof(head), "(%s & %uu)", var, idmask);
+    return head + e;
+}
+
 // One register round: the interpreter's round loop (tile_kernels.cu) with every structural
 // field of the operations as a literal.  (16-amplitude rounds -- 4 register bits, 22% fewer
 // rounds for C4 -- were measured no faster at 2 resident tiles per SM and slower for C3.)
-void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) {
+// `map`: the layout relabelling so far (updated by the round's leading TOP_PERM ops); `last`:
+// the program's last round, which stores straight to HBM when the layout is not the identity
+// or trailing TOP_PERM ops permute its result.  Returns true when it did.
+bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, Affine& map, bool last) {
     const RoundDesc& R = P.rounds[ri];
+    int ob = R.op_begin, oe = R.op_begin + R.op_count;
+    while (ob < oe && (P.ops[ob].kind & KF_KIND) == TOP_PERM) map.compose_right(P.ops[ob++]);
+    Affine store(P.m);  // trailing permutations: where the round's (last) results go
+    int te = oe;
+    while (te > ob && (P.ops[te - 1].kind & KF_KIND) == TOP_PERM) --te;
+    for (int i = te; i < oe; ++i) store.compose_left(P.ops[i]);
+    if (te < oe && !last) raise(QCS_ERR_SIM, "internal: trailing relabelling outside a pass's last round");
+    const bool relabel = !map.identity(P.m);
+    const bool direct = last && (relabel || te < oe);
     constexpr int W = 3, G = 1 << W;
     const unsigned long long gmask = (1ull << G) - 1;
     const unsigned ngroups = (1u << P.m) >> W;
@@ -138,7 +238,7 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
     // bits 3..5 of the (swizzled) position; when those three bits do not map to 8 distinct
     // groups, swap one of them with a higher non-register bit that does (same groups, another
     // thread order: the accesses become conflict-free).
-    auto bank = [](int b) { return (b < 3 ? 1u << b : 0u) ^ (b >= 3 && b < 6 ? 1u << (b - 3) : 0u); };
+    auto bank = [&](int b) { const unsigned v = map.col[b]; return (v & 7u) ^ ((v >> 3) & 7u); };
     auto independent = [&](int a, int b, int c) {
         const unsigned x = bank(a), y = bank(b), z = bank(c);
         return x && y && z && x != y && x != z && y != z && (x ^ y) != z;
@@ -164,15 +264,22 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
     if (swap_a >= 0)
         o("      { const unsigned d = ((lb >> %d) ^ (lb >> %d)) & 1u; lb ^= (d << %d) | (d << %d); }\n", swap_a, swap_b,
           swap_a, swap_b);
-    o("      const unsigned slb = swz(lb);\n");
+    if (relabel)  // physical position of the group's first amplitude
+        o("      const unsigned slb = swz(%s ^ %s);\n", affine_expr(map, "lb", regmask, P.m).c_str(),
+          map.offset_expr().c_str());
+    else
+        o("      const unsigned slb = swz(lb);\n");
+    unsigned soff[16];
+    for (int q = 0; q < G; ++q) soff[q] = swz(map.apply(off[q]) ^ map.b);  // A off[q]
     o("      double2 v[%d];\n", G);
-    for (int q = 0; q < G; ++q) o("      v[%d] = sm[slb ^ %uu];\n", q, swz(off[q]));
+    for (int q = 0; q < G; ++q) o("      v[%d] = sm[slb ^ %uu];\n", q, soff[q]);
     o("      const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];\n");
     o("      unsigned negacc = 0;\n");
     o("      (void)g0; (void)negacc;\n");
-    for (int oi = R.op_begin; oi < R.op_begin + R.op_count; ++oi) {
+    for (int oi = ob; oi < te; ++oi) {
         const RegOp& op = P.ops[oi];
         const int kb = op.kind, kind = kb & KF_KIND;
+        if (kind == TOP_PERM) raise(QCS_ERR_SIM, "internal: relabelling inside a round");
         if (kb & KF_FLUSH) o("      flip_signs1(v, negacc);\n");
         const bool gc = kb & KF_GCTRL;
         if (gc) o("      if ((base & 0x%llxull) == 0x%llxull) {\n", (unsigned long long)op.gctrl_mask,
@@ -248,8 +355,20 @@ void emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads) 
         if (gc) o("      }\n");
     }
     if (R.flags & RD_SIGNS) o("      flip_signs1(v, negacc);\n");
-    for (int q = 0; q < G; ++q) o("      sm[slb ^ %uu] = v[%d];\n", swz(off[q]), q);
+    if (direct) {  // straight to HBM: logical index store(lb ^ off[q]) of the tile
+        o("      { const unsigned sd = %s ^ %s;\n", affine_expr(store, "lb", regmask, P.m).c_str(),
+          store.offset_expr().c_str());
+        o("        const u64 gs = base | hi_tab[sd >> 3];\n");
+        for (int q = 0; q < G; ++q) {
+            const unsigned cq = store.apply(off[q]) ^ store.b;  // A_s off[q]
+            o("        __stcs(a + (gs ^ u64((sd ^ %uu) & 7u) ^ hi_tab[%u]), v[%d]);\n", cq, cq >> 3, q);
+        }
+        o("      }\n    }\n  }\n");
+        return true;
+    }
+    for (int q = 0; q < G; ++q) o("      sm[slb ^ %uu] = v[%d];\n", soff[q], q);
     o("    }\n    __syncthreads();\n  }\n");
+    return false;
 }
 
 void emit_smem_round(Out& o, const PassParams& P, int ri, unsigned threads) {
@@ -265,11 +384,19 @@ void emit_smem_round(Out& o, const PassParams& P, int ri, unsigned threads) {
     o("  }\n");
 }
 
+// one program (the main rounds or the missed-tile alternative), then the tile's write-back
 void emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threads) {
+    Affine map(P.m);
+    bool direct = false;
     for (int ri = begin; ri < end; ++ri) {
-        if (P.rounds[ri].flags & RD_SMEM) emit_smem_round(o, P, ri, threads);
-        else emit_register_round(o, P, ri, threads);
+        if (P.rounds[ri].flags & RD_SMEM) {
+            if (!map.identity(P.m)) raise(QCS_ERR_SIM, "internal: shared-memory round after a relabelling");
+            emit_smem_round(o, P, ri, threads);
+        } else {
+            direct = emit_register_round(o, P, ri, threads, map, ri + 1 == end);
+        }
     }
+    if (!direct) o("  tile_end(a, P, tmap, c);\n");
 }
 
 std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
@@ -296,7 +423,7 @@ std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
     } else {
         emit_rounds(o, P, 0, P.nrounds, threads);
     }
-    o("  tile_end(a, P, tmap, c);\n}\n");
+    o("}\n");
     return o.s;
 }
 
@@ -422,6 +549,14 @@ int jit_mode() { return g_mode.load(std::memory_order_relaxed); }
 void set_jit_mode(int mode) {
     if (mode < 0 || mode > 3) raise(QCS_ERR_ARG, "jit mode must be 0, 1, 2 or 3");
     g_mode.store(mode);
+}
+
+bool jit_virtual(int n, int m, bool skip_pass) {
+    static const bool perms = [] { const char* v = std::getenv("QCS_JIT_PERMS"); return !v || std::atoi(v) != 0; }();
+    const int mode = jit_mode();
+    if (m < 3 || !perms) return false;
+    if (mode == 3) return true;
+    return mode == 1 && !skip_pass && n - m >= 11;  // big passes (>= 2048 tiles): specialised anyway
 }
 
 bool jit_pivot(int n, const PassParams& p) {

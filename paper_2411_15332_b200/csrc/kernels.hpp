@@ -63,6 +63,9 @@ enum TileOpKind : std::int32_t {
     TOP_SIGN = 2,    // diag sign step: flipped list (global memory) XOR flip_rest
     TOP_WHT = 3,     // unnormalised butterflies (a+b, a-b) over round bits (wht_mask)
     TOP_SCALE = 4,   // multiply by a real scalar (the RH magnitude, rh.cpp:99-100)
+    TOP_PERM = 6,    // specialised kernels only: a virtual X-like gate (target local bit t, at most one
+                     // control in lctrl): leading ops of a round relabel its loads, trailing ops of the
+                     // last round its stores
     TOP_DTAB = 5,    // register round: diagonal given per register, pool[ref + q] (q = 0..7); dskip bit q
                      // = entry q is exactly 1 (the round's diagonals on its register bits, combined)
 };
@@ -188,6 +191,7 @@ bool launch_tile_pass_jit(double2* amps, const struct PassParams& p, unsigned F,
                           unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st);
 int jit_mode();                      // 0 off, 1 passes with enough work (default), 2 every tile pass, 3 = 2 + pivots
 bool jit_pivot(int n, const struct PassParams& p);  // lower this pass's gates to the pivoted form
+bool jit_virtual(int n, int m, bool skip_pass);      // lower this pass's X-like gates to relabellings
 void set_jit_mode(int mode);
 std::size_t jit_compile_only(const struct PassParams& p);  // NVRTC only (no device): cubin bytes
 void tile_pass_shape(const struct PassParams& p, unsigned& F, unsigned& threads);  // kernel variant, CTA size

@@ -386,6 +386,11 @@ void pivot_pass(PassParams& P, int& npool) {
             ops.insert(ops.end(), rops.begin(), rops.end());
             continue;
         }
+        std::vector<RegOp> trailing;  // relabellings of the last round's stores stay last
+        while (!rops.empty() && (rops.back().kind & KF_KIND) == TOP_PERM) {
+            trailing.insert(trailing.begin(), rops.back());
+            rops.pop_back();
+        }
         unsigned regmask = 0;
         for (int i = 0; i < 3; ++i) regmask |= 1u << R.r[i];
         // the round's table: the existing one (the last operation) or a new one
@@ -478,6 +483,7 @@ void pivot_pass(PassParams& P, int& npool) {
             }
         }
         ops.insert(ops.end(), rops.begin(), rops.end());
+        ops.insert(ops.end(), trailing.begin(), trailing.end());
         R.op_count = std::uint16_t(ops.size() - R.op_begin);
     }
     if (int(ops.size()) > kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many operations in a pass");
@@ -624,16 +630,57 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             }
         int nops = 0, nsign = 0, npool = 0;
         std::uint64_t flip_off = 0, flip_cnt = 0;
+        const bool virt_pass = jit_virtual(n, P.m, has_alt[pi] && alts[pi].empty());
         // rounds of <= 3 register bits; gates on 2-3 targets get shared-memory rounds
         struct RoundPlan {
             bool smem;
             unsigned mask;
             std::vector<int> ops;
+            std::vector<int> perms;  // virtual permutations at the round's start (TOP_PERM)
+        };
+        // Virtual permutations (specialised kernels only): an X-like gate with at most one
+        // control, all in the tile, moves no data and needs no register bit -- it becomes a
+        // relabelling of the shared-memory addresses of the following rounds (an affine map over
+        // the local index bits), and at the pass end, if the layout is not the identity, the
+        // last round stores straight to HBM at the relabelled indices.  The gate is placed at a
+        // round boundary; operations after it join the current round only if they commute.
+        auto is_perm = [&](const FOp& f) {
+            if (f.kind != TOP_GATE || f.K != 1 || f.nrows != 2 || f.nnz[0] != 1 || f.nnz[1] != 1) return false;
+            if (!(f.val[0][0].x == 1.0 && f.val[0][0].y == 0.0 && f.val[1][0].x == 1.0 && f.val[1][0].y == 0.0 &&
+                  f.col_member[0][0] == 1 && f.col_member[1][0] == 0 && f.row_member[0] == 0 && f.row_member[1] == 1))
+                return false;
+            if (loc[f.tpos[0]] < 0) return false;
+            int inside = 0, outside = 0;
+            for (int b = 0; b < n; ++b)
+                if (f.ctrl_mask >> b & 1) ++(loc[b] >= 0 ? inside : outside);
+            // one control in the tile (a linear relabelling), or controls outside it only (a
+            // relabelling offset on the tiles where they hold)
+            return (inside <= 1 && outside == 0) || inside == 0;
         };
         auto lower_list = [&](const std::vector<FOp>& src, const std::vector<int>& list) {
         std::vector<RoundPlan> rounds;
+        bool virt = virt_pass;
+        for (int idx : list)  // shared-memory gate rounds address the tile directly: no relabelling
+            if (src[std::size_t(idx)].kind == TOP_GATE && src[std::size_t(idx)].K >= 2) virt = false;
+        std::vector<int> pending;  // virtual permutations after the current round's operations
+        u64 pending_touch = 0;
         for (int idx : list) {
             const FOp& f = src[std::size_t(idx)];
+            if (virt && is_perm(f)) {
+                pending.push_back(idx);
+                pending_touch |= f.touch;
+                continue;
+            }
+            if (!pending.empty() && (f.kind == TOP_SIGN || (f.touch & pending_touch) || rounds.empty())) {
+                // after the pending permutations: a new round whose loads apply them
+                unsigned t0 = 0;
+                if (!elementwise(f))
+                    for (int i = 0; i < f.K; ++i) t0 |= 1u << loc[f.tpos[i]];
+                rounds.push_back({false, t0, {idx}, pending});
+                pending.clear();
+                pending_touch = 0;
+                continue;
+            }
             const bool smem = f.kind == TOP_GATE && f.K >= 2;
             unsigned t = 0;
             if (!elementwise(f))
@@ -656,6 +703,10 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             } else {
                 rounds.push_back({false, t, {idx}});
             }
+        }
+        if (!pending.empty()) {  // permutations after the last operation: the last round's stores
+            if (rounds.empty()) rounds.push_back({false, 0u, {}, {}});
+            for (int idx : pending) rounds.back().ops.push_back(idx);  // trailing TOP_PERM ops
         }
         for (auto& r : rounds) {
             if (P.nrounds >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many rounds in a pass");
@@ -705,8 +756,33 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 seq = r.ops;
             }
             bool pending_signs = false;  // a +-1 diagonal since the last butterfly / gate
+            auto perm_op = [&](const FOp& f) {  // virtual permutation: target / control as local bits
+                if (nops >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many operations in a pass");
+                RegOp o{};
+                o.kind = TOP_PERM;
+                o.t = std::uint8_t(loc[f.tpos[0]]);
+                for (int b = 0; b < n; ++b) {
+                    if (!(f.ctrl_mask >> b & 1)) continue;
+                    const bool want = f.ctrl_val >> b & 1;
+                    if (loc[b] >= 0) {
+                        o.lctrl_mask = std::uint16_t(o.lctrl_mask | (1u << loc[b]));
+                        if (want) o.lctrl_val = std::uint16_t(o.lctrl_val | (1u << loc[b]));
+                    } else {
+                        o.gctrl_mask |= u64(1) << b;
+                        if (want) o.gctrl_val |= u64(1) << b;
+                    }
+                }
+                if (o.gctrl_mask) o.kind = std::uint8_t(o.kind | KF_GCTRL);
+                P.ops[nops++] = o;
+            };
+            for (int idx : r.perms) perm_op(src[std::size_t(idx)]);  // before the round's loads
+            std::vector<int> trailing;  // after the pass's last operations: the last round's stores
             for (int idx : seq) {
                 const FOp& f = src[std::size_t(idx)];
+                if (virt && is_perm(f)) {
+                    trailing.push_back(idx);
+                    continue;
+                }
                 if (nops >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many operations in a pass");
                 RegOp o{};
                 o.kind = std::uint8_t(f.kind);
@@ -906,6 +982,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 npool += 8;
                 P.ops[nops++] = o;
             }
+            for (int idx : trailing) perm_op(src[std::size_t(idx)]);
             rd.op_count = std::uint16_t(nops - rd.op_begin);
             if (pending_signs) rd.flags = std::uint8_t(rd.flags | RD_SIGNS);
         }
@@ -996,9 +1073,9 @@ void dump_pass(std::FILE* f, const PassParams& p, std::size_t nsrc) {
                      R.r[0], R.r[1], R.r[2]);
         for (int i = R.op_begin; i < R.op_begin + R.op_count; ++i) {
             const RegOp& o = p.ops[i];
-            static const char* names[] = {"G", "D", "SIGN", "WHT", "SC", "DTAB"};
+            static const char* names[] = {"G", "D", "SIGN", "WHT", "SC", "DTAB", "PERM"};
             const int k = o.kind & KF_KIND;
-            std::fprintf(f, " %s%s%s%s%s%s", k <= 5 ? names[k] : "?", (o.kind & KF_BUNDLE) ? "b" : "",
+            std::fprintf(f, " %s%s%s%s%s%s", k <= 6 ? names[k] : "?", (o.kind & KF_BUNDLE) ? "b" : "",
                          (o.kind & KF_SIGNED) ? "s" : "", (o.kind & KF_GCTRL) ? "g" : "", (o.kind & KF_FLUSH) ? "f" : "", (o.kind & KF_REAL) ? "r" : "");
             if (k == TOP_GATE || k == TOP_WHT) std::fprintf(f, "[t%d%s]", o.t, o.lctrl_mask ? " c" : "");
             if (k == TOP_DIAG) std::fprintf(f, "[dk%d r%d,%d]", o.dk, o.dreg[0] == 0xff ? -1 : o.dreg[0],

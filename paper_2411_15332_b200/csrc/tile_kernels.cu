@@ -373,8 +373,8 @@ void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev
         return;
     }
     for (int i = 0; i < p.nops; ++i)
-        if ((p.ops[i].kind & KF_KIND) == TOP_GATE && (p.ops[i].kind & KF_PIVOT))
-            raise(QCS_ERR_SIM, "internal: pivoted gates need the specialised kernel");
+        if (((p.ops[i].kind & KF_KIND) == TOP_GATE && (p.ops[i].kind & KF_PIVOT)) || (p.ops[i].kind & KF_KIND) == TOP_PERM)
+            raise(QCS_ERR_SIM, "internal: pivoted gates and relabellings need the specialised kernel");
     switch (f) {
 #define QCS_TILE_CASE(x) \
     case x: launch_f<x>(amps, p, big_dev, flipped_dev, unsigned(tiles), tables_dev, tmap, threads, smem, st); break;
