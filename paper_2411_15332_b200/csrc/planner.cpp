@@ -494,6 +494,50 @@ void pivot_pass(PassParams& P, int& npool) {
 
 }  // namespace
 
+namespace {
+
+// D' (y) = D (pi_k ( ... pi_1 (y))) for X-like relabellings pi_i (target t, controls in ctrl_mask:
+// y -> y ^ (cond(y) ? e_t : 0)), as a diagonal on the bits D's bits depend on; false when those
+// are more than three.
+template <class At>
+bool conjugate_diag(const FOp& d, const std::vector<int>& perms, At at, FOp& out) {
+    u64 dep[64];  // bits of y that bit b of pi_k(...pi_1(y)) depends on
+    for (int b = 0; b < 64; ++b) dep[b] = u64(1) << b;
+    for (int idx : perms) {  // (controls outside the tile make the diagonal depend on them: fine)
+        const FOp& p = at(idx);
+        const int t = p.tpos[0];
+        for (int b = 0; b < 64; ++b)
+            if (p.ctrl_mask >> b & 1) dep[t] |= dep[b];
+    }
+    u64 sup = 0;
+    for (int i = 0; i < d.dk; ++i) sup |= dep[d.dpos[i]];
+    const int k = __builtin_popcountll(sup);
+    if (k > 3 || k < 1) return false;
+    int pos[3], np = 0;  // ascending support positions
+    for (int b = 0; b < 64; ++b)
+        if (sup >> b & 1) pos[np++] = b;
+    GateOp g;
+    g.k = k;
+    for (int i = 0; i < k; ++i) g.pos[i] = pos[k - 1 - i];  // most significant first
+    const int dim = 1 << k;
+    g.m.assign(std::size_t(dim) * dim, cplx(0.0, 0.0));
+    for (int a = 0; a < dim; ++a) {
+        u64 y = 0;  // canonical local index a: bit k-1-i <-> pos[i] (most significant first)
+        for (int i = 0; i < k; ++i)
+            if (a >> (k - 1 - i) & 1) y |= u64(1) << g.pos[i];
+        for (int idx : perms) {
+            const FOp& p = at(idx);
+            if ((y & p.ctrl_mask) == p.ctrl_val) y ^= u64(1) << p.tpos[0];
+        }
+        int e = 0;
+        for (int i = 0; i < d.dk; ++i) e |= int((y >> d.dpos[i]) & 1) << (d.dk - 1 - i);
+        g.m[std::size_t(a) * dim + a] = cplx(d.dval[e].x, d.dval[e].y);
+    }
+    return make_fop(g, out) && out.kind == TOP_DIAG;
+}
+
+}  // namespace
+
 void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered& out) {
     out = Lowered{};
     // Missed-tile programs (tile-kernel passes of >= 2 operations).  One that is only a scalar
@@ -658,18 +702,36 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             return (inside <= 1 && outside == 0) || inside == 0;
         };
         auto lower_list = [&](const std::vector<FOp>& src, const std::vector<int>& list) {
+        // diagonals moved ahead of pending relabellings (conjugated): indices past src
+        std::vector<FOp> extra;
+        extra.reserve(list.size());
+        auto at = [&](int idx) -> const FOp& {
+            return idx < int(src.size()) ? src[std::size_t(idx)] : extra[std::size_t(idx) - src.size()];
+        };
         std::vector<RoundPlan> rounds;
         bool virt = virt_pass;
         for (int idx : list)  // shared-memory gate rounds address the tile directly: no relabelling
-            if (src[std::size_t(idx)].kind == TOP_GATE && src[std::size_t(idx)].K >= 2) virt = false;
+            if (at(idx).kind == TOP_GATE && at(idx).K >= 2) virt = false;
         std::vector<int> pending;  // virtual permutations after the current round's operations
         u64 pending_touch = 0;
         for (int idx : list) {
-            const FOp& f = src[std::size_t(idx)];
+            const FOp& f = at(idx);
             if (virt && is_perm(f)) {
                 pending.push_back(idx);
                 pending_touch |= f.touch;
                 continue;
+            }
+            if (!pending.empty() && f.kind == TOP_DIAG && (f.touch & pending_touch) && !rounds.empty() &&
+                !rounds.back().smem) {
+                // D after the pending relabellings pi_1..pi_k is D' = D o pi_k o ... o pi_1 before
+                // them: still diagonal, on the bits D's bits depend on through the relabellings
+                FOp g;
+                if (conjugate_diag(f, pending, at, g)) {
+                    extra.push_back(std::move(g));
+                    const int nidx = int(src.size() + extra.size()) - 1;
+                    rounds.back().ops.push_back(nidx);
+                    continue;
+                }
             }
             if (!pending.empty() && (f.kind == TOP_SIGN || (f.touch & pending_touch) || rounds.empty())) {
                 // after the pending permutations: a new round whose loads apply them
@@ -775,10 +837,10 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 if (o.gctrl_mask) o.kind = std::uint8_t(o.kind | KF_GCTRL);
                 P.ops[nops++] = o;
             };
-            for (int idx : r.perms) perm_op(src[std::size_t(idx)]);  // before the round's loads
+            for (int idx : r.perms) perm_op(at(idx));  // before the round's loads
             std::vector<int> trailing;  // after the pass's last operations: the last round's stores
             for (int idx : seq) {
-                const FOp& f = src[std::size_t(idx)];
+                const FOp& f = at(idx);
                 if (virt && is_perm(f)) {
                     trailing.push_back(idx);
                     continue;
@@ -971,7 +1033,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 for (int q = 0; q < 8; ++q) {
                     cplx t(1.0, 0.0);
                     for (int idx : tab) {
-                        const FOp& f = src[std::size_t(idx)];
+                        const FOp& f = at(idx);
                         int g = 0;
                         for (int i = 0; i < f.dk; ++i) g |= ((q >> reg(f.dpos[i])) & 1) << (f.dk - 1 - i);
                         if (!f.dskip[g]) t *= cplx(f.dval[g].x, f.dval[g].y);
@@ -982,7 +1044,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 npool += 8;
                 P.ops[nops++] = o;
             }
-            for (int idx : trailing) perm_op(src[std::size_t(idx)]);
+            for (int idx : trailing) perm_op(at(idx));
             rd.op_count = std::uint16_t(nops - rd.op_begin);
             if (pending_signs) rd.flags = std::uint8_t(rd.flags | RD_SIGNS);
         }
