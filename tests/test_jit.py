@@ -156,6 +156,19 @@ def test_pivoted_gates_against_oracle(Q, cfg, oracle):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(2))
+def test_default_mode_relabels_big_passes(Q, cfg, seed):
+    """At n = 23 (2048 tiles per pass) the default mode lowers X-like gates (X, CNOT, the X of Y)
+    to relabellings and conjugates later diagonals ahead of them: the C5 family and random
+    whole-catalog circuits (controls inside and outside the tile, reversed pairs) agree with the
+    interpreter, which the oracle checks elsewhere."""
+    c = cfg.c5_circuit(23, 4, global_qubits=2) if seed == 0 else random_catalog_circuit(Q, 7, 23, 30)
+    got, want = run_mode(Q, c, 1), run_mode(Q, c, 0)
+    assert np.abs(got - want).max() <= TOL_AMP
+    assert np.linalg.norm(got - want) <= TOL_L2
+
+
+@pytest.mark.gpu
 def test_default_mode_specialises_big_passes(Q, cfg):
     """At n = 22 the C4 passes (1024 tiles x >= 32 rounds) take the specialised kernels with
     pivoted gates in the default mode: within the bar of the (oracle-checked) interpreter."""
