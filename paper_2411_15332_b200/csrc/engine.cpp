@@ -113,6 +113,7 @@ qcs_state::~qcs_state() {
     if (timer) qcs::destroy_timer(timer);
     if (flip_buf) cudaFree(flip_buf);
     if (plan_buf) cudaFree(plan_buf);
+    qcs::delete_plan_cache(plan_cache);
     for (auto& st : stage) {
         if (st.host) cudaFreeHost(st.host);
         if (st.done) cudaEventDestroy(st.done);
@@ -270,13 +271,7 @@ void run_single(qcs_state* s, const FOp& f, const u64* flips_dev, u64 flip_cnt) 
     }
 }
 
-// Plan, lower, upload and launch a list of operations on the state.
-// init (>= 0): the state is to start from the basis state |init>; consumed (set to -1) by folding
-// it into the first pass when that pass writes every tile, else by a fill kernel first.
-void run_fused(qcs_state* s, const std::vector<FOp>& ops, std::int64_t* init = nullptr) {
-    if (ops.empty()) return;
-    const int n = s->n;
-    Lowered low;
+void plan_fused(int n, const std::vector<FOp>& ops, Lowered& low) {
     if (n >= 3) {
         lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
         jit_prepare(n, low.passes, low.pass_ops);
@@ -289,13 +284,22 @@ void run_fused(qcs_state* s, const std::vector<FOp>& ops, std::int64_t* init = n
             low.passes.emplace_back();
         }
     }
+}
+
+// Upload and launch a lowered plan on the state.  init (>= 0): the state is to start from the
+// basis state |init>; consumed (set to -1) by folding it into the first pass when that pass
+// writes every tile, else by a fill kernel first.  jit: per pass, the specialised kernel (kept by
+// cached plans); cached: the plan's identity, whose tables need no upload when plan_buf holds them.
+void execute_fused(qcs_state* s, const std::vector<FOp>& ops, Lowered& low, std::int64_t* init,
+                   std::vector<void*>* jit = nullptr, const void* cached = nullptr) {
+    const int n = s->n;
     // plan buffer: [TileOps | flip lists | u64 tables], 256-byte aligned sections
     const std::size_t bb = low.big.size() * sizeof(TileOp);
     const std::size_t fb = low.flips.size() * sizeof(u64);
     const std::size_t tb = low.tables.size() * sizeof(u64);
     const std::size_t f_off = (bb + 255) & ~std::size_t(255);
     const std::size_t t_off = (f_off + fb + 255) & ~std::size_t(255);
-    if (bb + fb + tb) {
+    if ((bb + fb + tb) && !(cached && s->plan_loaded == cached)) {
         const std::size_t bytes = t_off + tb;
         ensure_plan(s, bytes + 8);
         // stream order keeps the upload behind the previous plan's kernels; the pinned slot is
@@ -317,11 +321,13 @@ void run_fused(qcs_state* s, const std::vector<FOp>& ops, std::int64_t* init = n
         if (tb) std::memcpy(host + t_off, low.tables.data(), tb);
         QCS_CUDA(cudaMemcpyAsync(s->plan_buf, host, bytes, cudaMemcpyHostToDevice, s->stream));
         QCS_CUDA(cudaEventRecord(sg.done, s->stream));
+        s->plan_loaded = cached;
     }
     auto* base = static_cast<unsigned char*>(s->plan_buf);
     const auto* big_dev = reinterpret_cast<const TileOp*>(base);
     const auto* flips_dev = reinterpret_cast<const u64*>(base + f_off);
     const auto* tables_dev = reinterpret_cast<const u64*>(base + t_off);
+    if (!low.passes.empty()) low.passes[0].init = 0;
     if (init && *init >= 0) {
         const bool fold = !low.passes.empty() && low.pass_ops[0].size() >= 2 && n >= 3 && low.passes[0].list_cnt == 0 &&
                           low.passes[0].alt_mode != ALT_SKIP;
@@ -333,11 +339,21 @@ void run_fused(qcs_state* s, const std::vector<FOp>& ops, std::int64_t* init = n
         }
         *init = -1;
     }
+    if (jit && jit->size() != low.passes.size()) jit->assign(low.passes.size(), nullptr);
     for (std::size_t i = 0; i < low.passes.size(); ++i) {
         const auto& po = low.pass_ops[i];
         if (po.size() == 1) run_single(s, ops[std::size_t(po[0])], flips_dev + low.single_flip_off[i], low.single_flip_cnt[i]);
-        else launch_tile_pass(s->amps, n, low.passes[i], big_dev, flips_dev, tables_dev, s->stream);
+        else launch_tile_pass(s->amps, n, low.passes[i], big_dev, flips_dev, tables_dev, s->stream, jit ? &(*jit)[i] : nullptr);
     }
+}
+
+// Plan, lower, upload and launch a list of operations on the state.
+void run_fused(qcs_state* s, const std::vector<FOp>& ops, std::int64_t* init = nullptr) {
+    if (ops.empty()) return;
+    Lowered low;
+    plan_fused(s->n, ops, low);
+    s->plan_loaded = nullptr;
+    execute_fused(s, ops, low, init);
 }
 
 std::vector<FOp> rh_ops(int n) {
@@ -452,6 +468,67 @@ u64 rh_sign_count(int n, int method, u64 block) {
 
 }  // namespace
 
+struct CachedPlan {
+    std::vector<unsigned char> key;
+    std::vector<FOp> ops;
+    Lowered low;
+    std::vector<void*> jit;                 // per pass: its specialised kernel, once found
+    std::vector<qcs_step_report> reports;
+};
+
+struct PlanCache {
+    static constexpr std::size_t kEntries = 4;
+    std::vector<std::unique_ptr<CachedPlan>> entries;  // most recently used last
+    CachedPlan* find(const std::vector<unsigned char>& key) {
+        for (std::size_t i = 0; i < entries.size(); ++i)
+            if (entries[i]->key == key) {
+                std::rotate(entries.begin() + std::ptrdiff_t(i), entries.begin() + std::ptrdiff_t(i) + 1, entries.end());
+                return entries.back().get();
+            }
+        return nullptr;
+    }
+    CachedPlan& insert(std::unique_ptr<CachedPlan> p) {
+        if (entries.size() >= kEntries) entries.erase(entries.begin());
+        entries.push_back(std::move(p));
+        return *entries.back();
+    }
+};
+
+void delete_plan_cache(PlanCache* p) { delete p; }
+
+namespace {
+// everything the plan and the reports depend on, as bytes
+void plan_key(int n, int engine, const qcs_sim_options& o, const qcs_step* steps, int nsteps,
+              std::vector<unsigned char>& key) {
+    auto put = [&](const void* p, std::size_t b) {
+        const auto* c = static_cast<const unsigned char*>(p);
+        key.insert(key.end(), c, c + b);
+    };
+    const std::int64_t head[] = {n, engine, o.sign_method, std::int64_t(o.block_size), o.fuse, jit_mode(),
+                                 std::int64_t(dense_cap()), nsteps};
+    put(head, sizeof(head));
+    for (int i = 0; i < nsteps; ++i) {
+        const qcs_step& st = steps[i];
+        const std::int64_t sh[] = {st.kind, st.stage, st.flip_rest, std::int64_t(st.num_flipped), st.num_placements};
+        put(sh, sizeof(sh));
+        if (st.kind == QCS_STEP_DIAG) {
+            if (st.num_flipped) put(st.flipped, st.num_flipped * sizeof(u64));
+            continue;
+        }
+        for (int j = 0; j < st.num_placements; ++j) {
+            const qcs_placement& p = st.placements[j];
+            put(&p.arity, sizeof(p.arity));
+            put(p.qubits, sizeof(int) * std::size_t(p.arity));
+            put(p.matrix, sizeof(double) * 2 * (std::size_t(1) << (2 * p.arity)));
+            // the name selects RH dispatch ("Hadamard", circuit.cpp:31-39)
+            const std::size_t len = p.name ? std::strlen(p.name) : 0;
+            put(&len, sizeof(len));
+            if (len) put(p.name, len);
+        }
+    }
+}
+}  // namespace
+
 void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
               qcs_step_report* reports) {
     const int n = s->n;
@@ -464,6 +541,21 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
     DeviceGuard g(s->device);
     TimerScope ts(s);
     std::int64_t init = o.reset ? std::int64_t(o.initial) : -1;
+    // fused mode: a circuit simulated again on this state (same steps, engine, options) reuses
+    // its plan -- operations, lowered passes, reports, specialised kernels -- and, when the
+    // device plan buffer still holds its tables, their upload
+    std::vector<unsigned char> key;
+    if (o.fuse) {
+        plan_key(n, engine, o, steps, nsteps, key);
+        if (!s->plan_cache) s->plan_cache = new PlanCache;
+        if (CachedPlan* hit = s->plan_cache->find(key)) {
+            if (reports) std::copy(hit->reports.begin(), hit->reports.end(), reports);
+            execute_fused(s, hit->ops, hit->low, &init, &hit->jit, hit);
+            if (init >= 0) fill_basis(s->amps, dim, u64(init), s->stream);
+            return;
+        }
+    }
+    std::vector<qcs_step_report> reps(static_cast<std::size_t>(nsteps));
     std::vector<FOp> ops;  // fused mode: the whole circuit; stepwise: one step at a time
     for (int i = 0; i < nsteps; ++i) {
         const qcs_step& st = steps[i];
@@ -500,12 +592,21 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
             }
         }
         if (!o.fuse) run_fused(s, ops, &init);  // one step: fused only within the step
-        if (reports) reports[i] = r;
+        reps[std::size_t(i)] = r;
     }
+    if (reports) std::copy(reps.begin(), reps.end(), reports);
     if (o.fuse) {
         merge_single_qubit(n, ops);
         split_phases(ops);
-        run_fused(s, ops, &init);
+        if (!ops.empty()) {
+            auto cp = std::make_unique<CachedPlan>();
+            cp->key = std::move(key);
+            cp->ops = std::move(ops);
+            cp->reports = std::move(reps);
+            plan_fused(n, cp->ops, cp->low);
+            CachedPlan& e = s->plan_cache->insert(std::move(cp));
+            execute_fused(s, e.ops, e.low, &init, &e.jit, &e);
+        }
     }
     if (init >= 0) fill_basis(s->amps, dim, u64(init), s->stream);  // no operation at all
 }

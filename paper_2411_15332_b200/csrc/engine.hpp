@@ -7,7 +7,7 @@
 #include "common.hpp"
 #include "kernels.hpp"
 
-namespace qcs { struct LaunchTimer; }
+namespace qcs { struct LaunchTimer; struct PlanCache; }
 
 struct qcs_state {
     int n = 0;
@@ -29,6 +29,8 @@ struct qcs_state {
         cudaEvent_t done = nullptr;       // the upload from this slot has been read
     } stage[4];
     int stage_next = 0;
+    qcs::PlanCache* plan_cache = nullptr;   // recently simulated circuits: their lowered plans (engine.cpp)
+    const void* plan_loaded = nullptr;      // the cached plan whose tables plan_buf holds
     cudaEvent_t events[8] = {};
     qcs::LaunchTimer* timer = nullptr;   // per-launch timing (qcs_timing_enable)
     ~qcs_state();
@@ -37,6 +39,7 @@ struct qcs_state {
 namespace qcs {
 
 using u64 = std::uint64_t;
+void delete_plan_cache(PlanCache* p);
 
 // Make `dev` current for the lifetime of the guard.
 struct DeviceGuard {

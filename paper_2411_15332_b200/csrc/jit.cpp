@@ -622,9 +622,9 @@ std::size_t jit_compile_only(const PassParams& p) {
 
 bool launch_tile_pass_jit(double2* amps, const PassParams& p, unsigned F, const TileOp* big_dev,
                           const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, const TmapParam& tmap,
-                          unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st) {
-    if (!wanted(p, double(tiles))) return false;
-    const std::string src = pass_source(p, F, threads);
+                          unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st,
+                          void** jit_slot) {
+    if (!(jit_slot && *jit_slot) && !wanted(p, double(tiles))) return false;
     int dev = 0;
     QCS_CUDA(cudaGetDevice(&dev));
     cudaKernel_t kern;
@@ -632,7 +632,9 @@ bool launch_tile_pass_jit(double2* amps, const PassParams& p, unsigned F, const 
     const Driver& drv = driver();
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        JitKernel& k = compile(src);
+        // a plan the caller keeps remembers its kernel (no source generation on reuse)
+        JitKernel& k = jit_slot && *jit_slot ? *static_cast<JitKernel*>(*jit_slot) : compile(pass_source(p, F, threads));
+        if (jit_slot) *jit_slot = &k;
         if (drv.ok) {
             auto it = k.fn.find(dev);
             if (it == k.fn.end()) {

@@ -188,7 +188,8 @@ struct alignas(64) TmapParam {
 // worth a compile (or QCS_JIT=0), and the interpreter k_tile runs it.
 bool launch_tile_pass_jit(double2* amps, const struct PassParams& p, unsigned F, const struct TileOp* big_dev,
                           const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, const TmapParam& tmap,
-                          unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st);
+                          unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st,
+                          void** jit_slot = nullptr);
 int jit_mode();                      // 0 off, 1 passes with enough work (default), 2 every tile pass, 3 = 2 + pivots
 bool jit_pivot(int n, const struct PassParams& p);  // lower this pass's gates to the pivoted form
 bool jit_virtual(int n, int m, bool skip_pass);      // lower this pass's X-like gates to relabellings
@@ -200,8 +201,10 @@ unsigned long long jit_compiles();   // pass kernels compiled so far
 
 // tables_dev: the plan's u64 tables (Lowered::tables): run offsets and tile lists
 // sets p.tma_* for the launch
+// jit_slot (optional): the pass's specialised kernel, found once and kept by the caller's plan
 void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev,
-                      const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, cudaStream_t st);
+                      const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, cudaStream_t st,
+                      void** jit_slot = nullptr);
 int tile_max_bits();
 
 // A gate on a shard-global qubit over peer memory (peer_kernels.cu): blocks v (selected by the

@@ -355,7 +355,7 @@ void tile_pass_shape(const PassParams& p, unsigned& f, unsigned& threads) {
 }
 
 void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev, const std::uint64_t* flipped_dev,
-                      const std::uint64_t* tables_dev, cudaStream_t st) {
+                      const std::uint64_t* tables_dev, cudaStream_t st, void** jit_slot) {
     if (p.m < 3 || p.m > kMaxBits || p.m > n) raise(QCS_ERR_ARG, "tile bits out of range");
     const std::size_t smem = tile_smem(p.m);
     TmapParam tmap{};
@@ -368,7 +368,7 @@ void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev
     const int threads = int(nthreads);
     TimedLaunch tl("tile_pass", 32.0 * double(tiles) * double(1u << p.m), st);
     if (launch_tile_pass_jit(amps, p, f, big_dev, flipped_dev, tables_dev, tmap, unsigned(tiles), unsigned(threads), smem,
-                             tile_smem(kMaxBits), st)) {
+                             tile_smem(kMaxBits), st, jit_slot)) {
         check_launch("qcs_pass");
         return;
     }

@@ -161,3 +161,35 @@ def test_state_wait_orders_streams(Q, oracle):
     assert np.abs(a.download() - oracle.wht(n, want)).max() <= 1e-12
     a.close()
     b.close()
+
+
+def test_plan_cache_reuse_and_invalidation(Q, oracle):
+    """simulate() on the same state reuses a circuit's plan (and its uploaded tables) when the
+    steps repeat exactly; a changed angle, another circuit in between, or a new jit mode plans
+    afresh.  Every result against the oracle."""
+    n = 14
+    G = Q.gate_catalog_lookup
+
+    def circ(theta):
+        return Q.Circuit(n, [Q.hadamard_all(n), Q.CircuitStep.of_gates(
+            [Q.Placement(G("RY", [theta]), q) for q in range(n)]), Q.CircuitStep.of_gates(
+            [Q.Placement(G("Controlled-X"), q) for q in range(0, n - 1, 2)])], 3)
+
+    def want(c):
+        return oracle_run(oracle, c)
+
+    st = Q.DeviceState(n)
+    a, b = circ(0.3), circ(0.7)
+    wa, wb = want(a), want(b)
+    old = Q.jit_mode()
+    try:
+        for c, w in ((a, wa), (a, wa), (b, wb), (a, wa), (b, wb), (b, wb)):
+            rep = Q.simulate(c, Q.Engine.rh_dax, state=st)
+            assert np.abs(st.download() - w).max() <= TOL_AMP
+            assert len(rep.steps) == 3
+        Q.set_jit_mode(2 if old != 2 else 0)
+        Q.simulate(a, Q.Engine.rh_dax, state=st)
+        assert np.abs(st.download() - wa).max() <= TOL_AMP
+    finally:
+        Q.set_jit_mode(old)
+    st.close()
