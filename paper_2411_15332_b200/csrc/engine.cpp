@@ -271,7 +271,26 @@ void run_single(qcs_state* s, const FOp& f, const u64* flips_dev, u64 flip_cnt) 
     }
 }
 
+void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low);
+
 void plan_fused(int n, const std::vector<FOp>& ops, Lowered& low) {
+    plan_fused_passes(n, ops, low);
+    // support: from a basis state, an amplitude can only become nonzero by flipping bits that
+    // non-diagonal operations target (gates, butterflies); diagonals and scales never do
+    low.reached.assign(low.passes.size(), 0);
+    u64 reached = 0;
+    for (std::size_t i = 0; i < low.passes.size(); ++i) {
+        low.reached[i] = reached;
+        for (int idx : low.pass_ops[i]) {
+            if (idx >= int(ops.size())) continue;  // a scale the planner added
+            const FOp& f = ops[std::size_t(idx)];
+            if (f.diagonal) continue;
+            for (int k = 0; k < f.K; ++k) reached |= u64(1) << f.tpos[k];
+        }
+    }
+}
+
+void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low) {
     if (n >= 3) {
         lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
         jit_prepare(n, low.passes, low.pass_ops);
@@ -328,6 +347,17 @@ void execute_fused(qcs_state* s, const std::vector<FOp>& ops, Lowered& low, std:
     const auto* flips_dev = reinterpret_cast<const u64*>(base + f_off);
     const auto* tables_dev = reinterpret_cast<const u64*>(base + t_off);
     if (!low.passes.empty()) low.passes[0].init = 0;
+    // from a basis state: tiles outside the support reached before a pass are zero (no load)
+    const u64 full = n >= 64 ? ~u64(0) : (u64(1) << n) - 1;
+    for (std::size_t i = 0; i < low.passes.size() && n >= 3; ++i) {
+        PassParams& P = low.passes[i];
+        P.zmask = P.zval = 0;
+        if (!(init && *init >= 0) || low.pass_ops[i].size() < 2) continue;
+        u64 tile = 0;
+        for (int b = 0; b < P.m; ++b) tile |= u64(1) << P.bits[b];
+        P.zmask = full & ~tile & ~low.reached[i];
+        P.zval = u64(*init) & P.zmask;
+    }
     if (init && *init >= 0) {
         const bool fold = !low.passes.empty() && low.pass_ops[0].size() >= 2 && n >= 3 && low.passes[0].list_cnt == 0 &&
                           low.passes[0].alt_mode != ALT_SKIP;

@@ -171,6 +171,8 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
     std::uint32_t list_off, list_cnt;  // list_cnt > 0: run only these tiles (ALT_SKIP passes)
     std::uint32_t init;       // 1: the pass starts from the basis state |init_index> instead of loading
     std::uint64_t init_index;
+    std::uint64_t zmask, zval;  // tiles whose base bits under zmask differ from zval hold only zeros
+                                // (outside the support the circuit has reached): nothing to load
     RoundDesc rounds[kPassMaxOps];
     RegOp ops[kPassMaxOps];
     double2 pool[kPassPool];

@@ -63,6 +63,7 @@ struct Lowered {
     std::vector<u64> tables;                 // per pass: run offsets (PassParams::hi_off), tile lists
     std::vector<std::vector<int>> pass_ops;  // FOp indices per pass
     std::vector<u64> single_flip_off, single_flip_cnt;  // sign step of a single-op pass
+    std::vector<u64> reached;  // per pass: the bits operations before it may have changed (support)
 };
 void lower_plan(int n, const std::vector<FOp>& ops, const Plan& plan, Lowered& out);
 // compile (in parallel, NVRTC) the specialised kernels of the plan's passes that will use one (jit.cpp)

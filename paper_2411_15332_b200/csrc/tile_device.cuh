@@ -446,7 +446,9 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
     if (P.tma_rank)
         for (int d = 1; d < P.tma_rank; ++d)
             if (P.tma_gap_len[d]) c.tc[d] = int((base >> P.tma_gap_pos[d]) & ((u64(1) << P.tma_gap_len[d]) - 1));
-    if (P.init) {  // the pass starts from |init_index>: zeros and at most one 1, nothing to load
+    if (P.init || (P.zmask && (base & P.zmask) != P.zval)) {
+        // the pass starts from |init_index> (zeros and at most one 1), or from a tile the
+        // circuit has not reached yet (zeros): nothing to load
         for (unsigned j = t; j < sz; j += bt) c.sm[j] = make_double2(0.0, 0.0);
         cp_async_wait_all();  // the run-offset table
         __syncthreads();
@@ -457,7 +459,7 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
                 tile_mask |= u64(1) << P.bits[b];
                 local |= unsigned((P.init_index >> P.bits[b]) & 1) << b;
             }
-            if ((P.init_index & ~tile_mask) == base) c.sm[swz(local)] = make_double2(1.0, 0.0);
+            if (P.init && (P.init_index & ~tile_mask) == base) c.sm[swz(local)] = make_double2(1.0, 0.0);
         }
         __syncthreads();
         return true;

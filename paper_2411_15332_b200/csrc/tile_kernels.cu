@@ -31,6 +31,7 @@
 // 1e-12 bar and uses fused multiply-adds (half the FP64 instructions).  Passes of a single
 // operation never come here: the engine runs them with the bit-exact gate kernels.
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 
 #include <cuda.h>
@@ -366,7 +367,10 @@ void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev
     unsigned f = 0, nthreads = 0;
     tile_pass_shape(p, f, nthreads);
     const int threads = int(nthreads);
-    TimedLaunch tl("tile_pass", 32.0 * double(tiles) * double(1u << p.m), st);
+    // algorithmic bytes: every launched tile is written (16 B per amplitude) and read (16 B) unless
+    // it starts from the basis state or lies outside the support reached so far (zmask)
+    const double read_frac = p.init ? 0.0 : p.zmask ? std::ldexp(1.0, -__builtin_popcountll(p.zmask)) : 1.0;
+    TimedLaunch tl("tile_pass", 16.0 * (1.0 + read_frac) * double(tiles) * double(1u << p.m), st);
     if (launch_tile_pass_jit(amps, p, f, big_dev, flipped_dev, tables_dev, tmap, unsigned(tiles), unsigned(threads), smem,
                              tile_smem(kMaxBits), st, jit_slot)) {
         check_launch("qcs_pass");
