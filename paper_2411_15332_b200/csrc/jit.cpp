@@ -58,6 +58,11 @@ bool knob_swaps() {
     return on;
 }
 
+// a non-signed diagonal whose phase bits are all constant over a register group (dk <= 2)
+bool group_const(const RegOp& op) {
+    return op.dk >= 1 && op.dk <= 2 && op.dreg[0] == 0xff && (op.dk == 1 || op.dreg[1] == 0xff);
+}
+
 bool has_pivot(const PassParams& p) {  // pivoted gates or virtual permutations: specialised kernels only
     for (int i = 0; i < p.nops; ++i) {
         const int k = p.ops[i].kind & KF_KIND;
@@ -275,6 +280,14 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
     for (int q = 0; q < G; ++q) o("      v[%d] = sm[slb ^ %uu];\n", q, soff[q]);
     o("      const u64 g0 = base | (lb & 7u) | hi_tab[lb >> 3];\n");
     o("      unsigned negacc = 0;\n");
+    // phases constant over a group (diagonals on bits outside the registers) multiply into one
+    // scalar per group when a round has several -- passes that pivot their gates only (a
+    // different rounding; the pivot-free passes stay value-identical to the interpreter)
+    int nconst = 0;
+    for (int oi = ob; oi < te; ++oi)
+        if ((P.ops[oi].kind & KF_KIND) == TOP_DIAG && !(P.ops[oi].kind & KF_SIGNED) && group_const(P.ops[oi])) ++nconst;
+    const bool accumulate = nconst >= 2 && has_pivot(P);
+    if (accumulate) o("      double2 gs = make_double2(1.0, 0.0);\n");
     o("      (void)g0; (void)negacc;\n");
     for (int oi = ob; oi < te; ++oi) {
         const RegOp& op = P.ops[oi];
@@ -327,6 +340,19 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
                 else
                     o("      v[%d] = cmul_f(P.pool[%d], v[%d]);\n", q, op.ref + q, q);
             }
+        } else if (kind == TOP_DIAG && accumulate && group_const(op)) {
+            // a phase constant over the group: into the group's scalar, applied once at the end
+            if (op.dk == 1) {
+                o("      { const int g = int((g0 >> %d) & 1);\n", op.dpos[0]);
+                o("        if (!((%uu >> g) & 1u)) gs = cmul_f(g ? P.ops[%d].c[1] : P.ops[%d].c[0], gs); }\n",
+                  unsigned(op.dskip), oi, oi);
+            } else {
+                o("      { const int g = (int((g0 >> %d) & 1) << 1) | int((g0 >> %d) & 1);\n", op.dpos[0], op.dpos[1]);
+                o("        if (!((%uu >> g) & 1u)) { double2 d = P.ops[%d].c[0]; if (g == 1) d = P.ops[%d].c[1];\n",
+                  unsigned(op.dskip), oi, oi);
+                o("          if (g == 2) d = P.ops[%d].c[2]; if (g == 3) d = P.ops[%d].c[3]; gs = cmul_f(d, gs); } }\n", oi,
+                  oi);
+            }
         } else if (kind == TOP_DIAG) {
             if (op.dk == 1 && op.dreg[0] == 0xff) {
                 o("      { const int g = int((g0 >> %d) & 1);\n", op.dpos[0]);
@@ -354,6 +380,8 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
         }
         if (gc) o("      }\n");
     }
+    if (accumulate)
+        for (int q = 0; q < G; ++q) o("      v[%d] = cmul_f(gs, v[%d]);\n", q, q);
     if (R.flags & RD_SIGNS) o("      flip_signs1(v, negacc);\n");
     if (direct) {  // straight to HBM: logical index store(lb ^ off[q]) of the tile
         o("      { const unsigned sd = %s ^ %s;\n", affine_expr(store, "lb", regmask, P.m).c_str(),
