@@ -361,6 +361,20 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
                 o("          for (int q = 0; q < %d; ++q) v[q] = cmul_f(d, v[q]); } }\n", G);
             } else if (op.dk == 1) {
                 o("      diag_reg<%d>(v, P.ops[%d].c[0], P.ops[%d].c[1], %uu);\n", op.dreg[0], oi, oi, unsigned(op.dskip));
+            } else if (op.dk == 2 && has_pivot(P) && ((op.dreg[0] == 0xff) != (op.dreg[1] == 0xff))) {
+                // one register bit and one bit constant over the group: two entries per group, a
+                // static choice per register (no per-register selection)
+                const int ci = op.dreg[0] == 0xff ? 0 : 1, ri = 1 - ci, rb = op.dreg[ri];
+                auto entry = [&](int rv, const char* cb) {  // source of the entry for register-bit value rv
+                    char buf[96];
+                    if (ri == 0) std::snprintf(buf, sizeof(buf), "P.ops[%d].c[%d | %s]", oi, rv << 1, cb);
+                    else std::snprintf(buf, sizeof(buf), "P.ops[%d].c[(%s << 1) | %d]", oi, cb, rv);
+                    return std::string(buf);
+                };
+                o("      { const int cb = int((g0 >> %d) & 1);\n", op.dpos[ci]);
+                o("        const double2 e0 = %s, e1 = %s;\n", entry(0, "cb").c_str(), entry(1, "cb").c_str());
+                for (int q = 0; q < G; ++q) o("        v[%d] = cmul_f(e%d, v[%d]);\n", q, (q >> rb) & 1, q);
+                o("      }\n");
             } else {
                 o("      diag_op(v, P.ops[%d], big, g0);\n", oi);
             }
