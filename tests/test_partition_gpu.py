@@ -61,6 +61,36 @@ def test_emulated_peer_gates_match_single_gpu(world):
         assert all(o[0].splits > 0 for o in outs)
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_emulated_ranks_specialised_kernels(world):
+    """The same sharded circuits with every local pass as a specialised kernel (jit mode 3:
+    pivoted gates, relabellings, group scalars), against the single-GPU interpreter."""
+    from paper_2411_15332_b200 import configs
+    from paper_2411_15332_b200 import qcsim as Q
+    from paper_2411_15332_b200.partition import DeviceBackend, ShardedState
+    g = world.bit_length() - 1
+    old = Q.jit_mode()
+    try:
+        for c in (configs.c4_circuit(n=16, layers=2), configs.c5_circuit(n=17, layers=2, global_qubits=g)):
+            Q.set_jit_mode(0)
+            want = Q.simulate(c, Q.Engine.rh_dax).final.download()
+            Q.set_jit_mode(3)
+            hub = ThreadTransport()
+
+            def rank_fn(r):
+                st = ShardedState(c.n, world, r, DeviceBackend(c.n - g), hub.endpoint(r), initial=c.initial,
+                                  chunk_elems=1 << 12)
+                run_ops(st, circuit_ops(c))
+                return st, st.local_numpy()
+
+            outs = run_ranks(world, rank_fn)
+            got = gather([o[0] for o in outs], [o[1] for o in outs])
+            assert np.abs(got - want).max() < 1e-12
+            assert np.linalg.norm(got - want) < 1e-10
+    finally:
+        Q.set_jit_mode(old)
+
+
 def test_split_gate_bit_exact():
     """One gate on a global qubit through qcs_apply_split equals the single-GPU gate kernel
     bit for bit (both follow dax_mvm's arithmetic)."""
