@@ -89,7 +89,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         raise RuntimeError(f"nvcc failed:\n{msg}")
     cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
     link = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-Xcompiler", "-fPIC", "-lnvrtc", "-L" + cudalib,
-            "-Xlinker", "-rpath=" + cudalib]
+            "-Xlinker", "-rpath=" + cudalib] + os.environ.get("QCS_EXTRA_LINK", "").split()
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.run(link, check=True)

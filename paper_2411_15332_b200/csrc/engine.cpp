@@ -358,8 +358,28 @@ void execute_fused(qcs_state* s, const std::vector<FOp>& ops, Lowered& low, std:
         P.zmask = full & ~tile & ~low.reached[i];
         P.zval = u64(*init) & P.zmask;
     }
+    // a tile that is zero after this pass and that the next pass (running every tile) reads as
+    // zero need not be written at all
+    static const bool no_skip = std::getenv("QCS_NO_TILE_SKIP") != nullptr;  // A/B switch
+    static const bool no_zero = std::getenv("QCS_NO_ZERO_INPUT") != nullptr;
+    if (no_zero)
+        for (auto& P : low.passes) P.zmask = P.zval = 0;
+    for (std::size_t i = 0; i + 1 < low.passes.size() && n >= 3 && !no_skip; ++i) {
+        PassParams& P = low.passes[i];
+        const PassParams& Q = low.passes[i + 1];
+        P.smask = P.sval = 0;
+        if (!Q.zmask || low.pass_ops[i].size() < 2 || low.pass_ops[i + 1].size() < 2 || Q.list_cnt ||
+            Q.alt_mode == ALT_SKIP)
+            continue;
+        u64 tile = 0;
+        for (int b = 0; b < P.m; ++b) tile |= u64(1) << P.bits[b];
+        P.smask = Q.zmask & ~tile;
+        P.sval = Q.zval & ~tile;
+    }
+    if (!low.passes.empty()) low.passes.back().smask = low.passes.back().sval = 0;
+    static const bool no_fold = std::getenv("QCS_NO_INIT_FOLD") != nullptr;  // A/B switch
     if (init && *init >= 0) {
-        const bool fold = !low.passes.empty() && low.pass_ops[0].size() >= 2 && n >= 3 && low.passes[0].list_cnt == 0 &&
+        const bool fold = !no_fold && !low.passes.empty() && low.pass_ops[0].size() >= 2 && n >= 3 && low.passes[0].list_cnt == 0 &&
                           low.passes[0].alt_mode != ALT_SKIP;
         if (fold) {
             low.passes[0].init = 1;
@@ -575,7 +595,8 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
     // its plan -- operations, lowered passes, reports, specialised kernels -- and, when the
     // device plan buffer still holds its tables, their upload
     std::vector<unsigned char> key;
-    if (o.fuse) {
+    static const bool no_cache = std::getenv("QCS_NO_PLAN_CACHE") != nullptr;  // A/B switch
+    if (o.fuse && !no_cache) {
         plan_key(n, engine, o, steps, nsteps, key);
         if (!s->plan_cache) s->plan_cache = new PlanCache;
         if (CachedPlan* hit = s->plan_cache->find(key)) {
@@ -628,7 +649,9 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
     if (o.fuse) {
         merge_single_qubit(n, ops);
         split_phases(ops);
-        if (!ops.empty()) {
+        if (!ops.empty() && no_cache) {
+            run_fused(s, ops, &init);
+        } else if (!ops.empty()) {
             auto cp = std::make_unique<CachedPlan>();
             cp->key = std::move(key);
             cp->ops = std::move(ops);

@@ -643,7 +643,8 @@ void jit_prepare(int n, const std::vector<PassParams>& passes, const std::vector
             }
         }
     };
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    static const unsigned threads_env = [] { const char* v = std::getenv("QCS_JIT_THREADS"); return v ? unsigned(std::atoi(v)) : 0u; }();
+    const unsigned hw = threads_env ? threads_env : std::max(1u, std::thread::hardware_concurrency());
     const std::size_t nthreads = std::min<std::size_t>(todo.size(), std::min(hw, 32u));
     std::vector<std::thread> pool;
     for (std::size_t i = 1; i < nthreads; ++i) pool.emplace_back(worker);

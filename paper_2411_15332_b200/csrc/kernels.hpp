@@ -173,6 +173,8 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
     std::uint64_t init_index;
     std::uint64_t zmask, zval;  // tiles whose base bits under zmask differ from zval hold only zeros
                                 // (outside the support the circuit has reached): nothing to load
+    std::uint64_t smask, sval;  // tiles whose base bits under smask differ from sval are skipped: zero
+                                // and read as zero by the next pass (its zmask), nothing to write
     RoundDesc rounds[kPassMaxOps];
     RegOp ops[kPassMaxOps];
     double2 pool[kPassPool];

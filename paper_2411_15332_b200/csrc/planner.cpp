@@ -721,7 +721,8 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 pending_touch |= f.touch;
                 continue;
             }
-            if (!pending.empty() && f.kind == TOP_DIAG && (f.touch & pending_touch) && !rounds.empty() &&
+            static const bool no_conj = std::getenv("QCS_NO_CONJ") != nullptr;  // A/B switch
+            if (!no_conj && !pending.empty() && f.kind == TOP_DIAG && (f.touch & pending_touch) && !rounds.empty() &&
                 !rounds.back().smem) {
                 // D after the pending relabellings pi_1..pi_k is D' = D o pi_k o ... o pi_1 before
                 // them: still diagonal, on the bits D's bits depend on through the relabellings
@@ -794,7 +795,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             std::vector<int> seq, tab;
             if (!r.smem) {
                 for (std::size_t i = 0; i < r.ops.size(); ++i) {
-                    const FOp& f = src[std::size_t(r.ops[i])];
+                    const FOp& f = at(r.ops[i]);
                     bool movable = !kNoTables && f.kind == TOP_DIAG && npool + 8 <= kPassPool - 12;
                     for (int j = 0; movable && j < f.dk; ++j) movable = loc[f.dpos[j]] >= 0 && reg(f.dpos[j]) >= 0;
                     if (movable) {  // +-1 diagonals stay pending sign flips (cheaper)
@@ -806,7 +807,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                         movable = !signed_only;
                     }
                     for (std::size_t j = i + 1; movable && j < r.ops.size(); ++j) {
-                        const FOp& g = src[std::size_t(r.ops[j])];
+                        const FOp& g = at(r.ops[j]);
                         if (g.kind != TOP_GATE && g.kind != TOP_WHT) continue;
                         u64 tg = 0;
                         for (int k = 0; k < g.K; ++k) tg |= u64(1) << g.tpos[k];

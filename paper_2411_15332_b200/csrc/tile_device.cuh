@@ -408,7 +408,6 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
     c.hi_tab = reinterpret_cast<u64*>(c.sm + sz);
     c.bar = reinterpret_cast<unsigned long long*>(c.hi_tab + (ngroups < 2 ? 2 : ngroups));
     const unsigned t = threadIdx.x, bt = blockDim.x;
-    for (unsigned j = 2 * t; j < ngroups; j += 2 * bt) cp_async16(c.hi_tab + j, tables + P.hi_off + j);
     // basis offset of the tile: its index deposited into the bits outside the tile (host-listed runs)
     u64 base = 0;
     {
@@ -419,6 +418,9 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
         }
     }
     c.base = base;
+    // zero, and the next pass reads it as zero: nothing to do (before any asynchronous copy)
+    if (P.smask && (base & P.smask) != P.sval) return false;
+    for (unsigned j = 2 * t; j < ngroups; j += 2 * bt) cp_async16(c.hi_tab + j, tables + P.hi_off + j);
     // sign steps whose listed indices miss this tile act uniformly (negate all or nothing):
     // decide that once per tile
     c.sign_hit = 0;
@@ -438,7 +440,10 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
     c.rb = 0;
     c.re = P.nrounds;
     if ((F & F_SIGN) && P.alt_mode != ALT_NONE && c.sign_hit == 0) {
-        if (P.alt_mode == ALT_SKIP) return false;  // the pass is the identity here: no HBM traffic
+        if (P.alt_mode == ALT_SKIP) {  // the pass is the identity here: no HBM traffic
+            cp_async_wait_all();         // (no copy may land after the CTA exits)
+            return false;
+        }
         c.rb = P.alt_begin;
         c.re = c.rb + P.alt_nrounds;
     }

@@ -370,7 +370,8 @@ void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev
     // algorithmic bytes: every launched tile is written (16 B per amplitude) and read (16 B) unless
     // it starts from the basis state or lies outside the support reached so far (zmask)
     const double read_frac = p.init ? 0.0 : p.zmask ? std::ldexp(1.0, -__builtin_popcountll(p.zmask)) : 1.0;
-    TimedLaunch tl("tile_pass", 16.0 * (1.0 + read_frac) * double(tiles) * double(1u << p.m), st);
+    const double active = p.smask ? std::ldexp(1.0, -__builtin_popcountll(p.smask)) : 1.0;  // not skipped
+    TimedLaunch tl("tile_pass", 16.0 * active * (1.0 + read_frac) * double(tiles) * double(1u << p.m), st);
     if (launch_tile_pass_jit(amps, p, f, big_dev, flipped_dev, tables_dev, tmap, unsigned(tiles), unsigned(threads), smem,
                              tile_smem(kMaxBits), st, jit_slot)) {
         check_launch("qcs_pass");
