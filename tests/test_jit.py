@@ -71,6 +71,21 @@ def test_generated_sources_compile(Q, cfg):
         assert r["cubin_bytes"] > 0
 
 
+def test_plans_do_not_depend_on_history(Q, cfg):
+    """The same circuit plans the same way whatever was planned before (a read past the
+    operation list once made relabelled plans depend on heap contents)."""
+    old = Q.jit_mode()
+    try:
+        Q.set_jit_mode(3)
+        c = cfg.c5_circuit(15, 3, global_qubits=2)
+        first = Q.plan_stats(c)
+        for other in (random_catalog_circuit(Q, 0, 13), sign_sandwich(Q, 15), cfg.c4_circuit(11, 3)):
+            Q.plan_stats(other)
+            assert Q.plan_stats(c) == first
+    finally:
+        Q.set_jit_mode(old)
+
+
 def test_jit_mode_switch(Q):
     old = Q.jit_mode()
     try:
