@@ -236,8 +236,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
     auto swz = [](unsigned j) { return j ^ ((j >> 3) & 7u); };
     o("  {  // round %d: register bits", ri);
     for (int i = 0; i < W; ++i) o(" %d", R.r[i]);
-    o("\n#pragma unroll %d\n", knob_unroll());
-    o("    for (unsigned gb = t; gb < %uu; gb += %uu) {\n", ngroups, threads);
+    o("\n");
     // Thread order: the 8 threads of one 16-byte shared-memory phase differ in gb's low 3 bits,
     // i.e. in the round's lowest 3 non-register tile bits.  Their bank group is bits 0..2 XOR
     // bits 3..5 of the (swizzled) position; when those three bits do not map to 8 distinct
@@ -263,17 +262,51 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
                 }
             }
     }
-    std::string lbx = "gb";
+    // The group index lb = S(D(gb)) (D: zeros inserted at the register bits, S: the swap) and
+    // its relabelled position are linear in gb, and gb = t + k * threads: the thread's part is
+    // computed once per round, each iteration adds a constant.
+    auto deposit = [&](unsigned g) {
+        for (int i = 0; i < W; ++i) g = ((g >> R.r[i]) << (R.r[i] + 1)) | (g & ((1u << R.r[i]) - 1));
+        if (swap_a >= 0 && ((g >> swap_a) ^ (g >> swap_b)) & 1u) g ^= (1u << swap_a) | (1u << swap_b);
+        return g;
+    };
+    const unsigned iters = ngroups > threads ? ngroups / threads : 1u;
+    std::vector<unsigned> lk, pk, sk;  // per bit j of k: lb, A lb and A_s lb of k = 2^j
+    for (unsigned j = 0; (1u << j) < iters; ++j) {
+        const unsigned l = deposit(threads << j);
+        lk.push_back(l);
+        pk.push_back(map.apply(l) ^ map.b);
+        sk.push_back(store.apply(l) ^ store.b);
+    }
+    auto kexpr = [&](const std::vector<unsigned>& v) {
+        std::string e = "0u";
+        char buf[96];
+        for (std::size_t j = 0; j < v.size(); ++j) {
+            std::snprintf(buf, sizeof(buf), " ^ ((0u - ((k >> %zu) & 1u)) & %uu)", j, v[j]);
+            e += buf;
+        }
+        return e;
+    };
+    std::string lbx = "t";
     for (int i = 0; i < W; ++i) lbx = "insert_zero(" + lbx + ", " + std::to_string(R.r[i]) + ")";
-    o("      %sunsigned lb = %s;\n", swap_a < 0 ? "const " : "", lbx.c_str());
+    o("    unsigned lb_t = %s;\n", lbx.c_str());
     if (swap_a >= 0)
-        o("      { const unsigned d = ((lb >> %d) ^ (lb >> %d)) & 1u; lb ^= (d << %d) | (d << %d); }\n", swap_a, swap_b,
-          swap_a, swap_b);
-    if (relabel)  // physical position of the group's first amplitude
-        o("      const unsigned slb = swz(%s ^ %s);\n", affine_expr(map, "lb", regmask, P.m).c_str(),
+        o("    { const unsigned d = ((lb_t >> %d) ^ (lb_t >> %d)) & 1u; lb_t ^= (d << %d) | (d << %d); }\n", swap_a,
+          swap_b, swap_a, swap_b);
+    if (relabel)
+        o("    const unsigned pl_t = %s ^ %s;\n", affine_expr(map, "lb_t", regmask, P.m).c_str(),
           map.offset_expr().c_str());
     else
-        o("      const unsigned slb = swz(lb);\n");
+        o("    const unsigned pl_t = lb_t;\n");
+    if (direct)
+        o("    const unsigned sd_t = %s ^ %s;\n", affine_expr(store, "lb_t", regmask, P.m).c_str(),
+          store.offset_expr().c_str());
+    if (threads > ngroups) o("    if (t < %uu)\n", ngroups);
+    o("#pragma unroll %d\n", knob_unroll());
+    o("    for (unsigned k = 0; k < %uu; ++k) {\n", iters);
+    o("      const unsigned lb = lb_t ^ %s;\n", kexpr(lk).c_str());
+    o("      const unsigned slb = swz(pl_t ^ %s);  // physical position of the group's first amplitude\n",
+      kexpr(pk).c_str());
     unsigned soff[16];
     for (int q = 0; q < G; ++q) soff[q] = swz(map.apply(off[q]) ^ map.b);  // A off[q]
     o("      double2 v[%d];\n", G);
@@ -398,8 +431,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
         for (int q = 0; q < G; ++q) o("      v[%d] = cmul_f(gs, v[%d]);\n", q, q);
     if (R.flags & RD_SIGNS) o("      flip_signs1(v, negacc);\n");
     if (direct) {  // straight to HBM: logical index store(lb ^ off[q]) of the tile
-        o("      { const unsigned sd = %s ^ %s;\n", affine_expr(store, "lb", regmask, P.m).c_str(),
-          store.offset_expr().c_str());
+        o("      { const unsigned sd = sd_t ^ %s;\n", kexpr(sk).c_str());
         o("        const u64 gs = base | hi_tab[sd >> 3];\n");
         for (int q = 0; q < G; ++q) {
             const unsigned cq = store.apply(off[q]) ^ store.b;  // A_s off[q]
