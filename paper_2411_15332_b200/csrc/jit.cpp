@@ -18,6 +18,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -547,7 +548,56 @@ std::mutex g_mu;
 std::map<std::string, std::unique_ptr<JitKernel>> g_cache;
 std::atomic<unsigned long long> g_compiles{0};
 
+std::vector<char> nvrtc_cubin(const std::string& src);
+
+// Optional on-disk cache of compiled pass kernels (QCS_JIT_CACHE=<directory>): a kernel's cubin
+// is stored with its full source (the key is the complete text: headers, options, generated
+// code), so a later process reuses it instead of compiling.  Off by default.
+std::string full_key(const std::string& src) {
+    int major = 0, minor = 0;
+    nvrtcVersion(&major, &minor);
+    return std::string(kJitSrcKernels) + kJitSrcDevice + "\n// nvrtc " + std::to_string(major) + "." +
+           std::to_string(minor) + " sm_100a\n" + src;
+}
+
 std::vector<char> compile_cubin(const std::string& src) {
+    static const char* dir = std::getenv("QCS_JIT_CACHE");
+    if (!dir || !*dir) return nvrtc_cubin(src);
+    const std::string key = full_key(src);
+    std::uint64_t h = 1469598103934665603ull;  // FNV-1a
+    for (unsigned char ch : key) h = (h ^ ch) * 1099511628211ull;
+    char name[32];
+    std::snprintf(name, sizeof(name), "%016llx", (unsigned long long)h);
+    const std::string base = std::string(dir) + "/qcs_" + name;
+    auto read = [](const std::string& path, std::string& out) {
+        std::FILE* f = std::fopen(path.c_str(), "rb");
+        if (!f) return false;
+        char buf[65536];
+        std::size_t k;
+        out.clear();
+        while ((k = std::fread(buf, 1, sizeof(buf), f)) > 0) out.append(buf, k);
+        std::fclose(f);
+        return true;
+    };
+    std::string stored, bin;
+    if (read(base + ".key", stored) && stored == key && read(base + ".cubin", bin) && !bin.empty())
+        return std::vector<char>(bin.begin(), bin.end());
+    std::vector<char> cubin = nvrtc_cubin(src);
+    auto write = [](const std::string& path, const char* p, std::size_t n) {  // temp file, then rename
+        const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<std::uintptr_t>(p));
+        std::FILE* f = std::fopen(tmp.c_str(), "wb");
+        if (!f) return;
+        const bool ok = std::fwrite(p, 1, n, f) == n;
+        std::fclose(f);
+        if (ok) std::rename(tmp.c_str(), path.c_str());
+        else std::remove(tmp.c_str());
+    };
+    write(base + ".cubin", cubin.data(), cubin.size());
+    write(base + ".key", key.data(), key.size());
+    return cubin;
+}
+
+std::vector<char> nvrtc_cubin(const std::string& src) {
     if (std::getenv("QCS_JIT_DUMP")) std::fprintf(stderr, "---- qcs_pass\n%s", src.c_str());
     nvrtcProgram prog;
     const char* headers[] = {kJitSrcKernels, kJitSrcDevice};

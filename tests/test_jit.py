@@ -6,6 +6,10 @@ zeros (same arithmetic, same order; X-like gates become register swaps instead o
 on circuits that exercise gates (real / complex, bundled, controls inside and outside
 the tile), diagonal tables and phases on 1-3 bits, sign flips and sign steps with missed-tile
 programs, butterflies, scales and shared-memory gate rounds."""
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 
@@ -84,6 +88,21 @@ def test_plans_do_not_depend_on_history(Q, cfg):
             assert Q.plan_stats(c) == first
     finally:
         Q.set_jit_mode(old)
+
+
+def test_disk_cache_of_compiled_kernels(tmp_path):
+    """QCS_JIT_CACHE=<dir>: a second process finds the compiled pass kernels on disk (each stored
+    with its full source as the key) instead of compiling them."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import time; t = time.time(); from paper_2411_15332_b200 import configs, qcsim as Q; "
+            "r = Q.plan_compile(configs.c4_circuit(14, 2)); print(r['kernels'], r['cubin_bytes'], time.time() - t)")
+    env = dict(os.environ, QCS_JIT_CACHE=str(tmp_path))
+    runs = [subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, check=True)
+            .stdout.split() for _ in range(2)]
+    assert runs[0][:2] == runs[1][:2] and int(runs[0][0]) > 0
+    cubins = [f for f in os.listdir(tmp_path) if f.endswith(".cubin")]
+    assert len(cubins) == int(runs[0][0])
+    assert float(runs[1][2]) < float(runs[0][2])
 
 
 def test_jit_mode_switch(Q):
