@@ -382,6 +382,9 @@ __device__ __forceinline__ void flip_signs1(double2 (&v)[8], unsigned& negacc) {
     negacc = 0;
 }
 
+struct TileCtx;
+__device__ __forceinline__ void tile_end(double2* a, const PassParams& P, const TmapParam& tmap, const TileCtx& c);
+
 struct TileCtx {
     double2* sm;          // the tile (swizzled), 1 KB aligned
     u64* hi_tab;          // basis offset of local bits 3..m-1 (runs of 8), copied from the host table
@@ -457,15 +460,18 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
         for (unsigned j = t; j < sz; j += bt) c.sm[j] = make_double2(0.0, 0.0);
         cp_async_wait_all();  // the run-offset table
         __syncthreads();
-        if (t == 0) {
-            u64 tile_mask = 0;
-            unsigned local = 0;
-            for (int b = 0; b < m; ++b) {
-                tile_mask |= u64(1) << P.bits[b];
-                local |= unsigned((P.init_index >> P.bits[b]) & 1) << b;
-            }
-            if (P.init && (P.init_index & ~tile_mask) == base) c.sm[swz(local)] = make_double2(1.0, 0.0);
+        u64 tile_mask = 0;
+        unsigned local = 0;
+        for (int b = 0; b < m; ++b) {
+            tile_mask |= u64(1) << P.bits[b];
+            local |= unsigned((P.init_index >> P.bits[b]) & 1) << b;
         }
+        if (!(P.init && (P.init_index & ~tile_mask) == base)) {
+            // zeros in, and every operation is linear: zeros out, without the rounds
+            tile_end(a, P, tmap, c);
+            return false;
+        }
+        if (t == 0) c.sm[swz(local)] = make_double2(1.0, 0.0);
         __syncthreads();
         return true;
     }
