@@ -1,22 +1,45 @@
 #!/usr/bin/env python
-"""Benchmark: amplitude-updates/s of the single-gate sweep (BASELINE.json configs[1], "C2").
+"""Benchmark: amplitude-updates/s per circuit and % of the HBM roofline (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--n 28]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload c4|c1|c2|c3|c5|rh-signs] [--n-circuit n] [--peer] [--dry-run]
 
-One step = the whole C2 sweep: X, Y, Z, S, T, CNOT, CZ, SWAP, Toffoli, H, RX(theta),
-U3(theta, phi, lambda) with the target swept over all n qubits (controls at seeded distinct
-qubits) -- 12 * n single-gate steps applied in place to an n-qubit complex128 random state
-resident in HBM.  amplitude-updates per step = 12 * n * 2^n.
+Default workload: BASELINE ``configs[3]``, "C4", the largest configuration that fits one B200.
+It is a 32-qubit QNN (64 GiB complex128 state): H on all qubits, then 10 layers of RY(theta_q)
+and RZ(phi_q) on every qubit plus a CZ ring, with angles seeded (configs.c4_circuit).  The
+gate count is 992, so amplitude-updates = 992 * 2^32 per circuit.
 
-Prints ONE JSON line (rank 0).  Timing: CUDA events on the state's stream, warm-up first,
-barrier + synchronize on both sides, max over ranks.  The 4 GiB state is 32x the 126 MB L2,
-so no L2 flush is needed between iterations.  N > 1 runs N independent replicas (one per GPU,
-weak scaling); the sharded multi-GPU path is not this benchmark's workload.
+One step is one whole circuit run through ``qcsim.simulate``, the reference's ``simulate``
+(engine.cpp:153-210).  It runs from |0...0> on a state resident in HBM.
+
+- N = 1: ``value`` is device-timed with CUDA events on the state's stream.  The state (64 GiB)
+  is 500x the L2, so no flush is needed.
+- ``e2e`` uses the C ABI with host buffers.  Each step builds a fresh circuit with new angles,
+  which misses the plan cache, so planning and table uploads run inside the timed region.  The
+  step then calls ``qcs_simulate`` and reads back what ``render_report`` needs (norm, argmax,
+  top-16) into host memory.
+- ``roofline`` is taken for the dominant kernel (the fused tile pass).  Its achieved bytes are
+  the algorithmic bytes per launch divided by the per-launch CUDA-event time.
+- ``c2_sweep`` is the single-gate kernel line (BASELINE configs[1], n=28), carried as an extra key.
+- ``cpu_baseline`` is the reference itself (``oracle/_ref``, 1 thread) on a bounded sample of the
+  same C4 gate list at n=22.  It is extrapolated, because the reference's per-gate cost is
+  O(2^n); at n=32 it is infeasible (>=256 GiB of DAX entries per gate).
+
+N > 1 (``--gpus N``; re-executed under torchrun unless WORLD_SIZE is already set): the same C4
+circuit sharded over N ranks by its top log2(N) qubits (partition.py; "strong" scaling, since the
+circuit is fixed).  Global qubits move in batched remaps: one grouped NCCL send/recv per remap,
+or the peer-memory swap kernel with ``--peer``.  The line reports the exchanged bytes, the exchange
+time measured by CUDA events, the NVLink GB/s and the fraction of 900 GB/s.
+
+``--impl reference`` times the reference's own CPU code path: the compiled, unmodified
+``oracle/_ref`` library.  It imports nothing from the product package.  The config matches the
+b200 arm's; rank 0 alone runs it.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -30,6 +53,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "amplitude-updates/sec per circuit and % of HBM roofline at n qubits, 1/2/4/8 B200"
 UNIT = "amplitude-updates/s"
+NVLINK_GBPS = 900.0  # NVLink 5, per direction per GPU
+SEED = 20241122      # configs.SEED; seed of config k is SEED + k
+TWO_PI = 2.0 * math.pi
 
 
 def dist_env():
@@ -41,13 +67,20 @@ class Dist:
 
     def __init__(self, world, local_rank, backend="nccl"):
         self.world = world
-        self.pg = None
+        self.backend = backend
+        self.init_lines = []
         if world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(local_rank)
-            dist.init_process_group(backend, device_id=torch.device("cuda", local_rank)
-                                    if backend == "nccl" else None)
+            if backend == "nccl":
+                torch.cuda.set_device(local_rank)
+                dist.init_process_group(backend, device_id=torch.device("cuda", local_rank))
+                v = torch.cuda.nccl.version()
+                self.init_lines.append(f"NCCL {'.'.join(map(str, v)) if isinstance(v, tuple) else v} "
+                                       f"communicator: rank {dist.get_rank()}/{world} on cuda:{local_rank}")
+            else:
+                dist.init_process_group(backend)
+                self.init_lines.append(f"{backend} process group: rank {dist.get_rank()}/{world}")
             self.dist = dist
             self.torch = torch
 
@@ -58,7 +91,8 @@ class Dist:
     def max(self, v: float) -> float:
         if self.world == 1:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -74,9 +108,10 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, enabled: bool = True):
         self.gpu = gpu_index
         self.samples = []
+        self.enabled = enabled
         self._stop = threading.Event()
         self._t = None
 
@@ -92,8 +127,9 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self.enabled:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *exc):
@@ -116,13 +152,13 @@ def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def ncu_traffic(kernel_class: str):
-    """DRAM bytes per launch of the dominant kernel class from the committed ncu summary."""
+    """DRAM bytes per launch of a kernel class from the committed ncu summary (profiles/)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
@@ -131,24 +167,63 @@ def ncu_traffic(kernel_class: str):
         return None
 
 
-# ------------------------------------------------------------------ CPU baselines (rank 0, N = 1)
-def cpu_sample_pairs(n_sample: int, count: int):
-    from paper_2411_15332_b200 import configs
-    sweep = configs.c2_sweep(n_sample, seed=configs.seed_of(2))
-    step = max(1, len(sweep) // count)
-    return [sweep[i] for i in range(0, len(sweep), step)][:count]
+# ------------------------------------------------------------------ workloads, standalone
+# The reference arm must not import the product package, so the C4 gate list is restated here.
+# tests/test_bench.py checks that it equals configs.c4_circuit gate by gate.
+def c4_gate_list(n: int = 32, layers: int = 10, seed: int = SEED + 4):
+    """[(reference gate name, params, qubits)]: H on all qubits, then per layer RY(theta_q) on all,
+    RZ(phi_q) on all, CZ(q, q+1) for even q, odd q, and the wrap CZ(n-1, 0)."""
+    rng = np.random.default_rng(seed)
+    out = [("Hadamard", [], [q]) for q in range(n)]
+    for _ in range(layers):
+        theta = rng.uniform(0.0, TWO_PI, n)
+        phi = rng.uniform(0.0, TWO_PI, n)
+        out += [("RY", [float(theta[q])], [q]) for q in range(n)]
+        out += [("RZ", [float(phi[q])], [q]) for q in range(n)]
+        out += [("Controlled-Z", [], [q, q + 1]) for q in range(0, n - 1, 2)]
+        out += [("Controlled-Z", [], [q, q + 1]) for q in range(1, n - 1, 2)]
+        out.append(("Controlled-Z", [], [n - 1, 0]))
+    return out
 
 
-def reference_sample(n_sample: int, pairs, threads: int):
-    """Time the reference's own pipeline (step_matrix_dax + dax_mvm, engine.cpp:192-199) on the
-    sampled (gate, target) runs; `threads` runs execute concurrently (the library is reentrant,
-    ctypes releases the GIL).  Returns (updates/s, seconds, kind)."""
+def workload_config(workload: str, n: int):
+    """The `config` of both arms (identical, so the driver can pair them)."""
+    if workload == "c4":
+        return {"workload": f"C4 QNN circuit (BASELINE configs[3]), n={n}, 10 layers", "n_qubits": n,
+                "gates_per_circuit": n + 30 * n, "amplitude_updates_per_step": (n + 30 * n) << n,
+                "initial": "|0...0>", "seed": SEED + 4,
+                "l2": f"state {16 << n} B >> 126 MB L2, no flush needed"}
+    if workload == "c2":
+        return {"workload": f"C2 single-gate sweep (BASELINE configs[1]), n={n}", "n_qubits": n,
+                "gates_per_step": 12 * n, "amplitude_updates_per_step": (12 * n) << n, "seed": SEED + 2,
+                "l2": f"state {16 << n} B >> 126 MB L2, no flush needed"}
+    return {"workload": f"{workload.upper()} circuit, n={n}", "n_qubits": n}
+
+
+def _ref_gate_matrix(Reference, name, params):
+    if Reference.available():
+        return Reference.gate(name, params)
+    # oracle port only: standard matrices (timing sample, values irrelevant)
+    if name == "Hadamard":
+        return np.array([[1, 1], [1, -1]], np.complex128) / math.sqrt(2)
+    if name == "RY":
+        c, s = math.cos(params[0] / 2), math.sin(params[0] / 2)
+        return np.array([[c, -s], [s, c]], np.complex128)
+    if name == "RZ":
+        return np.diag([np.exp(-0.5j * params[0]), np.exp(0.5j * params[0])])
+    return np.diag([1, 1, 1, -1]).astype(np.complex128)
+
+
+def reference_gate_sample(n_sample: int, gates, threads: int):
+    """Time the reference's own per-gate pipeline (step_matrix_dax + dax_mvm, engine.cpp:192-199)
+    on the sampled gates; `threads` gates run concurrently on independent states (the library is
+    reentrant; ctypes releases the GIL).  -> (updates/s, seconds, kind)."""
     from oracle.oracle_py import Oracle, Reference
     use_ref = Reference.available()
     rng = np.random.default_rng(0)
     x = (rng.standard_normal(1 << n_sample) + 1j * rng.standard_normal(1 << n_sample))
     x = (x / np.linalg.norm(x)).astype(np.complex128)
-    work = list(pairs)
+    work = [(qs, _ref_gate_matrix(Reference, name, params)) for name, params, qs in gates]
     lock = threading.Lock()
 
     def worker():
@@ -156,11 +231,11 @@ def reference_sample(n_sample: int, pairs, threads: int):
             with lock:
                 if not work:
                     return
-                g = work.pop()
+                qs, m = work.pop()
             if use_ref:
-                Reference.apply_step(n_sample, [(g.qubits, g.gate.matrix)], x)
+                Reference.apply_step(n_sample, [(qs, m)], x)
             else:
-                Oracle.apply_step(n_sample, [(g.qubits, g.gate.matrix)], x)
+                Oracle.apply_step(n_sample, [(qs, m)], x)
 
     t0 = time.perf_counter()
     ths = [threading.Thread(target=worker) for _ in range(max(1, threads))]
@@ -169,61 +244,121 @@ def reference_sample(n_sample: int, pairs, threads: int):
     for t in ths:
         t.join()
     secs = time.perf_counter() - t0
-    return len(pairs) * (1 << n_sample) / secs, secs, ("reference" if use_ref else "port")
+    return len(gates) * (1 << n_sample) / secs, secs, ("reference" if use_ref else "port")
 
 
-def host_threads():
+def host_threads(gib_per_thread: float):
     n = os.cpu_count() or 1
     try:
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     except Exception:
         avail = 64 << 30
-    return max(1, min(n, int(avail // (3 << 30)), 64))
+    return max(1, min(n, int(avail // (gib_per_thread * (1 << 30))), 64))
 
 
-# ------------------------------------------------------------------ arms
+def c4_sample(n_sample: int, count: int, offset: int = 0):
+    """`count` gates spread over the C4 gate list (same kinds and proportions), retargeted to
+    qubits < n_sample."""
+    full = c4_gate_list(32)
+    step = len(full) / count
+    out = []
+    for i in range(count):
+        name, params, qs = full[(int(i * step) + offset) % len(full)]
+        out.append((name, params, [q % n_sample for q in qs] if len({q % n_sample for q in qs}) == len(qs)
+                    else [0, 1]))
+    return out
+
+
+# ------------------------------------------------------------------ reference arm
 def run_reference_arm(args, rank, world):
+    """The reference's CPU implementation on the host (oracle/_ref), same metric and config."""
     if rank != 0:
         return 0
-    n_sample = min(args.n, 24)
-    threads = host_threads()
-    pairs_per_step = max(threads, 4)
-    for _ in range(args.warmup):
-        reference_sample(n_sample, cpu_sample_pairs(n_sample, pairs_per_step), threads)
-    total_updates = 0
-    total_secs = 0.0
-    kind = "reference"
-    for _ in range(args.steps):
-        pairs = cpu_sample_pairs(n_sample, pairs_per_step)
-        v, secs, kind = reference_sample(n_sample, pairs, threads)
-        total_updates += len(pairs) << n_sample
-        total_secs += secs
-    value = total_updates / total_secs
-    sample = (f"{pairs_per_step} single-gate runs per step from the C2 sweep at n={n_sample} "
-              f"(reference step_matrix_dax + dax_mvm per gate, {threads} concurrent host threads)")
+    n = args.n_circuit or 32
+    n_sample = args.ref_n
+    threads = host_threads(3.0)
+    per_step = threads
+    for w in range(args.warmup):
+        reference_gate_sample(n_sample, c4_sample(n_sample, per_step, offset=w), threads)
+    total, secs, kind = 0, 0.0, "reference"
+    for s in range(args.steps):
+        gates = c4_sample(n_sample, per_step, offset=97 * s)
+        _, dt, kind = reference_gate_sample(n_sample, gates, threads)
+        total += len(gates) << n_sample
+        secs += dt
+    value = total / secs
+    updates = (n + 30 * n) << n
+    sample = (f"{per_step} gates per step spread over the C4 gate list (H, RY, RZ, CZ incl. the ring wrap), "
+              f"each through the reference's step_matrix_dax + dax_mvm at n={n_sample} on its own state, "
+              f"{threads} concurrent host threads; per-gate cost is O(2^n), so updates/s at n={n_sample} stands "
+              f"for n={n} (extrapolated: one C4 circuit = {updates / value:.0f} s; the reference cannot hold "
+              f"n={n}: >= 2^{n + 1} DAX entries per gate)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_secs / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": f"C2 single-gate sweep (sampled at n={n_sample})", "n_qubits": args.n,
-                       "gates": "X,Y,Z,S,T,CNOT,CZ,SWAP,Toffoli,H,RX,U3", "parallelism": "host threads"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic", "config": workload_config("c4", n),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+                             "extrapolated": True},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_b200_arm(args, rank, world, local_rank):
-    from paper_2411_15332_b200 import _lib, configs
-    from paper_2411_15332_b200 import qcsim as Q
-    import ctypes as C
+# ------------------------------------------------------------------ helpers of the b200 arm
+def circuit_bytes(c) -> int:
+    """Host bytes a qcs_simulate call reads for circuit c: matrices, qubit lists, sign lists."""
+    b = 0
+    for st in c.steps:
+        if int(st.kind) == 1:
+            b += 8 * len(st.diag.flipped)
+        else:
+            for p in st.placements:
+                b += 16 * p.gate.matrix.size + 4 * p.gate.arity
+    return b
 
-    dist = Dist(world, local_rank)
-    n = args.n
-    dev = local_rank if world > 1 else 0
-    lib = _lib.lib()
+
+def cpu_baseline_c4(n: int):
+    """The compiled reference on 1 thread, on a bounded sample of the C4 gate list at n=22
+    (about 10-20 s), extrapolated to n (per-gate cost O(2^n))."""
+    n_sample = 22
+    gates = c4_sample(n_sample, 12)
+    v, secs, kind = reference_gate_sample(n_sample, gates, 1)
+    updates = (n + 30 * n) << n
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "extrapolated": True,
+            "sample": f"{len(gates)} gates spread over the C4 gate list, reference step_matrix_dax + dax_mvm "
+                      f"per gate at n={n_sample}, 1 thread, {secs:.1f} s; O(2^n) per gate, so one C4 circuit "
+                      f"at n={n} extrapolates to {updates / v:.0f} s"}
+
+
+def timed_device(state, fn, steps):
+    """CUDA events on the state's stream around `steps` calls of fn."""
+    state.sync()
+    state.record(0)
+    for _ in range(steps):
+        fn()
+    state.record(1)
+    state.sync()
+    return state.elapsed_ms(0, 1)
+
+
+def roofline_of(timing, prefer=None):
+    """The dominant kernel class (largest device time) -> roofline dict."""
+    peak, peak_kind = measured_peaks()
+    dom = prefer if prefer in timing else max(timing, key=lambda k: timing[k][1])
+    launches, ms, byts = timing[dom]
+    achieved = (byts / launches) / (ms / launches / 1e3) / 1e9
+    total_ms = sum(v[1] for v in timing.values())
+    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": achieved / peak, "frac_nominal_8TBs": achieved / 8000.0,
+            "traffic": ncu_traffic(dom), "algorithmic_bytes_per_launch": byts / launches,
+            "avg_launch_us": 1e3 * ms / launches, "launches": launches, "share_of_kernel_time": ms / total_ms}
+
+
+def c2_sweep_line(Q, configs, lib, dev, steps=3, warmup=2, n=28):
+    """The single-gate kernels on the C2 sweep (BASELINE configs[1]): the HBM roofline of the
+    per-gate kernels, kept as an extra key of the C4 line."""
     sweep = configs.c2_sweep(n, seed=configs.seed_of(2))
     placements = [Q._placements([Q.Placement(g.gate, qubits=g.qubits)]) for g in sweep]
-    updates_per_step = len(sweep) << n
     state = Q.DeviceState(n, 0, dev)
     state.randomize(configs.seed_of(2))
     h = state.handle
@@ -233,268 +368,267 @@ def run_b200_arm(args, rank, world, local_rank):
             rc = lib.qcs_apply_step(h, arr, 1)
             if rc:
                 Q._check(rc)
-
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
+    state.timing(True)
+    state.timing_reset()
+    ms = timed_device(state, step, steps)
+    timing = state.timing_report()
+    state.timing(False)
+    state.close()
+    value = (len(sweep) << n) * steps / (ms / 1e3)
+    roof = roofline_of(timing, "gate_pair_dense")
+    roof["all_kernels_GBps"] = sum(v[2] for v in timing.values()) / (sum(v[1] for v in timing.values()) / 1e3) / 1e9
+    roof["all_kernels_frac"] = roof["all_kernels_GBps"] / roof["peak"]
+    return {"value": value, "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+            "config": workload_config("c2", n), "roofline": roof,
+            "kernel_classes": {k: {"launches": v[0], "ms": round(v[1], 3), "GBps": v[2] / (v[1] / 1e3) / 1e9}
+                               for k, v in timing.items()}}
+
+
+# ------------------------------------------------------------------ b200 arm, one GPU
+def run_single(args):
+    """Whole circuits (C4 by default; C1, C3, C5 selectable) through qcsim.simulate on one GPU."""
+    from paper_2411_15332_b200 import _lib, configs
+    from paper_2411_15332_b200 import qcsim as Q
+    import ctypes as C
+    lib = _lib.lib()
+    w = args.workload
+    n = args.n_circuit or {"c1": 12, "c3": 30, "c4": 32, "c5": 32}[w]
+    builders = {"c1": lambda s: configs.c1_circuit(n, seed=s), "c3": lambda s: configs.c3_circuit(n),
+                "c4": lambda s: configs.c4_circuit(n, seed=s),
+                "c5": lambda s: configs.c5_circuit(n, global_qubits=3, seed=s)}
+    seed = configs.seed_of(int(w[1]))
+    updates = {"c1": configs.c1_updates(n), "c3": configs.c3_updates(n), "c4": configs.c4_updates(n),
+               "c5": configs.c5_updates(n, 20)}[w]
+    c = builders[w](seed)
+    dev = 0
+    state = Q.DeviceState(n, c.initial, dev)
+
+    # cold: the first call in this process (planning, NVRTC compiles of the pass kernels, uploads)
+    t0 = time.perf_counter()
+    Q.simulate(c, Q.Engine.rh_dax, state=state)
     state.sync()
-    dist.barrier()
+    cold_ms = 1e3 * (time.perf_counter() - t0)
+    for _ in range(max(0, args.warmup - 1)):
+        Q.simulate(c, Q.Engine.rh_dax, state=state)
+    plan = Q.plan_stats(c)
+
+    # value: device-resident state, events on its stream, the plan cached after warm-up
     launches0 = lib.qcs_kernel_launches()
     state.timing(True)
     state.timing_reset()
-    with ClockSampler(dev) as clocks:
-        state.sync()
-        dist.barrier()
-        state.record(0)
-        for _ in range(args.steps):
-            step()
-        state.record(1)
-        state.sync()
-        ms = state.elapsed_ms(0, 1)
-    dist.barrier()
+    with ClockSampler(dev, not args.no_clocks) as clocks:
+        ms = timed_device(state, lambda: Q.simulate(c, Q.Engine.rh_dax, state=state), args.steps)
     launches = lib.qcs_kernel_launches() - launches0
     timing = state.timing_report()
     state.timing(False)
-    ms_max = dist.max(ms)
-    value = world * updates_per_step * args.steps / (ms_max / 1e3)
+    value = updates * args.steps / (ms / 1e3)
 
-    # roofline of the dominant kernel class (largest share of device time)
-    dom = max(timing.items(), key=lambda kv: kv[1][1])
-    dom_launches, dom_ms, dom_bytes = dom[1]
-    peak, peak_kind = measured_peaks()
-    achieved = (dom_bytes / dom_launches) / (dom_ms / dom_launches / 1e3) / 1e9
-    traffic = ncu_traffic(dom[0])
-    total_kernel_ms = sum(v[1] for v in timing.values())
-    all_bytes = sum(v[2] for v in timing.values())
-
-    # e2e: the public C ABI with host buffers.  Every step (one request) uploads its input
-    # state from pinned memory, runs the sweep and reads the result back into pinned memory.
-    # Two requests are in flight on two states (two streams), so one request's PCIe copies
-    # overlap the other's sweep -- the way a serving loop uses the API (the reference arm
-    # likewise runs concurrent requests on all host threads).  Each sweep waits for the
-    # previous request's sweep (qcs_state_wait) before its result's read-back is enqueued, so
-    # the sweeps run back to back instead of sharing the GPU and then leaving it idle while
-    # both streams copy.  The serial form (one state, copies not overlapped) is reported
-    # alongside.
+    # e2e: fresh angles every step (plan-cache miss, same kernel structure), host-side circuit in,
+    # render_report's numbers out (norm, argmax, top-16) into host memory
     e2e_steps = max(2, args.steps)
-    nbytes = 16 << n
-    bufs = []
-    for _ in range(3):  # input (read by both uploads), one output per state
-        hp = C.c_void_p()
-        Q._check(lib.qcs_host_alloc(nbytes, C.byref(hp)))
-        bufs.append(hp)
-    state2 = Q.DeviceState(n, 0, dev)
-    states = [state, state2]
-    try:
-        hin, hout = bufs[0], bufs[1:]
-        Q._check(lib.qcs_state_download(h, hin, 0, 1 << n))
+    circuits = [builders[w](seed + 1000 + i) for i in range(e2e_steps)] if w != "c3" else [c] * e2e_steps
+    h2d = sum(circuit_bytes(ci) for ci in circuits) // e2e_steps
+    Q.simulate(circuits[0], Q.Engine.rh_dax, state=state)  # not timed: the first fresh-angle plan
+    state.summary(16)
+    state.sync()
+    results = []
+    t0 = time.perf_counter()
+    for ci in circuits:
+        Q.simulate(ci, Q.Engine.rh_dax, state=state)
+        results.append(state.summary(16))
+    e2e_ms = 1e3 * (time.perf_counter() - t0)
+    d2h = 8 + 16 * 16
+    e2e_value = updates * e2e_steps / (e2e_ms / 1e3)
+    norm_err = max(abs(r[0] - 1.0) for r in results)
 
-        def run_sweep(st):
-            for arr, _keep in placements:
-                rc = lib.qcs_apply_step(st, arr, 1)
-                if rc:
-                    Q._check(rc)
+    roof = roofline_of(timing, "tile_pass")
+    roof.update({"passes_per_step": plan["passes"], "rounds_per_step": plan["rounds"],
+                 "kernel_ms_per_step": sum(v[1] for v in timing.values()) / args.steps,
+                 "hbm_floor_ms": sum(v[2] for v in timing.values()) / args.steps / (roof["peak"] * 1e9) * 1e3,
+                 "full_sweeps_per_step": sum(v[2] for v in timing.values()) / args.steps / (32.0 * (1 << n))})
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": workload_config(w, n) if w == "c4" else {"workload": f"{w.upper()} circuit, n={n}",
+                                                                "n_qubits": n, "amplitude_updates_per_step": updates},
+            "parallelism": "single GPU, fused shared-memory passes",
+            "roofline": roof,
+            "kernel_classes": {k: {"launches": v[0] / args.steps, "ms": round(v[1] / args.steps, 3),
+                                   "GBps": v[2] / (v[1] / 1e3) / 1e9} for k, v in timing.items()},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
+                    "timer": "host wall clock around qcs_simulate + qcs_summary (synchronous read-back)",
+                    "inputs": "a fresh-angle circuit per step (plan-cache miss: planning and table upload timed)",
+                    "outputs": "norm, argmax, top-16 probabilities", "max_norm_error": norm_err,
+                    "cold_first_call_ms": cold_ms},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary()}
+    state.close()
+    if w == "c4" and not args.no_c2:
+        line["c2_sweep"] = c2_sweep_line(Q, configs, lib, dev)
+    if w == "c4" and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_c4(n)
+    print(json.dumps(line), flush=True)
+    return 0
 
-        def request(i, last):
-            st, prev = states[i % 2].handle, states[(i - 1) % 2].handle
-            Q._check(lib.qcs_state_upload(st, hin, 0, 1 << n))
-            if i > 0:
-                Q._check(lib.qcs_state_wait(st, prev))  # after request i-1's sweep
-            run_sweep(st)
-            if i > 0:
-                Q._check(lib.qcs_state_download_async(prev, hout[(i - 1) % 2], 0, 1 << n))
-            if last:
-                Q._check(lib.qcs_state_download_async(st, hout[i % 2], 0, 1 << n))
 
-        def request_serial(i, last):
-            st = states[0].handle
-            Q._check(lib.qcs_state_upload(st, hin, 0, 1 << n))
-            run_sweep(st)
-            Q._check(lib.qcs_state_download_async(st, hout[0], 0, 1 << n))
-
-        def timed(fn, count):
-            for st in states:
-                st.sync()
-            dist.barrier()
-            t0 = time.perf_counter()
-            for i in range(count):
-                fn(i, i == count - 1)
-            for st in states:
-                st.sync()
-            return dist.max(1e3 * (time.perf_counter() - t0))
-
-        e2e_ms = timed(request, e2e_steps)
-        serial_ms = timed(request_serial, max(1, min(3, args.steps)))
-        serial_steps = max(1, min(3, args.steps))
-    finally:
-        state2.close()
-        for hp in bufs:
-            lib.qcs_host_free(hp)
-    e2e_value = world * updates_per_step * e2e_steps / (e2e_ms / 1e3)
-    e2e_serial = world * updates_per_step * serial_steps / (serial_ms / 1e3)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_sample = min(n, 22)
-        pairs = cpu_sample_pairs(n_sample, 12)
-        v, secs, kind = reference_sample(n_sample, pairs, 1)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
-               "sample": f"{len(pairs)} C2 single-gate runs at n={n_sample}, "
-                         f"{'reference step_matrix_dax + dax_mvm' if kind == 'reference' else 'oracle port'}, "
-                         f"1 thread, {secs:.1f} s"}
-
-    csum = clocks.summary()
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64 complex)", "data": "synthetic",
-        "config": {"workload": f"C2 single-gate sweep, n={n}", "n_qubits": n,
-                   "gates_per_step": len(sweep), "amplitude_updates_per_step": updates_per_step,
-                   "state_bytes": 16 << n, "l2": "state 32x larger than L2, no flush needed",
-                   "parallelism": "replicas" if world > 1 else "single GPU", "seed": configs.seed_of(2)},
-        "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "frac_nominal_8TBs": achieved / 8000.0, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": dom_bytes / dom_launches,
-                     "avg_launch_us": 1e3 * dom_ms / dom_launches, "launches": dom_launches,
-                     "share_of_kernel_time": dom_ms / total_kernel_ms,
-                     "all_kernels_GBps": all_bytes / (total_kernel_ms / 1e3) / 1e9,
-                     "all_kernels_frac": all_bytes / (total_kernel_ms / 1e3) / 1e9 / peak},
-        "kernel_classes": {k: {"launches": v[0], "ms": round(v[1], 3), "GBps": v[2] / (v[1] / 1e3) / 1e9}
-                           for k, v in timing.items()},
-        "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                "steps": e2e_steps, "requests_in_flight": 2, "timer": "host wall clock, both streams synced",
-                "serial_value": e2e_serial},
-        "gpu_launches": int(launches),
-        "clocks": csum,
-    }
+def run_c2(args, rank, world, local_rank):
+    """--workload c2: the single-gate sweep alone (BASELINE configs[1]); N > 1 runs replicas."""
+    from paper_2411_15332_b200 import _lib, configs
+    from paper_2411_15332_b200 import qcsim as Q
+    dist = Dist(world, local_rank)
+    lib = _lib.lib()
+    dev = local_rank if world > 1 else 0
+    with ClockSampler(dev, not args.no_clocks) as clocks:
+        launches0 = lib.qcs_kernel_launches()
+        r = c2_sweep_line(Q, configs, lib, dev, args.steps, args.warmup, args.n)
+        launches = lib.qcs_kernel_launches() - launches0
+    ms = dist.max(r["ms_per_step"] * args.steps)
+    value = world * r["config"]["amplitude_updates_per_step"] * args.steps / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": r["config"],
+            "parallelism": "replicas" if world > 1 else "single GPU", "roofline": r["roofline"],
+            "kernel_classes": r["kernel_classes"], "gpu_launches": int(launches), "clocks": clocks.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    state.close()
     dist.close()
     return 0
 
 
-def run_circuit_arm(args, rank, world, local_rank):
-    """Whole BASELINE circuits (C1, C3, C4, C5) through the fused engine.  World 1: qcsim.simulate
-    on one device state.  World > 1: the state sharded over the ranks by its top log2(world)
-    qubits (paper_2411_15332_b200/partition.py), half-shard exchanges over NCCL ("strong" scaling:
-    the circuit is fixed)."""
+# ------------------------------------------------------------------ b200 arm, sharded
+class NoComputeBackend:
+    """--dry-run: the shard is a CPU tensor and local operations are skipped, so the launcher,
+    the rendezvous, the remap exchanges (real bytes over gloo) and the JSON line can be exercised
+    on a CPU host.  The numbers it prints are not measurements (the line says dry_run)."""
+
+    def __init__(self, n_local):
+        import torch
+        self.torch = torch
+        self.n = n_local
+        self.tensor = torch.zeros(1 << n_local, dtype=torch.complex128)
+
+    def set_basis(self, index):
+        self.tensor.zero_()
+        if index is not None:
+            self.tensor[index] = 1.0
+
+    def run(self, ops):
+        pass
+
+    def block(self, k: int, j: int, start: int, count: int):
+        b = (1 << (self.n - k)) * j + start
+        return self.tensor[b: b + count]
+
+    def empty(self, count):
+        return self.torch.empty(count, dtype=self.torch.complex128)
+
+    def sync(self):
+        pass
+
+
+def run_sharded(args, rank, world, local_rank):
+    """The C4 circuit (default) sharded over `world` ranks: strong scaling of one circuit."""
     import torch
     from paper_2411_15332_b200 import configs
-    from paper_2411_15332_b200 import qcsim as Q
-    w = args.workload
-    n = args.n_circuit
-    build = {"c1": lambda: configs.c1_circuit(n or 12), "c3": lambda: configs.c3_circuit(n or 30),
-             "c4": lambda: configs.c4_circuit(n or 32), "c5": lambda: configs.c5_circuit(n or 35)}[w]
-    c = build()
-    updates = {"c1": configs.c1_updates(c.n), "c3": configs.c3_updates(c.n), "c4": configs.c4_updates(c.n),
-               "c5": configs.c5_updates(c.n)}[w]
-    dist = Dist(world, local_rank)
-    dev = local_rank if world > 1 else 0
-    torch.cuda.set_device(dev)
-    if world == 1:
-        state = Q.DeviceState(c.n, c.initial, dev)
-
-        def step():
-            Q.simulate(c, Q.Engine.rh_dax, state=state)
-        sync = state.sync
-        plan = Q.plan_stats(c)
+    from paper_2411_15332_b200.partition import DistTransport, ShardedState, circuit_ops
+    dry = args.dry_run
+    dist = Dist(world, local_rank, "gloo" if dry else "nccl")
+    w = args.workload if args.workload in ("c4", "c5", "c3") else "c4"
+    n = args.n_circuit or {"c3": 30, "c4": 32, "c5": 35}[w]
+    c = {"c3": lambda: configs.c3_circuit(n), "c4": lambda: configs.c4_circuit(n),
+         "c5": lambda: configs.c5_circuit(n, global_qubits=world.bit_length() - 1)}[w]()
+    updates = {"c3": configs.c3_updates(n), "c4": configs.c4_updates(n), "c5": configs.c5_updates(n, 20)}[w]
+    g = world.bit_length() - 1
+    ops = circuit_ops(c)
+    if dry:
+        backend = NoComputeBackend(n - g)
+        transport = DistTransport()
+    elif args.peer:
+        from paper_2411_15332_b200.partition import DeviceBackend, SymmetricTransport
+        backend = DeviceBackend(n - g, local_rank, symmetric=True)
+        transport = SymmetricTransport()
     else:
-        from paper_2411_15332_b200.partition import DeviceBackend, DistTransport, ShardedState
-        g = world.bit_length() - 1
-        if args.peer:  # fused global-qubit gates over NVLink peer memory (torch symmetric memory)
-            from paper_2411_15332_b200.partition import SymmetricTransport
-            backend = DeviceBackend(c.n - g, dev, symmetric=True)
-            sh = ShardedState(c.n, world, rank, backend, SymmetricTransport(), initial=c.initial)
-        else:  # half-shard swaps over NCCL send/recv
-            backend = DeviceBackend(c.n - g, dev)
-            sh = ShardedState(c.n, world, rank, backend, DistTransport(), initial=c.initial, peer=False)
-        ops = []
-        for st in c.steps:
-            if int(st.kind) == 1:
-                ops.append(("diag", list(st.diag.flipped), st.diag.flip_rest))
-            elif st.is_hadamard_all(c.n):
-                ops.append(("rh",))
-            else:
-                ops += [("gate", p.gate.matrix, p.qubit_list(), p.gate.name) for p in st.placements]
+        from paper_2411_15332_b200.partition import DeviceBackend
+        backend = DeviceBackend(n - g, local_rank)
+        transport = DistTransport()
+    sh = ShardedState(n, world, rank, backend, transport, initial=c.initial, peer=bool(args.peer) and not dry)
 
-        def step():
-            sh.phys = list(range(c.n))
-            sh.set_basis(c.initial)
-            for op in ops:
-                if op[0] == "gate":
-                    sh.apply_gate(op[1], op[2], op[3])
-                elif op[0] == "diag":
-                    sh.apply_diag(op[1], op[2])
-                else:
-                    sh.apply_rh()
-            sh.flush()
+    def step():
+        sh.reset(c.initial)
+        sh.run(ops)
+        sh.flush()
 
-        def sync():
-            torch.cuda.synchronize(dev)
+    def sync():
+        if not dry:
+            torch.cuda.synchronize(local_rank)
+
     for _ in range(args.warmup):
         step()
     sync()
     dist.barrier()
-    if world == 1:  # events on the state's own stream, per-launch timing of the kernel classes
-        state.timing(True)
-        state.timing_reset()
-        with ClockSampler(dev) as clocks:
-            state.record(0)
+    sh.timing(not dry)
+    sh.reset_stats()
+    with ClockSampler(local_rank, not (dry or args.no_clocks)) as clocks:
+        if dry:
+            t0 = time.perf_counter()
             for _ in range(args.steps):
                 step()
-            state.record(1)
-            sync()
-        ms = state.elapsed_ms(0, 1)
-        timing = state.timing_report()
-        state.timing(False)
-    else:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(dev) as clocks:
+            ms = 1e3 * (time.perf_counter() - t0)
+        else:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record()
             for _ in range(args.steps):
                 step()
-            sync()
             ev1.record()
             ev1.synchronize()
-        ms = dist.max(ev0.elapsed_time(ev1))
+            ms = ev0.elapsed_time(ev1)
+    ms = dist.max(ms)
+    st = sh.exchange_stats()
+    ex_ms = dist.max(st["ms"])
     value = updates * args.steps / (ms / 1e3)
+    shard_bytes = 16 << (n - g)
+    per_step_bytes = st["bytes_sent"] / args.steps
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "c128 (f64 complex)",
-            "data": "synthetic", "config": {"workload": f"{w.upper()} circuit, n={c.n}", "n_qubits": c.n,
-                                            "amplitude_updates_per_step": updates,
-                                            "parallelism": f"sharded over {world} ranks (top qubits)" if world > 1
-                                            else "single GPU, fused passes"},
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": workload_config(w, n) if w == "c4" else {"workload": f"{w.upper()} circuit, n={n}",
+                                                                "n_qubits": n, "amplitude_updates_per_step": updates},
+            "parallelism": f"state sharded over {world} ranks by its top {g} qubits",
+            "exchange": {"transport": ("peer-memory swap kernel (NVLink P2P)" if args.peer
+                                       else "grouped NCCL send/recv, chunked, double-buffered"),
+                         "remaps_per_step": st["remaps"] / args.steps,
+                         "bytes_sent_per_step_per_rank": per_step_bytes,
+                         "shards_moved_per_step": per_step_bytes / shard_bytes,
+                         "exchange_ms_per_step_max_rank": ex_ms / args.steps,
+                         "nvlink_GBps": (st["bytes_sent"] / (ex_ms / 1e3) / 1e9) if ex_ms > 0 else None,
+                         "nvlink_peak_GBps": NVLINK_GBPS,
+                         "nvlink_frac": (st["bytes_sent"] / (ex_ms / 1e3) / 1e9 / NVLINK_GBPS) if ex_ms > 0 else None,
+                         "share_of_step": (ex_ms / ms) if ms > 0 else None},
+            "comm_init": dist.init_lines,
             "clocks": clocks.summary()}
-    if world == 1:
-        peak, peak_kind = measured_peaks()
-        k_ms = sum(v[1] for v in timing.values())
-        k_bytes = sum(v[2] for v in timing.values())
-        achieved = k_bytes / (k_ms / 1e3) / 1e9
-        # algorithmic bytes: 32 B per amplitude per HBM pass (tile passes and single-op gate kernels)
-        line["roofline"] = {"bound": "hbm", "kernel": "all passes", "achieved": achieved, "peak": peak,
-                            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                            "frac_nominal_8TBs": achieved / 8000.0, "traffic": None,
-                            "passes_per_step": plan["passes"], "skip_passes_per_step": plan["skip_passes"],
-                            "kernel_ms_per_step": k_ms / args.steps,
-                            # the launched passes' algorithmic bytes at copy bandwidth (skip passes and
-                            # pass pairs move only the tiles they reach)
-                            "pass_floor_ms": k_bytes / args.steps / (peak * 1e9) * 1e3,
-                            "full_sweeps_per_step": k_bytes / args.steps / (32.0 * (1 << c.n))}
-        line["kernel_classes"] = {k: {"launches": v[0] / args.steps, "ms": round(v[1] / args.steps, 3),
-                                      "GBps": v[2] / (v[1] / 1e3) / 1e9} for k, v in timing.items()}
-        line["gpu_launches"] = int(sum(v[0] for v in timing.values()))
-        state.close()
-    if world > 1:
-        line["exchanges_per_step"] = sh.swaps / (args.steps + args.warmup)
-        line["peer_gates_per_step"] = sh.splits / (args.steps + args.warmup)
-        line["config"]["global_qubit_gates"] = "peer-memory kernel" if sh.peer else "NCCL half-shard swaps"
+    if dry:
+        line["dry_run"] = True
+        line["data"] = "none (dry run: local operations skipped, exchanges real over gloo)"
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.close()
     return 0
+
+
+# ------------------------------------------------------------------ launcher
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` (N > 1) without a torchrun environment: start N ranks on this node."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -503,21 +637,32 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=28)
-    ap.add_argument("--workload", default="c2", choices=["c2", "c1", "c3", "c4", "c5"],
-                    help="c2 (default): the single-gate sweep; c1/c3/c4/c5: whole BASELINE circuits")
-    ap.add_argument("--n-circuit", type=int, default=0, help="qubits for c1/c3/c4/c5 (default: BASELINE size)")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c1", "c2", "c3", "c5", "rh-signs"],
+                    help="c4 (default): BASELINE configs[3]; c2: the single-gate sweep; c1/c3/c5: other circuits")
+    ap.add_argument("--n", type=int, default=28, help="qubits of the c2 sweep")
+    ap.add_argument("--n-circuit", type=int, default=0, help="qubits of c1/c3/c4/c5 (default: BASELINE size)")
+    ap.add_argument("--ref-n", type=int, default=24, help="qubits of the reference arm's per-gate sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c2", action="store_true", help="skip the c2_sweep extra key of the C4 line")
+    ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--peer", action="store_true",
-                    help="c4/c5 under torchrun: gates on global qubits as one kernel over NVLink peer memory "
-                         "(qcs_apply_split) instead of NCCL half-shard swaps")
+                    help="N > 1: remaps through the peer-memory swap kernel (torch symmetric memory) instead of NCCL")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="N > 1 on a CPU host (gloo): exchanges only, no compute -- tests the launcher path")
     args = ap.parse_args()
     rank, world, local_rank = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
-    if args.workload != "c2":
-        return run_circuit_arm(args, rank, world, local_rank)
-    return run_b200_arm(args, rank, world, local_rank)
+    if args.workload == "rh-signs":
+        from paper_2411_15332_b200 import bench_modes
+        return bench_modes.rh_signs(args)
+    if args.workload == "c2":
+        return run_c2(args, rank, world, local_rank)
+    if world > 1:
+        return run_sharded(args, rank, world, local_rank)
+    return run_single(args)
 
 
 if __name__ == "__main__":

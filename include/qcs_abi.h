@@ -141,6 +141,15 @@ int qcs_apply_diag(qcs_state* s, const uint64_t* flipped, uint64_t count, int fl
 int qcs_apply_split(qcs_state* s, void* peer_amps, int self_bit, int num_sel, const int* sel_bits,
                     const double* blocks, uint32_t skip_mask);
 
+/* Swap the amplitudes [offset, offset+count) of this shard with `count` amplitudes of peer
+ * memory at `peer_amps` (a partner shard mapped into this device's address space: NVLink P2P,
+ * or another buffer on one device).  The data movement of a global<->local qubit remap of a
+ * sharded state (partition.py): the two ranks of a pair each swap one half of their block pair,
+ * so nothing is staged and every amplitude crosses the link once each way.  The caller orders
+ * it after the partner's earlier work and before its later work (a barrier on each side).
+ * B200-specific (the reference has no multi-device code). */
+int qcs_swap_peer(qcs_state* s, uint64_t offset, void* peer_amps, uint64_t count);
+
 /* rh_mvm(rh_build(n), s) (rh.hpp:64-66): H^{(x)n} as a Walsh-Hadamard butterfly, scaled once
  * by exp2(-n/2) (rh.cpp:20).  Within 1e-12 of the reference (whose own error is larger). */
 int qcs_apply_rh(qcs_state* s);
@@ -155,6 +164,14 @@ int qcs_probabilities(qcs_state* s, double* out, int mem);
 int qcs_argmax(qcs_state* s, uint64_t* index, double* probability);
 /* k largest probabilities, descending, ties to the lower index (circuit_io.cpp:140-147) */
 int qcs_topk(qcs_state* s, int k, uint64_t* indices, double* probabilities);
+/* max_i |a_i - b_i| and ||a - b||_2 over two states of the same size on one device, reduced
+ * on the device (no download).  Ordered after both states' pending work.  B200-specific: the
+ * BASELINE-size parity tests compare the fused engine with its per-gate kernels this way. */
+int qcs_state_distance(qcs_state* a, qcs_state* b, double* max_abs, double* l2);
+/* What a report needs from a state in ONE pass over it: the norm (sqrt of the summed
+ * probabilities, core.cpp:30-34) and the k <= 16 largest probabilities as qcs_topk gives them
+ * (indices[0] is the argmax).  Host outputs; synchronous. */
+int qcs_summary(qcs_state* s, int k, double* norm, uint64_t* indices, double* probabilities);
 /* amplitudes at arbitrary indices (host index list, host output 2*count doubles) */
 int qcs_gather(qcs_state* s, const uint64_t* indices, uint64_t count, double* out);
 

@@ -86,10 +86,13 @@ SIGNATURES = {
     "qcs_argmax": (C.c_int, [_P, _U64, _D]),
     "qcs_topk": (C.c_int, [_P, C.c_int, _U64, _D]),
     "qcs_gather": (C.c_int, [_P, _U64, C.c_uint64, _D]),
+    "qcs_state_distance": (C.c_int, [_P, _P, _D, _D]),
+    "qcs_summary": (C.c_int, [_P, C.c_int, _D, _U64, _D]),
     "qcs_simulate": (C.c_int, [_P, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
                                C.POINTER(qcs_step_report)]),
     "qcs_memory_report": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_step_report)]),
     "qcs_apply_split": (C.c_int, [_P, _P, C.c_int, C.c_int, _I, _D, C.c_uint32]),
+    "qcs_swap_peer": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64]),
     "qcs_plan_stats": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
                                  C.POINTER(qcs_plan_info)]),
     "qcs_set_jit_mode": (C.c_int, [C.c_int]),

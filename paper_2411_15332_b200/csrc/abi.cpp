@@ -150,6 +150,26 @@ void check_range(const qcs_state* s, uint64_t first, uint64_t count) {
     const uint64_t dim = uint64_t(1) << s->n;
     if (first > dim || count > dim - first) qcs::raise(QCS_ERR_DIMENSION, "amplitude range out of bounds");
 }
+
+// Work enqueued on s from now on starts after everything enqueued on `other` so far: an event on
+// other's stream, waited on by s's stream (the host does not block).
+void cross_wait(qcs_state* s, const qcs_state* other) {
+    if (s == other || s->stream == other->stream) return;
+    cudaEvent_t ev = nullptr;
+    {
+        qcs::DeviceGuard g(other->device);
+        QCS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        const cudaError_t e = cudaEventRecord(ev, other->stream);
+        if (e != cudaSuccess) {
+            cudaEventDestroy(ev);
+            QCS_CUDA(e);
+        }
+    }
+    qcs::DeviceGuard g(s->device);
+    const cudaError_t e = cudaStreamWaitEvent(s->stream, ev, 0);
+    cudaEventDestroy(ev);  // the wait stays valid (the event completes on its own)
+    QCS_CUDA(e);
+}
 }  // namespace
 
 int qcs_state_upload(qcs_state* s, const double* host, uint64_t first, uint64_t count) {
@@ -192,21 +212,7 @@ int qcs_state_wait(qcs_state* s, const qcs_state* other) {
     return guarded([&] {
         need(s, "state");
         need(other, "other");
-        if (s == other) return;
-        cudaEvent_t ev = nullptr;
-        {
-            qcs::DeviceGuard g(other->device);
-            QCS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            const cudaError_t e = cudaEventRecord(ev, other->stream);
-            if (e != cudaSuccess) {
-                cudaEventDestroy(ev);
-                QCS_CUDA(e);
-            }
-        }
-        qcs::DeviceGuard g(s->device);
-        const cudaError_t e = cudaStreamWaitEvent(s->stream, ev, 0);
-        cudaEventDestroy(ev);  // the wait stays valid (the event completes on its own)
-        QCS_CUDA(e);
+        cross_wait(s, other);
     });
 }
 
@@ -215,9 +221,16 @@ int qcs_state_copy(qcs_state* dst, const qcs_state* src) {
         need(dst, "dst");
         need(src, "src");
         if (dst->n != src->n) qcs::raise(QCS_ERR_DIMENSION, "state copy qubit count mismatch");
-        qcs::DeviceGuard g(dst->device);
-        QCS_CUDA(cudaStreamSynchronize(src->stream));
-        QCS_CUDA(cudaMemcpyAsync(dst->amps, src->amps, (sizeof(double2)) << src->n, cudaMemcpyDefault, dst->stream));
+        if (dst == src) return;
+        // device-side ordering both ways, the host never blocks: the copy (on dst's stream)
+        // starts after src's pending work, and src's later work starts after the copy has read it
+        auto* s = const_cast<qcs_state*>(src);
+        cross_wait(dst, s);
+        {
+            qcs::DeviceGuard g(dst->device);
+            QCS_CUDA(cudaMemcpyAsync(dst->amps, src->amps, (sizeof(double2)) << src->n, cudaMemcpyDefault, dst->stream));
+        }
+        cross_wait(s, dst);
     });
 }
 
@@ -271,6 +284,17 @@ int qcs_apply_split(qcs_state* s, void* peer_amps, int self_bit, int num_sel, co
     });
 }
 
+int qcs_swap_peer(qcs_state* s, uint64_t offset, void* peer_amps, uint64_t count) {
+    return guarded([&] {
+        need(s, "state");
+        if (count && !peer_amps) qcs::raise(QCS_ERR_ARG, "null peer block");
+        check_range(s, offset, count);
+        qcs::DeviceGuard g(s->device);
+        qcs::TimerScope ts(s);
+        qcs::launch_swap_peer(s->amps + offset, static_cast<double2*>(peer_amps), count, s->stream);
+    });
+}
+
 int qcs_apply_rh(qcs_state* s) {
     return guarded([&] {
         need(s, "state");
@@ -308,6 +332,21 @@ int qcs_probabilities(qcs_state* s, double* out, int mem) {
     });
 }
 
+int qcs_state_distance(qcs_state* a, qcs_state* b, double* max_abs, double* l2) {
+    return guarded([&] {
+        need(a, "a");
+        need(b, "b");
+        need(max_abs, "max_abs");
+        need(l2, "l2");
+        if (a->n != b->n) qcs::raise(QCS_ERR_DIMENSION, "state distance qubit count mismatch");
+        if (a->device != b->device) qcs::raise(QCS_ERR_ARG, "states on different devices");
+        cross_wait(a, b);
+        qcs::DeviceGuard g(a->device);
+        qcs::distance(a->amps, b->amps, uint64_t(1) << a->n, max_abs, l2, a->stream);
+        cross_wait(b, a);
+    });
+}
+
 int qcs_argmax(qcs_state* s, uint64_t* index, double* probability) {
     return guarded([&] {
         need(s, "state");
@@ -325,6 +364,17 @@ int qcs_topk(qcs_state* s, int k, uint64_t* indices, double* probabilities) {
         need(probabilities, "probabilities");
         qcs::DeviceGuard g(s->device);
         qcs::topk(s->amps, uint64_t(1) << s->n, k, indices, probabilities, s->stream);
+    });
+}
+
+int qcs_summary(qcs_state* s, int k, double* norm, uint64_t* indices, double* probabilities) {
+    return guarded([&] {
+        need(s, "state");
+        need(norm, "norm");
+        need(indices, "indices");
+        need(probabilities, "probabilities");
+        qcs::DeviceGuard g(s->device);
+        qcs::topk(s->amps, uint64_t(1) << s->n, k, indices, probabilities, s->stream, norm);
     });
 }
 

@@ -308,9 +308,10 @@ void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low) {
 // Upload and launch a lowered plan on the state.  init (>= 0): the state is to start from the
 // basis state |init>; consumed (set to -1) by folding it into the first pass when that pass
 // writes every tile, else by a fill kernel first.  jit: per pass, the specialised kernel (kept by
-// cached plans); cached: the plan's identity, whose tables need no upload when plan_buf holds them.
+// cached plans); cached: the cached plan's id (never reused, unlike its address), whose tables
+// need no upload when plan_buf holds them; 0 for an uncached plan.
 void execute_fused(qcs_state* s, const std::vector<FOp>& ops, Lowered& low, std::int64_t* init,
-                   std::vector<void*>* jit = nullptr, const void* cached = nullptr) {
+                   std::vector<void*>* jit = nullptr, std::uint64_t cached = 0) {
     const int n = s->n;
     // plan buffer: [TileOps | flip lists | u64 tables], 256-byte aligned sections
     const std::size_t bb = low.big.size() * sizeof(TileOp);
@@ -402,7 +403,7 @@ void run_fused(qcs_state* s, const std::vector<FOp>& ops, std::int64_t* init = n
     if (ops.empty()) return;
     Lowered low;
     plan_fused(s->n, ops, low);
-    s->plan_loaded = nullptr;
+    s->plan_loaded = 0;
     execute_fused(s, ops, low, init);
 }
 
@@ -518,7 +519,10 @@ u64 rh_sign_count(int n, int method, u64 block) {
 
 }  // namespace
 
+std::atomic<std::uint64_t> g_plan_ids{0};
+
 struct CachedPlan {
+    std::uint64_t id = ++g_plan_ids;        // identifies the plan's tables in plan_buf
     std::vector<unsigned char> key;
     std::vector<FOp> ops;
     Lowered low;
@@ -601,7 +605,7 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
         if (!s->plan_cache) s->plan_cache = new PlanCache;
         if (CachedPlan* hit = s->plan_cache->find(key)) {
             if (reports) std::copy(hit->reports.begin(), hit->reports.end(), reports);
-            execute_fused(s, hit->ops, hit->low, &init, &hit->jit, hit);
+            execute_fused(s, hit->ops, hit->low, &init, &hit->jit, hit->id);
             if (init >= 0) fill_basis(s->amps, dim, u64(init), s->stream);
             return;
         }
@@ -658,7 +662,7 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
             cp->reports = std::move(reps);
             plan_fused(n, cp->ops, cp->low);
             CachedPlan& e = s->plan_cache->insert(std::move(cp));
-            execute_fused(s, e.ops, e.low, &init, &e.jit, &e);
+            execute_fused(s, e.ops, e.low, &init, &e.jit, e.id);
         }
     }
     if (init >= 0) fill_basis(s->amps, dim, u64(init), s->stream);  // no operation at all

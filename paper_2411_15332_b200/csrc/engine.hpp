@@ -30,7 +30,7 @@ struct qcs_state {
     } stage[4];
     int stage_next = 0;
     qcs::PlanCache* plan_cache = nullptr;   // recently simulated circuits: their lowered plans (engine.cpp)
-    const void* plan_loaded = nullptr;      // the cached plan whose tables plan_buf holds
+    std::uint64_t plan_loaded = 0;          // id of the cached plan whose tables plan_buf holds (0: none)
     cudaEvent_t events[8] = {};
     qcs::LaunchTimer* timer = nullptr;   // per-launch timing (qcs_timing_enable)
     ~qcs_state();

@@ -223,14 +223,21 @@ struct SplitParams {
     unsigned char nz[4];  // bit k: entry k of block v is nonzero
     double2 m[4][4];
 };
+void launch_swap_peer(double2* self, double2* peer, std::uint64_t count, cudaStream_t st);
 void launch_split_pair(double2* self, double2* peer, const SplitParams& p, cudaStream_t st);
 
 // ---------------------------------------------------------------- reductions
 double reduce_norm2(const double2* amps, int n, double* scratch_dev, cudaStream_t st);
 void probabilities(const double2* amps, std::uint64_t dim, double* out_dev, cudaStream_t st);
+// max |a_i - b_i| and the L2 norm of a - b (synchronises st)
+void distance(const double2* a, const double2* b, std::uint64_t dim, double* max_abs, double* l2,
+              cudaStream_t st);
 void argmax(const double2* amps, std::uint64_t dim, std::uint64_t* idx, double* p, void* scratch_dev,
             cudaStream_t st);
-void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st);
+// k <= 16 largest probabilities, descending, ties to the lower index; norm (optional): the
+// state's norm from the same pass (sqrt of the summed probabilities)
+void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st,
+          double* norm = nullptr);
 void gather(const double2* amps, const std::uint64_t* idx_dev, std::uint64_t count, double2* out_dev,
             cudaStream_t st);
 void scale(double2* amps, std::uint64_t dim, double s, cudaStream_t st);

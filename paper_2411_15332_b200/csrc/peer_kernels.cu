@@ -54,7 +54,30 @@ __global__ void __launch_bounds__(256) k_split_pair(double2* __restrict__ self, 
     }
 }
 
+// Swap [self, self + count) with [peer, peer + count): the data movement of a global<->local
+// qubit remap (partition.py).  Each rank of a pair swaps one half of the block pair, so every
+// amplitude crosses the link once each way and nothing is staged.  32-byte vectors (two
+// amplitudes) when both ends are 32-byte aligned.
+__global__ void __launch_bounds__(256) k_swap_peer(double2* __restrict__ self, double2* __restrict__ peer, u64 count) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const double2 a = __ldcs(self + i), b = __ldcs(peer + i);
+        __stcs(self + i, b);
+        __stcs(peer + i, a);
+    }
+}
+
 }  // namespace
+
+void launch_swap_peer(double2* self, double2* peer, std::uint64_t count, cudaStream_t st) {
+    if (!count) return;
+    const u64 want = (count + 255) / 256;
+    const unsigned grid = unsigned(want < 1 ? 1 : (want > 148 * 16 ? 148 * 16 : want));
+    // algorithmic bytes: both blocks read and written once (half of it over the peer link)
+    TimedLaunch tl("swap_peer", 64.0 * double(count), st);
+    k_swap_peer<<<grid, 256, 0, st>>>(self, peer, count);
+    check_launch("k_swap_peer");
+}
 
 void launch_split_pair(double2* self, double2* peer, const SplitParams& p, cudaStream_t st) {
     const u64 half = u64(1) << (p.nl - 1);

@@ -4,6 +4,7 @@
 // helpers (core.cpp:22-40).  All kernels are HBM streams; grids are sized in multiples of the
 // 148 SMs with grid-stride loops so reductions are deterministic for a given n.
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <vector>
 
@@ -81,6 +82,49 @@ __global__ void k_sum_partials(double* part, int count) {
     for (int i = threadIdx.x; i < count; i += blockDim.x) acc += part[i];
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) part[count] = acc;
+}
+
+// distance between two states: per block max |a_i - b_i| and sum |a_i - b_i|^2 (fixed grid)
+__global__ void k_distance_partial(const double2* __restrict__ a, const double2* __restrict__ b, u64 dim,
+                                   double* part) {
+    __shared__ double sh[32];
+    __shared__ double shm[32];
+    double acc = 0.0, mx = 0.0;
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride) {
+        const double2 x = __ldcs(a + i), y = __ldcs(b + i);
+        const double dr = x.x - y.x, di = x.y - y.y;
+        const double d2 = dr * dr + di * di;
+        acc += d2;
+        mx = fmax(mx, sqrt(d2));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) shm[threadIdx.x >> 5] = mx;
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) mx = fmax(mx, shm[w]);
+        part[2 * blockIdx.x] = acc;
+        part[2 * blockIdx.x + 1] = mx;
+    }
+}
+
+__global__ void k_distance_final(double* part, int count) {
+    __shared__ double sh[32];
+    double acc = 0.0, mx = 0.0;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
+        acc += part[2 * i];
+        mx = fmax(mx, part[2 * i + 1]);
+    }
+    acc = block_sum(acc, sh);
+    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
+        part[2 * count] = acc;
+        part[2 * count + 1] = mx;
+    }
 }
 
 __global__ void k_probabilities(const double2* __restrict__ a, u64 dim, double* __restrict__ p) {
@@ -175,17 +219,21 @@ __global__ void k_fill_random(double2* __restrict__ a, u64 dim, u64 seed) {
 // the list heads, K candidates per block; the host merges the block candidates.
 constexpr int kTopK = 16;
 
+// psum (optional): per-block sums of the probabilities (the norm of a report, in the same pass)
 __global__ void __launch_bounds__(256) k_topk_partial(const double2* __restrict__ a, u64 dim, int k,
-                                                      ArgMax* __restrict__ out) {
+                                                      ArgMax* __restrict__ out, double* __restrict__ psum) {
     __shared__ ArgMax sh[8];
     __shared__ ArgMax win;
+    __shared__ double shs[32];
     ArgMax lst[kTopK];
 #pragma unroll
     for (int j = 0; j < kTopK; ++j) lst[j] = ArgMax{-1.0, ~u64(0)};
+    double acc = 0.0;
     const u64 stride = u64(gridDim.x) * blockDim.x;
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < dim; i += stride) {
         const double2 x = __ldcs(a + i);
         ArgMax c{__dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)), i};
+        acc += c.p;
         if (!(better(lst[kTopK - 1], c).i == c.i)) continue;
 #pragma unroll
         for (int j = kTopK - 1; j >= 0; --j) {  // bubble c up the sorted list
@@ -196,6 +244,11 @@ __global__ void __launch_bounds__(256) k_topk_partial(const double2* __restrict_
                 lst[j] = c;
             }
         }
+    }
+    if (psum) {
+        acc = block_sum(acc, shs);
+        if (threadIdx.x == 0) psum[blockIdx.x] = acc;
+        __syncthreads();
     }
     int head = 0;
     for (int round = 0; round < k; ++round) {
@@ -257,6 +310,22 @@ double reduce_norm2(const double2* amps, int n, double* scratch, cudaStream_t st
     return h;
 }
 
+void distance(const double2* a, const double2* b, std::uint64_t dim, double* max_abs, double* l2,
+              cudaStream_t st) {
+    double* part = nullptr;
+    QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * (2 * kRedBlocks + 2), st));
+    k_distance_partial<<<kRedBlocks, kRedThreads, 0, st>>>(a, b, dim, part);
+    check_launch("k_distance_partial");
+    k_distance_final<<<1, 1024, 0, st>>>(part, kRedBlocks);
+    check_launch("k_distance_final");
+    double h[2];
+    QCS_CUDA(cudaMemcpyAsync(h, part + 2 * kRedBlocks, sizeof(h), cudaMemcpyDeviceToHost, st));
+    QCS_CUDA(cudaFreeAsync(part, st));
+    QCS_CUDA(cudaStreamSynchronize(st));
+    *l2 = std::sqrt(h[0]);
+    *max_abs = h[1];
+}
+
 void probabilities(const double2* amps, std::uint64_t dim, double* out, cudaStream_t st) {
     k_probabilities<<<grid_for(dim, 256), 256, 0, st>>>(amps, dim, out);
     check_launch("k_probabilities");
@@ -297,17 +366,27 @@ void fill_random(double2* amps, std::uint64_t dim, std::uint64_t seed, cudaStrea
     check_launch("k_fill_random");
 }
 
-void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st) {
+void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st,
+          double* norm) {
     if (k < 1 || k > kTopK) raise(QCS_ERR_ARG, "top-k supports 1 <= k <= 16");
     const int blocks = kSMs * 2;
     ArgMax* part = nullptr;
-    QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(ArgMax) * blocks * k, st));
-    k_topk_partial<<<blocks, 256, 0, st>>>(amps, dim, k, part);
+    const std::size_t pbytes = sizeof(ArgMax) * blocks * k;
+    QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), pbytes + sizeof(double) * blocks, st));
+    double* psum = norm ? reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(part) + pbytes) : nullptr;
+    k_topk_partial<<<blocks, 256, 0, st>>>(amps, dim, k, part, psum);
     check_launch("k_topk_partial");
     std::vector<ArgMax> h(std::size_t(blocks) * k);
+    std::vector<double> hs(norm ? blocks : 0);
     QCS_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(ArgMax) * h.size(), cudaMemcpyDeviceToHost, st));
+    if (norm) QCS_CUDA(cudaMemcpyAsync(hs.data(), psum, sizeof(double) * blocks, cudaMemcpyDeviceToHost, st));
     QCS_CUDA(cudaFreeAsync(part, st));
     QCS_CUDA(cudaStreamSynchronize(st));
+    if (norm) {
+        double acc = 0.0;
+        for (double v : hs) acc += v;  // fixed block order: deterministic for a given n
+        *norm = std::sqrt(acc);
+    }
     std::vector<ArgMax> c;
     for (const ArgMax& x : h)
         if (x.i != ~u64(0)) c.push_back(x);

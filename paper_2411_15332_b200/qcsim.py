@@ -114,6 +114,9 @@ def gate_known(name: str) -> bool:
         return False
 
 
+_RATIOS = None  # catalog name -> declared zero ratio (the catalog is constant)
+
+
 def gate_catalog_lookup(name: str, params: Sequence[float] = ()) -> GateSpec:
     p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(-1))
     m = np.zeros(64, np.complex128)
@@ -122,7 +125,10 @@ def gate_catalog_lookup(name: str, params: Sequence[float] = ()) -> GateSpec:
     _check(L.lib().qcs_gate_lookup(name.encode(), _dptr(p) if p.size else None, p.size,
                                    m.ctypes.data_as(C.POINTER(C.c_double)), C.byref(ar), C.byref(canon)))
     d = 1 << ar.value
-    ratio = next((g.zero_ratio for g in gate_catalog() if g.name == canon.value.decode()), 0.0)
+    global _RATIOS
+    if _RATIOS is None:
+        _RATIOS = {g.name: g.zero_ratio for g in gate_catalog()}
+    ratio = _RATIOS.get(canon.value.decode(), 0.0)
     return GateSpec(canon.value.decode(), ar.value, list(map(float, p)), m[: d * d].reshape(d, d).copy(), ratio)
 
 
@@ -407,11 +413,26 @@ class DeviceState:
         _check(L.lib().qcs_topk(self._h, k, idx, pr))
         return list(idx), list(pr)
 
+    def summary(self, k: int = 16):
+        """(norm, [top-k indices], [their probabilities]) from one pass over the state; the argmax
+        is the first index.  What render_report needs, without downloading 2^n values."""
+        nrm = C.c_double()
+        idx = (C.c_uint64 * k)()
+        pr = (C.c_double * k)()
+        _check(L.lib().qcs_summary(self._h, k, C.byref(nrm), idx, pr))
+        return nrm.value, list(idx), list(pr)
+
     def gather(self, indices) -> np.ndarray:
         idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
         out = np.empty(idx.size, np.complex128)
         _check(L.lib().qcs_gather(self._h, idx.ctypes.data_as(C.POINTER(C.c_uint64)), idx.size, _dptr(out)))
         return out
+
+    def distance(self, other: "DeviceState"):
+        """(max_i |a_i - b_i|, ||a - b||_2), reduced on the device (no download).  B200-specific."""
+        mx, l2 = C.c_double(), C.c_double()
+        _check(L.lib().qcs_state_distance(self._h, other._h, C.byref(mx), C.byref(l2)))
+        return mx.value, l2.value
 
     # one step at a time
     def apply_step(self, placements: Sequence[Placement]) -> None:

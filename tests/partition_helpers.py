@@ -31,9 +31,16 @@ class OracleBackend:
     def apply_rh(self):
         self._set(self.O.wht(self.n, self.tensor.numpy()))
 
-    def chunk(self, upper, start, count):
-        base = (1 << (self.n - 1)) if upper else 0
-        return self.tensor[base + start: base + start + count]
+    def block(self, k, j, start, count):
+        b = (1 << (self.n - k)) * j + start
+        return self.tensor[b: b + count]
+
+    def swap_peer(self, offset, peer_block, count):
+        """qcs_swap_peer's contract on the CPU."""
+        mine = self.tensor[offset: offset + count]
+        tmp = mine.clone()
+        mine.copy_(peer_block[:count])
+        peer_block[:count].copy_(tmp)
 
     def apply_split(self, peer, self_bit, sel_bits, blocks, skip):
         """qcs_apply_split's contract on the CPU: this rank's half of the pairs, both outputs,
@@ -142,20 +149,18 @@ def gather(states, parts):
 
 
 def circuit_ops(circuit):
-    """Circuit -> flat op list for ShardedState: ('gate', m, qubits, name) / ('diag', f, r) / ('rh',)."""
-    ops = []
-    for st in circuit.steps:
-        if int(st.kind) == 1:
-            ops.append(("diag", list(st.diag.flipped), st.diag.flip_rest))
-        elif st.is_hadamard_all(circuit.n):
-            ops.append(("rh",))
-        else:
-            for p in st.placements:
-                ops.append(("gate", p.gate.matrix, p.qubit_list(), p.gate.name))
-    return ops
+    from paper_2411_15332_b200.partition import circuit_ops as ops
+    return ops(circuit)
 
 
 def run_ops(state, ops):
+    """The whole list through the scheduler (reordering, batched remaps)."""
+    state.run(ops)
+    state.flush()
+
+
+def run_ops_one_by_one(state, ops):
+    """Immediate mode: one operation at a time (no reordering across operations)."""
     for op in ops:
         if op[0] == "gate":
             state.apply_gate(op[1], op[2], op[3])

@@ -1,0 +1,133 @@
+"""Parity at the BASELINE.json sizes (VERDICT r1 "next round" item 1).
+
+- C3 (configs[2]): 30-qubit Grover, 8 iterations, against the closed form of SURVEY.md section 8c
+  (a_marked = sin((2k+1)t), a_other = cos((2k+1)t)/sqrt(2^n - 1), t = asin(2^{-n/2})), which
+  follows the reference's Z0 semantics (circuit.cpp:92).
+- C2 (configs[1]): the 28-qubit single-gate sweep at targets {0, 13, 27} for all 12 gates,
+  bit-exact against the oracle's streaming dax_mvm (oracle/qcs_oracle.c, dax.cpp:96-103).
+- C4 (configs[3]) and the C5 family at n=32 (64 GiB states): no CPU oracle fits, so the default
+  fused engine is checked against the per-gate kernels (each bit-exact against the oracle at
+  n <= 28, test_parity_gpu.py) and against the interpreter kernel (jit mode 0), compared on the
+  device (qcs_state_distance) within the north-star tolerance, plus the norm.
+"""
+import numpy as np
+import pytest
+
+from conftest import bits_equal
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+TOL_AMP = 1e-12
+TOL_L2 = 1e-10
+
+
+@pytest.fixture(scope="module")
+def Q():
+    from paper_2411_15332_b200 import qcsim
+    return qcsim
+
+
+@pytest.fixture(scope="module")
+def cfg():
+    from paper_2411_15332_b200 import configs
+    return configs
+
+
+def free_bytes():
+    import torch
+    free, _ = torch.cuda.mem_get_info(0)
+    return free
+
+
+def test_c3_grover_n30_closed_form(Q, cfg):
+    n, k = 30, 8
+    marked = cfg.c3_marked(n)
+    c = cfg.c3_circuit(n, k)
+    rep = Q.simulate(c, Q.Engine.rh_dax)
+    a_m, a_o = cfg.grover_closed_form(n, k)
+    rng = np.random.default_rng(30)
+    idx = [marked, 0, (1 << n) - 1, marked ^ 1, marked ^ (1 << (n - 1))]
+    idx += [int(v) for v in rng.integers(0, 1 << n, 59)]
+    idx = np.array(idx, np.uint64)
+    got = rep.final.gather(idx)
+    want = np.where(idx == marked, a_m, a_o).astype(np.complex128)
+    assert np.abs(got - want).max() <= TOL_AMP
+    i, p = rep.final.argmax()
+    assert i == marked and abs(p - a_m * a_m) <= 1e-12
+    assert abs(rep.final.norm() - 1.0) <= 1e-12
+    rep.final.close()
+
+
+def test_c2_sweep_n28_sampled_targets_bit_exact(Q, cfg, oracle):
+    n = 28
+    s = Q.DeviceState(n)
+    s.randomize(cfg.seed_of(2))
+    x = s.download()
+    done = set()
+    for g in cfg.c2_sweep(n, seed=cfg.seed_of(2)):
+        if g.qubits[-1] not in (0, 13, 27):
+            continue
+        s.upload(x)
+        s.apply_gate(g.gate, g.qubits)
+        got = s.download()
+        want = oracle.apply_step(n, [(g.qubits, g.gate.matrix)], x)
+        assert bits_equal(got, want), (g.label, g.qubits, float(np.abs(got - want).max()))
+        done.add(g.label)
+        del got, want
+    assert done == set(cfg.C2_GATES)
+    s.close()
+
+
+def per_gate(Q, c, state):
+    """The circuit step by step through the per-gate kernels (one HBM pass per gate, dax_mvm's
+    arithmetic) and the RH butterflies; no fusion across gates."""
+    state.set_basis(c.initial)
+    for st in c.steps:
+        if st.is_hadamard_all(c.n):
+            state.apply_rh()
+        elif int(st.kind) == 1:
+            state.apply_diag(st.diag)
+        else:
+            for p in st.placements:
+                state.apply_gate(p.gate, p.qubit_list())
+
+
+@pytest.mark.parametrize("family", ["c4", "c5"])
+def test_n32_fused_vs_per_gate_vs_interpreter(Q, cfg, family):
+    n = 32
+    if free_bytes() < 2 * (16 << n) + (4 << 30):
+        pytest.skip("two 64 GiB states do not fit")
+    c = cfg.c4_circuit(n) if family == "c4" else cfg.c5_circuit(n, global_qubits=3)
+    a = Q.DeviceState(n)
+    b = Q.DeviceState(n)
+    try:
+        Q.simulate(c, Q.Engine.rh_dax, state=a)  # the default: fused, specialised pass kernels
+        assert abs(a.norm() - 1.0) <= 1e-12
+        per_gate(Q, c, b)
+        mx, l2 = a.distance(b)
+        assert mx <= TOL_AMP and l2 <= TOL_L2, (family, "per-gate", mx, l2)
+        old = Q.jit_mode()
+        try:
+            Q.set_jit_mode(0)  # every pass on the interpreter kernel
+            Q.simulate(c, Q.Engine.rh_dax, state=b)
+        finally:
+            Q.set_jit_mode(old)
+        mx, l2 = a.distance(b)
+        assert mx <= TOL_AMP and l2 <= TOL_L2, (family, "interpreter", mx, l2)
+        # a few amplitudes read back through the ordinary path agree as well
+        idx = np.array([0, 1, 12345, (1 << n) - 1], np.uint64)
+        assert np.abs(a.gather(idx) - b.gather(idx)).max() <= TOL_AMP
+    finally:
+        a.close()
+        b.close()
+
+
+def test_state_distance_small(Q):
+    from conftest import random_state
+    x = random_state(10, 1)
+    y = x.copy()
+    y[17] += 1e-3j
+    a, b = Q.DeviceState.from_numpy(x), Q.DeviceState.from_numpy(y)
+    mx, l2 = a.distance(b)
+    assert abs(mx - 1e-3) < 1e-15 and abs(l2 - 1e-3) < 1e-15
+    assert a.distance(a) == (0.0, 0.0)

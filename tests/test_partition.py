@@ -16,7 +16,7 @@ import torch.multiprocessing as mp
 
 from conftest import ROOT
 from partition_helpers import (OracleBackend, ThreadTransport, circuit_ops, gather, oracle_full, run_ops,
-                               run_ranks)
+                               run_ops_one_by_one, run_ranks)
 
 
 def circuits():
@@ -52,10 +52,80 @@ def test_threads_match_full_state(oracle, world, name):
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name", ["c4", "c5", "grover"])
+def test_threads_one_op_at_a_time(oracle, world, name):
+    """Immediate mode (apply_gate / apply_diag / apply_rh one by one): no reordering across
+    operations, a remap whenever a gate needs a global qubit."""
+    from paper_2411_15332_b200.partition import ShardedState
+    c = circuits()[name]
+    want = oracle_full(oracle, c)
+    hub = ThreadTransport()
+    g = world.bit_length() - 1
+
+    def rank_fn(r):
+        st = ShardedState(c.n, world, r, OracleBackend(c.n - g, oracle), hub.endpoint(r), initial=c.initial,
+                          chunk_elems=5)
+        run_ops_one_by_one(st, circuit_ops(c))
+        return st, st.local_numpy()
+
+    outs = run_ranks(world, rank_fn)
+    assert np.abs(gather([o[0] for o in outs], [o[1] for o in outs]) - want).max() < 1e-12
+
+
+@pytest.mark.parametrize("world,layers", [(2, 2), (4, 2), (8, 3)])
+def test_c4_one_batched_remap_per_layer(oracle, world, layers):
+    """The scheduler runs every gate it can before exchanging (later layers' gates included),
+    then brings the global qubits the waiting gates need down in ONE remap: H^n plus `layers`
+    RY layers cost at most layers + 1 remaps, each moving at most (2^g - 1)/2^g of a shard.
+    (Qubit-at-a-time swaps would cost g half-shard exchanges per layer.)"""
+    from paper_2411_15332_b200 import configs
+    from paper_2411_15332_b200.partition import ShardedState
+    c = configs.c4_circuit(n=9, layers=layers)
+    want = oracle_full(oracle, c)
+    hub = ThreadTransport()
+    g = world.bit_length() - 1
+
+    def rank_fn(r):
+        st = ShardedState(c.n, world, r, OracleBackend(c.n - g, oracle), hub.endpoint(r), chunk_elems=16)
+        run_ops(st, circuit_ops(c))
+        return st, st.local_numpy()
+
+    outs = run_ranks(world, rank_fn)
+    assert np.abs(gather([o[0] for o in outs], [o[1] for o in outs]) - want).max() < 1e-12
+    for st, _ in outs:
+        s = st.exchange_stats()
+        assert 1 <= s["remaps"] <= layers + 1 and s["qubits"] <= g * (layers + 1)
+        shard = 16 << (c.n - g)
+        assert s["bytes_sent"] <= s["remaps"] * shard * (world - 1) // world
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name", ["c4", "c5", "grover"])
+def test_threads_peer_remap_match_full_state(oracle, world, name):
+    """Remaps over mapped partner shards (the CPU model of qcs_swap_peer: each rank of a pair
+    swaps one half of the block pair between two barriers)."""
+    from paper_2411_15332_b200.partition import ShardedState
+    c = circuits()[name]
+    want = oracle_full(oracle, c)
+    hub = ThreadTransport(world, peers=True)
+    g = world.bit_length() - 1
+
+    def rank_fn(r):
+        st = ShardedState(c.n, world, r, OracleBackend(c.n - g, oracle), hub.endpoint(r), initial=c.initial)
+        assert st.peer and st.mode == "remap"
+        run_ops(st, circuit_ops(c))
+        return st, st.local_numpy()
+
+    outs = run_ranks(world, rank_fn)
+    assert np.abs(gather([o[0] for o in outs], [o[1] for o in outs]) - want).max() < 1e-12
+    assert all(o[0].swaps > 0 and o[0].splits == 0 for o in outs)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("name", ["c4", "c5", "grover", "c1"])
 def test_threads_peer_gates_match_full_state(oracle, world, name):
-    """Peer mode: gates mixing only a global qubit run over the partner shard (the CPU model of
-    qcs_apply_split), everything else as before."""
+    """Split mode: gates mixing only a global qubit run over the partner shard (the CPU model of
+    qcs_apply_split), everything else through remaps."""
     from paper_2411_15332_b200.partition import ShardedState
     c = circuits()[name]
     want = oracle_full(oracle, c)
@@ -64,7 +134,7 @@ def test_threads_peer_gates_match_full_state(oracle, world, name):
 
     def rank_fn(r):
         st = ShardedState(c.n, world, r, OracleBackend(c.n - g, oracle), hub.endpoint(r), initial=c.initial,
-                          chunk_elems=7)
+                          chunk_elems=7, mode="split")
         assert st.peer
         run_ops(st, circuit_ops(c))
         return st, st.local_numpy()
@@ -97,7 +167,7 @@ def test_split_blocks_for_controlled_gates(oracle):
     hub = ThreadTransport(world, peers=True)
 
     def rank_fn(r):
-        st = ShardedState(n, world, r, OracleBackend(n - 2, oracle), hub.endpoint(r), chunk_elems=3)
+        st = ShardedState(n, world, r, OracleBackend(n - 2, oracle), hub.endpoint(r), chunk_elems=3, mode="split")
         run_ops(st, circuit_ops(c))
         return st, st.local_numpy()
 
@@ -202,7 +272,7 @@ class _SharedPeerTransport:
         dist.barrier()
 
 
-def _gloo_peer_worker(rank, world, port, name, shards, result_path):
+def _gloo_peer_worker(rank, world, port, name, shards, result_path, mode):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -216,7 +286,8 @@ def _gloo_peer_worker(rank, world, port, name, shards, result_path):
     g = world.bit_length() - 1
     backend = OracleBackend(c.n - g, Oracle)
     backend.tensor = shards[rank]  # this rank's shard is the shared one the partners map
-    st = ShardedState(c.n, world, rank, backend, _SharedPeerTransport(shards), initial=c.initial, chunk_elems=5)
+    st = ShardedState(c.n, world, rank, backend, _SharedPeerTransport(shards), initial=c.initial, chunk_elems=5,
+                      mode=mode)
     assert st.peer
     run_ops(st, circuit_ops(c))
     st.flush()
@@ -228,20 +299,22 @@ def _gloo_peer_worker(rank, world, port, name, shards, result_path):
         full = np.zeros(1 << c.n, dtype=np.complex128)
         for r, mp_ in enumerate(maps):
             full[mp_.numpy()] = shards[r].numpy()
-        np.save(result_path, np.array([full, st.splits], dtype=object), allow_pickle=True)
+        np.save(result_path, np.array([full, st.splits, st.swaps], dtype=object), allow_pickle=True)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,name", [(2, "c4"), (4, "grover"), (2, "c5")])
-def test_gloo_peer_mode_match_full_state(oracle, tmp_path, world, name):
-    """World 2 / 4 processes over gloo in peer mode: gates mixing one global qubit run on the
-    partner's shard directly (mapped through shared memory here, NVLink on the GPU box)."""
+@pytest.mark.parametrize("world,name,mode", [(2, "c4", "split"), (4, "grover", "split"), (2, "c5", "split"),
+                                            (4, "c4", "remap"), (4, "c5", "remap")])
+def test_gloo_peer_mode_match_full_state(oracle, tmp_path, world, name, mode):
+    """World 2 / 4 processes over gloo with the partner shards mapped (through shared memory
+    here, NVLink on the GPU box): split mode runs gates mixing one global qubit on the partner's
+    shard; remap mode swaps remap blocks over the mapping (qcs_swap_peer's contract)."""
     c = circuits()[name]
     g = world.bit_length() - 1
     shards = [torch.zeros(1 << (c.n - g), dtype=torch.complex128).share_memory_() for _ in range(world)]
     path = str(tmp_path / "full.npy")
-    mp.start_processes(_gloo_peer_worker, args=(world, _free_port(), name, shards, path), nprocs=world, join=True,
-                       start_method="spawn")
-    full, splits = np.load(path, allow_pickle=True)
+    mp.start_processes(_gloo_peer_worker, args=(world, _free_port(), name, shards, path, mode), nprocs=world,
+                       join=True, start_method="spawn")
+    full, splits, swaps = np.load(path, allow_pickle=True)
     assert np.abs(full - oracle_full(oracle, c)).max() < 1e-12
-    assert splits > 0
+    assert (splits > 0) if mode == "split" else (swaps > 0 and splits == 0)

@@ -1,6 +1,6 @@
 """The partitioner with real B200 kernels: P ranks emulated by P threads on one GPU, each with
 its own device shard (DeviceBackend: a torch tensor wrapped by qcs_state_wrap) and an
-in-process transport for the pairwise half-shard exchanges.  Compared with the single-GPU
+in-process transport for the remap exchanges.  Compared with the single-GPU
 engine (qcsim.simulate) on the same circuits ('a fake partition running
 P shards on one GPU, which exercises the exchange logic without NVLink')."""
 import numpy as np
@@ -34,10 +34,12 @@ def test_emulated_ranks_match_single_gpu(world):
         assert all(o[0].swaps > 0 for o in outs)
 
 
+@pytest.mark.parametrize("mode", ["split", "remap"])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_emulated_peer_gates_match_single_gpu(world):
-    """Peer mode on one GPU: the P shards are P buffers on the device, so qcs_apply_split's
-    partner loads/stores are plain device accesses (NVLink P2P on a multi-GPU box)."""
+def test_emulated_peer_gates_match_single_gpu(world, mode):
+    """Peer mode on one GPU: the P shards are P buffers on the device, so the partner
+    loads/stores of qcs_apply_split (mode split) and qcs_swap_peer (remaps) are plain device
+    accesses (NVLink P2P on a multi-GPU box)."""
     from paper_2411_15332_b200 import configs
     from paper_2411_15332_b200 import qcsim as Q
     from paper_2411_15332_b200.partition import DeviceBackend, ShardedState
@@ -49,7 +51,7 @@ def test_emulated_peer_gates_match_single_gpu(world):
 
         def rank_fn(r):
             st = ShardedState(c.n, world, r, DeviceBackend(c.n - g), hub.endpoint(r), initial=c.initial,
-                              chunk_elems=1 << 12)
+                              chunk_elems=1 << 12, mode=mode)
             assert st.peer
             run_ops(st, circuit_ops(c))
             return st, st.local_numpy()
@@ -58,7 +60,10 @@ def test_emulated_peer_gates_match_single_gpu(world):
         got = gather([o[0] for o in outs], [o[1] for o in outs])
         assert np.abs(got - want).max() < 1e-12
         assert np.linalg.norm(got - want) < 1e-10
-        assert all(o[0].splits > 0 for o in outs)
+        if mode == "split":
+            assert all(o[0].splits > 0 for o in outs)
+        else:
+            assert all(o[0].swaps > 0 and o[0].splits == 0 for o in outs)
 
 
 @pytest.mark.parametrize("world", [2, 4])
@@ -109,7 +114,7 @@ def test_split_gate_bit_exact():
 
         def rank_fn(r):
             import torch
-            st = ShardedState(n, world, r, DeviceBackend(n - 2), hub.endpoint(r))
+            st = ShardedState(n, world, r, DeviceBackend(n - 2), hub.endpoint(r), mode="split")
             local = x.reshape(world, -1)[r]
             st.backend.tensor.copy_(torch.from_numpy(local.copy()))
             st.apply_gate(gate.matrix, qubits, gate.name)
