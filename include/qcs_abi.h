@@ -153,6 +153,13 @@ int qcs_swap_peer(qcs_state* s, uint64_t offset, void* peer_amps, uint64_t count
 /* rh_mvm(rh_build(n), s) (rh.hpp:64-66): H^{(x)n} as a Walsh-Hadamard butterfly, scaled once
  * by exp2(-n/2) (rh.cpp:20).  Within 1e-12 of the reference (whose own error is larger). */
 int qcs_apply_rh(qcs_state* s);
+/* rh_mvm(RhMatrix{n, value}, s, method, stats, block_size) (rh.hpp:64-66, rh.cpp:92-156) in place:
+ * s <- value * H^(x)n s (scale first, then the butterflies).  sign_count / madd_count (optional)
+ * receive RhMvmStats as the reference's counters total them (madd = 4 * (2^(n-1))^2; signs per
+ * method, the Table-2 formulas).  Errors as the reference: n < 1 or n != the state's qubit count
+ * -> QCS_ERR_DIMENSION; an invalid block size for QCS_SIGN_BLOCK -> QCS_ERR_SIM (rh.cpp:58). */
+int qcs_rh_mvm(qcs_state* s, int n, double value, int sign_method, uint64_t block_size, uint64_t* sign_count,
+               uint64_t* madd_count);
 
 /* ------------------------------------------------------------------ reductions
  * StateVector::norm / probabilities (core.cpp:30-40). */
@@ -172,6 +179,13 @@ int qcs_state_distance(qcs_state* a, qcs_state* b, double* max_abs, double* l2);
  * probabilities, core.cpp:30-34) and the k <= 16 largest probabilities as qcs_topk gives them
  * (indices[0] is the argmax).  Host outputs; synchronous. */
 int qcs_summary(qcs_state* s, int k, double* norm, uint64_t* indices, double* probabilities);
+/* render_report's seeded sampling (circuit_io.cpp:114-128), index-exact: std::mt19937_64(seed),
+ * `count` draws of uniform_real_distribution<double>(0, acc), each the std::lower_bound of the
+ * draw in the SEQUENTIAL rounded prefix sum of the probabilities (acc += p_i).  The device
+ * reproduces that rounded chain exactly (binade-wise integer walk + serial replay of the chunks
+ * where the sum changes binade, csrc/sample_kernels.cu) without moving 2^n values to the host.
+ * out: host, count indices; total (optional): the final acc.  Synchronous. */
+int qcs_sample(qcs_state* s, uint64_t seed, uint64_t count, uint64_t* out, double* total);
 /* amplitudes at arbitrary indices (host index list, host output 2*count doubles) */
 int qcs_gather(qcs_state* s, const uint64_t* indices, uint64_t count, double* out);
 

@@ -2,6 +2,7 @@
 // golden-fixture generator.  TEST INFRASTRUCTURE ONLY: marshalling around the unmodified
 // reference functions parse_circuit_json, simulate and render_report.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -62,6 +63,38 @@ long io_gate_expression(const char* expr, double* out, long cap_doubles) {
         if (long(m.data.size()) * 2 > cap_doubles) return -100;
         std::memcpy(out, m.data.data(), sizeof(cplx) * m.data.size());
         return long(m.rows);
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return -code_of(ex);
+    }
+}
+
+// render_report's sampling (circuit_io.cpp:114-128) on a given state: the unmodified
+// render_report (human format) runs on a report whose final state and probabilities are the
+// given amplitudes, and its "samples (seed S): ..." line is parsed back into out.
+// Returns the number of samples, or -(code) on a reference exception.
+long io_sample(int n, const double* amps, int samples, unsigned long long seed, unsigned long long* out) {
+    try {
+        SimReport r;
+        r.final = StateVector(n);
+        std::memcpy(r.final.amps.data(), amps, sizeof(cplx) * r.final.amps.size());
+        r.probabilities = r.final.probabilities();
+        ReportOptions o;
+        o.format = "human";
+        o.samples = samples;
+        o.seed = seed;
+        o.engine = "dax";
+        const std::string rep = render_report(r, n, o);
+        const std::size_t at = rep.find("samples (seed ");
+        if (at == std::string::npos) return 0;
+        const char* p = rep.c_str() + rep.find("):", at) + 2;
+        long k = 0;
+        char* end = nullptr;
+        for (; k < samples; ++k, p = end) {
+            out[k] = std::strtoull(p, &end, 10);
+            if (end == p) break;
+        }
+        return k;
     } catch (const std::exception& ex) {
         g_err = ex.what();
         return -code_of(ex);

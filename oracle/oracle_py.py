@@ -25,6 +25,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libqcsim_ref.so")
+IO_SO = os.path.join(HERE, "_ref", "libqcsim_io.so")
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _cp = np.ctypeslib.ndpointer(dtype=np.complex128, flags="C_CONTIGUOUS")
@@ -209,6 +210,8 @@ class Reference:
             L.ref_canonical_params.argtypes = [C.c_char_p, _dp, C.POINTER(C.c_int)]
             L.ref_step_dax.restype = C.c_long
             L.ref_step_dax.argtypes = [C.c_int, C.c_int, _ip, _ip, _cp, _u64p, _u64p, _cp, C.c_long]
+            L.ref_step_dump.restype = C.c_long
+            L.ref_step_dump.argtypes = [C.c_int, C.c_int, _ip, _ip, _cp, C.c_int, C.c_char_p, C.c_long]
             L.ref_step_das.restype = C.c_long
             L.ref_step_das.argtypes = [C.c_int, C.c_int, _ip, _ip, _cp, _u64p, _u8p, _cp, C.c_long]
             L.ref_apply_step.argtypes = [C.c_int, C.c_int, _ip, _ip, _cp, C.c_int, _cp, _cp,
@@ -294,6 +297,22 @@ class Reference:
         if cnt < 0:
             raise OracleError(f"ref_step_das rc={cnt}: {L.ref_last_error().decode()}")
         return dis[:cnt].copy(), last[:cnt].copy(), vals[:cnt].copy()
+
+    @classmethod
+    def step_dump(cls, n, placements, das=False):
+        """dax_dump(step_matrix_dax(step)) / das_dump(step_matrix_das(step)) bytes (native steps)."""
+        L = cls.lib()
+        npl, ar, qb, mt = flatten_placements(placements)
+        cap = 28
+        ent = 1
+        for q, _ in placements:
+            ent *= 1 << len(q)
+        cap += (24 if das else 32) * (ent << n)
+        buf = C.create_string_buffer(cap)
+        k = L.ref_step_dump(n, npl, ar, qb, mt, 1 if das else 0, buf, cap)
+        if k < 0:
+            raise OracleError(f"ref_step_dump rc={k}: {L.ref_last_error().decode()}")
+        return buf.raw[:k]
 
     @classmethod
     def apply_step(cls, n, placements, state, engine="dax"):
@@ -408,3 +427,84 @@ class Reference:
     @classmethod
     def quadrant_sign(cls, r, c, n):
         return cls.lib().ref_quadrant_sign(r, c, n)
+
+
+class ReferenceIO:
+    """The reference's front end (oracle/_ref/libqcsim_io.so: circuit_io.cpp + the engine)."""
+
+    _lib = None
+
+    @staticmethod
+    def available():
+        return os.path.exists(IO_SO)
+
+    @classmethod
+    def lib(cls):
+        if cls._lib is None:
+            if not cls.available():
+                raise OracleError(f"{IO_SO} missing: build with `make -C oracle io` where /root/reference exists")
+            L = C.CDLL(IO_SO)
+            L.io_last_error.restype = C.c_char_p
+            L.io_sample.restype = C.c_long
+            L.io_sample.argtypes = [C.c_int, _cp, C.c_int, C.c_ulonglong, _u64p]
+            cls._lib = L
+        return cls._lib
+
+    @classmethod
+    def sample(cls, n, amps, count, seed):
+        """render_report's samples (circuit_io.cpp:114-128) for the state `amps`."""
+        out = np.zeros(max(count, 1), np.uint64)
+        k = cls.lib().io_sample(n, np.ascontiguousarray(amps, np.complex128), count, seed, out)
+        if k < 0:
+            raise OracleError(f"io_sample rc={k}: {cls.lib().io_last_error().decode()}")
+        return [int(x) for x in out[:k]]
+
+
+# ------------------------------------------------------------ sampling restatement (pure Python)
+class MT19937_64:
+    """std::mt19937_64 (the reference seeds it with the report seed, circuit_io.cpp:116)."""
+
+    def __init__(self, seed: int):
+        self.mt = [0] * 312
+        self.mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+        self.i = 312
+
+    def __call__(self) -> int:
+        if self.i >= 312:
+            mt = self.mt
+            for k in range(312):
+                y = (mt[k] & 0xFFFFFFFF80000000) | (mt[(k + 1) % 312] & 0x7FFFFFFF)
+                v = mt[(k + 156) % 312] ^ (y >> 1)
+                if y & 1:
+                    v ^= 0xB5026F5AA96619E9
+                mt[k] = v
+            self.i = 0
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & 0xFFFFFFFFFFFFFFFF
+
+
+def _uniform(rng, hi):
+    """uniform_real_distribution<double>(0, hi) over generate_canonical<double, 53> (libstdc++)."""
+    import math
+    c = float(rng()) / 18446744073709551616.0
+    if c >= 1.0:
+        c = math.nextafter(1.0, 0.0)
+    return (hi - 0.0) * c + 0.0
+
+
+def sequential_sample(probs, count, seed):
+    """circuit_io.cpp:114-128 restated: sequential rounded CDF, lower_bound per draw."""
+    rng = MT19937_64(seed)
+    cdf = np.empty(len(probs), np.float64)
+    acc = 0.0
+    for i, p in enumerate(np.asarray(probs, np.float64).tolist()):
+        acc += p
+        cdf[i] = acc
+    return [int(np.searchsorted(cdf, _uniform(rng, acc), side="left")) for _ in range(count)], acc

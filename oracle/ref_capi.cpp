@@ -14,6 +14,7 @@
 #include <random>
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -252,6 +253,30 @@ long ref_step_das(int n, int np, const int* arity, const int* qubits, const doub
             vals[2 * i + 1] = m.entries[i].value.imag();
         }
         return long(m.entries.size());
+    } catch (const std::exception& e) {
+        return -10 - fail(e);
+    }
+}
+
+// step_matrix_dax / step_matrix_das of native placements, serialised by the reference's own
+// dax_dump / das_dump (dax.cpp:107-118, das.cpp:154-165).  das: 0 = DAX1, 1 = DAS1.  Returns the
+// byte count (or -(bytes) when cap is too small).
+long ref_step_dump(int n, int np, const int* arity, const int* qubits, const double* mats, int das,
+                   unsigned char* out, long cap) {
+    try {
+        const auto ps = read_placements(np, arity, qubits, mats, nullptr);
+        std::vector<Placement> pl;
+        for (const auto& p : ps) {
+            if (!p.contiguous) throw SimError("dump oracle needs contiguous placements");
+            pl.push_back({spec_of(p), p.q[0]});
+        }
+        std::ostringstream os;
+        if (das) das_dump(step_matrix_das(CircuitStep::of_gates(pl), n), os);
+        else dax_dump(step_matrix_dax(CircuitStep::of_gates(pl), n), os);
+        const std::string b = os.str();
+        if (long(b.size()) > cap) return -long(b.size());
+        std::memcpy(out, b.data(), b.size());
+        return long(b.size());
     } catch (const std::exception& e) {
         return -10 - fail(e);
     }

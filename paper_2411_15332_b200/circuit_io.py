@@ -6,9 +6,9 @@
 * ``parse_gate_expression`` (circuit_io.cpp:85-107): catalog gates joined by ``x`` / ``*``;
 * ``render_report`` (circuit_io.cpp:109-203): human / JSON / CSV, key-ordered, with seeded
   sampling.  The JSON layout and number formatting follow nlohmann::ordered_json::dump(2); the
-  samples use the same generator chain as the reference (std::mt19937_64 ->
-  generate_canonical<double, 53> -> uniform_real_distribution(0, total) -> lower_bound on the
-  sequential CDF), so equal probabilities give equal samples.
+  samples come from the device (qcs_sample): the reference's generator chain (std::mt19937_64 ->
+  uniform_real_distribution(0, acc) -> lower_bound) on an exact reproduction of its sequential
+  rounded CDF, so equal probabilities give equal samples and no 2^n values are downloaded.
 
 Probabilities, argmax and the norm come from the device (qcs_probabilities is bit-exact; large
 states report argmax and top-16 without downloading the state, as the reference does above 2^16
@@ -153,58 +153,6 @@ def parse_gate_expression(expr: str) -> np.ndarray:  # circuit_io.cpp:85-107
     return acc
 
 
-# ---------------------------------------------------------------- sampling (bit-compatible)
-class MT19937_64:
-    """std::mt19937_64 (the reference seeds it with the report seed, circuit_io.cpp:116)."""
-
-    def __init__(self, seed: int):
-        self.mt = [0] * 312
-        self.mt[0] = seed & 0xFFFFFFFFFFFFFFFF
-        for i in range(1, 312):
-            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
-        self.i = 312
-
-    def __call__(self) -> int:
-        if self.i >= 312:
-            mt = self.mt
-            for k in range(312):
-                y = (mt[k] & 0xFFFFFFFF80000000) | (mt[(k + 1) % 312] & 0x7FFFFFFF)
-                v = mt[(k + 156) % 312] ^ (y >> 1)
-                if y & 1:
-                    v ^= 0xB5026F5AA96619E9
-                mt[k] = v
-            self.i = 0
-        y = self.mt[self.i]
-        self.i += 1
-        y ^= (y >> 29) & 0x5555555555555555
-        y ^= (y << 17) & 0x71D67FFFEDA60000
-        y ^= (y << 37) & 0xFFF7EEE000000000
-        y ^= y >> 43
-        return y & 0xFFFFFFFFFFFFFFFF
-
-
-def _uniform(rng: MT19937_64, hi: float) -> float:
-    """uniform_real_distribution<double>(0, hi) over generate_canonical<double, 53> (libstdc++)."""
-    c = float(rng()) / 18446744073709551616.0
-    if c >= 1.0:
-        c = math.nextafter(1.0, 0.0)
-    return (hi - 0.0) * c + 0.0
-
-
-def sample(probs: np.ndarray, count: int, seed: int) -> List[int]:  # circuit_io.cpp:114-128
-    rng = MT19937_64(seed)
-    cdf = np.empty(probs.size, np.float64)
-    acc = 0.0
-    for i, p in enumerate(probs.tolist()):  # sequential, as the reference accumulates
-        acc += p
-        cdf[i] = acc
-    out = []
-    for _ in range(count):
-        u = _uniform(rng, acc)
-        out.append(int(np.searchsorted(cdf, u, side="left")))
-    return out
-
-
 # ---------------------------------------------------------------- rendering
 def _num(x: float) -> str:
     """nlohmann::json number formatting: shortest round-trip digits, '.0' for integral values,
@@ -264,7 +212,7 @@ def render_report(report: Q.SimReport, n: int, opts: ReportOptions) -> str:  # c
     dim = 1 << n
     small = dim <= (1 << 16)
     state = report.final
-    probs = report.probabilities if (small or opts.samples > 0) else None
+    probs = report.probabilities if small else None
     if probs is not None:
         argmax = int(np.argmax(probs))
         pmax = float(probs[argmax])
@@ -275,7 +223,9 @@ def render_report(report: Q.SimReport, n: int, opts: ReportOptions) -> str:  # c
         norm = math.sqrt(_seq_norm2(amps))
     else:
         norm = state.norm()
-    samples = sample(probs, opts.samples, opts.seed) if opts.samples > 0 else []
+    # drawn on the device against the reference's exact sequential CDF (qcs_sample): nothing of
+    # size 2^n is downloaded for the samples
+    samples = state.sample(opts.samples, opts.seed)[0] if opts.samples > 0 else []
 
     if opts.format == "json":
         j = {"qubits": n, "engine": opts.engine, "argmax": argmax, "max_probability": pmax, "norm": norm}

@@ -302,6 +302,14 @@ int qcs_apply_rh(qcs_state* s) {
     });
 }
 
+int qcs_rh_mvm(qcs_state* s, int n, double value, int sign_method, uint64_t block_size, uint64_t* sign_count,
+               uint64_t* madd_count) {
+    return guarded([&] {
+        need(s, "state");
+        qcs::rh_mvm(s, n, value, sign_method, block_size, sign_count, madd_count);
+    });
+}
+
 // ---------------------------------------------------------------- reductions
 
 int qcs_norm(qcs_state* s, double* out) {
@@ -375,6 +383,15 @@ int qcs_summary(qcs_state* s, int k, double* norm, uint64_t* indices, double* pr
         need(probabilities, "probabilities");
         qcs::DeviceGuard g(s->device);
         qcs::topk(s->amps, uint64_t(1) << s->n, k, indices, probabilities, s->stream, norm);
+    });
+}
+
+int qcs_sample(qcs_state* s, uint64_t seed, uint64_t count, uint64_t* out, double* total) {
+    return guarded([&] {
+        need(s, "state");
+        if (count) need(out, "out");
+        qcs::DeviceGuard g(s->device);
+        qcs::sample(s->amps, uint64_t(1) << s->n, seed, count, out, total, s->stream);
     });
 }
 

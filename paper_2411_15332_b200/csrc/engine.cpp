@@ -407,16 +407,16 @@ void run_fused(qcs_state* s, const std::vector<FOp>& ops, std::int64_t* init = n
     execute_fused(s, ops, low, init);
 }
 
-std::vector<FOp> rh_ops(int n) {
+std::vector<FOp> rh_ops(int n, double value) {
     std::vector<FOp> ops;
-    ops.push_back(make_scale(std::exp2(-0.5 * n)));  // rh_build (rh.cpp:20), scale first (rh.cpp:99-100)
+    ops.push_back(make_scale(value));  // rh_build's magnitude (rh.cpp:20), scale first (rh.cpp:99-100)
     for (int b = 0; b < n; ++b) ops.push_back(make_wht(b));
     return ops;
 }
 
 void append_step_ops(int n, const qcs_step& st, bool rh, std::vector<FOp>& ops) {
     if (rh) {
-        auto r = rh_ops(n);
+        auto r = rh_ops(n, std::exp2(-0.5 * n));
         ops.insert(ops.end(), r.begin(), r.end());
     } else if (st.kind == QCS_STEP_DIAG) {
         const bool any = st.flip_rest || st.num_flipped;
@@ -434,7 +434,22 @@ void append_step_ops(int n, const qcs_step& st, bool rh, std::vector<FOp>& ops) 
 void apply_rh(qcs_state* s) {
     DeviceGuard g(s->device);
     TimerScope ts(s);
-    run_fused(s, rh_ops(s->n));
+    run_fused(s, rh_ops(s->n, std::exp2(-0.5 * s->n)));
+}
+
+u64 rh_sign_count(int n, int method, u64 block);
+
+void rh_mvm(qcs_state* s, int n, double value, int method, u64 block, u64* sign_count, u64* madd_count) {
+    // rh.cpp:92-96: the checks, in the reference's order
+    if (n < 1) raise(QCS_ERR_DIMENSION, "RH MVM needs n >= 1");
+    if (s->n != n) raise(QCS_ERR_DIMENSION, "RH MVM qubit count mismatch");
+    const u64 half = u64(1) << (n - 1);
+    const u64 signs = rh_sign_count(n, method, block);  // raises the block-size SimError (rh.cpp:58)
+    DeviceGuard g(s->device);
+    TimerScope ts(s);
+    run_fused(s, rh_ops(n, value));
+    if (sign_count) *sign_count = signs;
+    if (madd_count) *madd_count = 4 * half * half;  // rh.cpp:153
 }
 
 // ------------------------------------------------------------------ simulate
@@ -498,6 +513,8 @@ u64 optimal_block_size(int n) {  // rh.cpp:68-75
     return best;
 }
 
+}  // namespace
+
 // rh_mvm's sign counter totals per method (rh.cpp:110-154; the Table-2 formulas of
 // qcsim_cli.cpp:109-118), with the reference's u64 arithmetic.
 u64 rh_sign_count(int n, int method, u64 block) {
@@ -516,8 +533,6 @@ u64 rh_sign_count(int n, int method, u64 block) {
         default: raise(QCS_ERR_ARG, "unknown sign method");
     }
 }
-
-}  // namespace
 
 std::atomic<std::uint64_t> g_plan_ids{0};
 

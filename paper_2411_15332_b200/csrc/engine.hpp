@@ -56,6 +56,7 @@ bool build_gate_desc(const GateOp& op, GateDesc& d);
 void apply_step(qcs_state* s, const qcs_placement* p, int count);
 void apply_diag(qcs_state* s, const u64* flipped, u64 count, int flip_rest);
 void apply_rh(qcs_state* s);
+void rh_mvm(qcs_state* s, int n, double value, int method, u64 block, u64* sign_count, u64* madd_count);
 
 void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
               qcs_step_report* reports);

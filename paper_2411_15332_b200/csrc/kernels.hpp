@@ -238,6 +238,9 @@ void argmax(const double2* amps, std::uint64_t dim, std::uint64_t* idx, double* 
 // state's norm from the same pass (sqrt of the summed probabilities)
 void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st,
           double* norm = nullptr);
+// seeded sampling with the reference's sequential CDF (sample_kernels.cu)
+void sample(const double2* amps, std::uint64_t dim, std::uint64_t seed, std::uint64_t count, std::uint64_t* out,
+            double* total, cudaStream_t st);
 void gather(const double2* amps, const std::uint64_t* idx_dev, std::uint64_t count, double2* out_dev,
             cudaStream_t st);
 void scale(double2* amps, std::uint64_t dim, double s, cudaStream_t st);

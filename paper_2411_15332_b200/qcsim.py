@@ -422,6 +422,15 @@ class DeviceState:
         _check(L.lib().qcs_summary(self._h, k, C.byref(nrm), idx, pr))
         return nrm.value, list(idx), list(pr)
 
+    def sample(self, count: int, seed: int):
+        """render_report's seeded samples (circuit_io.cpp:114-128), drawn on the device: returns
+        ([indices], acc) with acc the sequential sum of the probabilities.  Index-exact against
+        the reference (the device reproduces its rounded sequential CDF)."""
+        out = (C.c_uint64 * max(count, 1))()
+        tot = C.c_double()
+        _check(L.lib().qcs_sample(self._h, seed & 0xFFFFFFFFFFFFFFFF, count, out, C.byref(tot)))
+        return list(out)[:count], tot.value
+
     def gather(self, indices) -> np.ndarray:
         idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
         out = np.empty(idx.size, np.complex128)

@@ -17,25 +17,14 @@
 
 #include "qcs_abi.h"
 #include "qcsim/engine.hpp"
+#include "shim_common.hpp"
 
 namespace qcsim {
 
+using b200::check;
+using b200::rethrow;
+
 namespace {
-
-[[noreturn]] void rethrow(int rc) {
-    const std::string msg = qcs_last_error();
-    switch (rc) {
-        case QCS_ERR_CAPACITY: throw CapacityError(msg);
-        case QCS_ERR_DIMENSION: throw DimensionError(msg);
-        case QCS_ERR_ENCODING: throw EncodingError(msg);
-        case QCS_ERR_PARSE: throw ParseError(msg);
-        default: throw SimError(msg);
-    }
-}
-
-void check(int rc) {
-    if (rc != QCS_OK) rethrow(rc);
-}
 
 // CircuitStep list -> qcs_step list (the vectors keep the pointed-to storage alive)
 struct Marshalled {
@@ -210,21 +199,25 @@ DasMatrix step_matrix_das(const CircuitStep& step, int n) {
     return out;
 }
 
-// simulate (engine.cpp:153-210) on the GPU: same dispatch, same StepReport accounting.
+// simulate (engine.cpp:153-210) on the GPU: same dispatch, same StepReport accounting.  The
+// device state is kept per thread and per qubit count between calls (shim_common.hpp), so a
+// repeated circuit reuses its lowered plan, specialised kernels and uploaded tables (the state's
+// plan cache) and no 2^n allocation happens per call; |initial> is written by the first pass.
 SimReport simulate(const Circuit& c, Engine engine, const SimOptions& opts) {
     c.validate();
     std::vector<const CircuitStep*> ptrs;
     for (const CircuitStep& s : c.steps) ptrs.push_back(&s);
     Marshalled m;
     marshal(ptrs, m);
-    qcs_state* st = nullptr;
-    check(qcs_state_create(c.n, Device{}.id, c.initial, &st));
     SimReport report;
-    try {
+    {
+        qcs_state* st = b200::pool().get(b200::kSimulate, c.n);
         qcs_sim_options o{};
         o.sign_method = int(opts.sign_method);
         o.block_size = opts.block_size;
         o.fuse = 1;
+        o.reset = 1;
+        o.initial = c.initial;
         std::vector<qcs_step_report> reps(c.steps.size());
         check(qcs_simulate(st, m.steps.data(), int(m.steps.size()), int(engine), &o, reps.data()));
         for (const qcs_step_report& r : reps) {
@@ -238,11 +231,7 @@ SimReport simulate(const Circuit& c, Engine engine, const SimOptions& opts) {
         check(qcs_state_download(st, reinterpret_cast<double*>(report.final.amps.data()), 0, dim));
         report.probabilities.resize(dim);
         check(qcs_probabilities(st, report.probabilities.data(), QCS_MEM_HOST));
-    } catch (...) {
-        qcs_state_destroy(st);
-        throw;
     }
-    qcs_state_destroy(st);
     return report;
 }
 

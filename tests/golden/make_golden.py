@@ -114,10 +114,16 @@ def main():
         d_, l_, dv_ = R.step_das(n, plc)
         s = R.random_unit_state(n, 5000 + t)
         o, _, _ = R.apply_step(n, plc, s)
+        # the reference's own DAX1 / DAS1 serialisation of the same steps (dax.cpp:107-118,
+        # das.cpp:154-165), hashed: the byte-level parity surface of SURVEY.md section 8f row 2
+        dump_x = R.step_dump(n, plc, das=False)
+        dump_s = R.step_dump(n, plc, das=True)
         recs.append(dict(n=n, names=[x[0] for x in pl], qubits=[x[1] for x in pl], seed=5000 + t,
                          dax=sha(np.concatenate([r_, c_, v_.view(np.uint64)])),
                          das=sha(np.concatenate([d_, l_.astype(np.uint64), dv_.view(np.uint64)])),
-                         count=len(r_), mvm=sha(o)))
+                         count=len(r_), mvm=sha(o),
+                         dax_dump=hashlib.sha256(dump_x).hexdigest(), dax_dump_len=len(dump_x),
+                         das_dump=hashlib.sha256(dump_s).hexdigest(), das_dump_len=len(dump_s)))
     with open(os.path.join(HERE, "steps.json"), "w") as f:
         json.dump(recs, f, indent=0)
     print("golden fixtures written")

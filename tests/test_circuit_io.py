@@ -40,7 +40,7 @@ def test_parse_matches_structure(io):
 
 
 def test_mt19937_64_and_canonical():
-    from paper_2411_15332_b200.circuit_io import MT19937_64
+    from oracle.oracle_py import MT19937_64
     r = MT19937_64(5489)  # the C++ standard's check value: the 10000th draw of a default engine
     for _ in range(9999):
         r()
@@ -87,3 +87,21 @@ def test_render_report_matches_reference(io):
             assert len(lg) == len(lr)
             assert [x for x in lg if "probab" not in x and "norm" not in x] == \
                    [x for x in lr if "probab" not in x and "norm" not in x]
+
+
+def test_sampling_restatement_pinned_to_reference():
+    """oracle_py.sequential_sample (the Python restatement the device sampler is checked against)
+    equals the reference's render_report samples (circuit_io.cpp:114-128), ties included."""
+    from oracle.oracle_py import ReferenceIO, sequential_sample
+    if not ReferenceIO.available():
+        pytest.skip("oracle/_ref/libqcsim_io.so not built")
+    rng = np.random.default_rng(3)
+    for n in (4, 9, 12):
+        x = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+        x /= np.linalg.norm(x)
+        p = x.real * x.real + x.imag * x.imag
+        assert ReferenceIO.sample(n, x, 300, 17 + n) == sequential_sample(p, 300, 17 + n)[0]
+    x = np.full(1 << 10, complex(3 * 2.0 ** -27, 4 * 2.0 ** -27))
+    x[0] = complex(0.5, 0.5)
+    p = x.real * x.real + x.imag * x.imag
+    assert ReferenceIO.sample(10, x, 200, 1) == sequential_sample(p, 200, 1)[0]

@@ -158,6 +158,12 @@ def test_oracle_matches_reference_step_bytes(oracle, golden):
         assert sha(rr, cc, vv) == r["dax"]
         d, l, v = oracle.step_das(r["n"], pl)
         assert sha(d, l.astype(np.uint64), v) == r["das"]
+        # the host DAX1 / DAS1 writers on the oracle's entries == the reference's dump bytes
+        dim = 1 << r["n"]
+        bx = Q.dax_dump(Q.DaxMatrix(dim, dim, rr, cc, vv))
+        bs = Q.das_dump(Q.DasMatrix(dim, dim, d, l, v))
+        assert hashlib.sha256(bx).hexdigest() == r["dax_dump"] and len(bx) == r["dax_dump_len"]
+        assert hashlib.sha256(bs).hexdigest() == r["das_dump"] and len(bs) == r["das_dump_len"]
 
 
 def test_oracle_grover_and_c1(oracle, golden):

@@ -269,6 +269,35 @@ def test_encoder_bytes_vs_oracle_and_golden(Q, oracle):
         assert sha(d.row, d.col, d.value) == r["dax"]
         s = Q.step_matrix_das(st, r["n"])
         assert sha(s.dis, s.last_in_row.astype(np.uint64), s.value) == r["das"]
+        # DAX1 / DAS1 dumps of the device-encoded steps, byte for byte the reference's dax_dump /
+        # das_dump of the same steps (dax.cpp:107-118, das.cpp:154-165)
+        bx, bs = Q.dax_dump(d), Q.das_dump(s)
+        assert len(bx) == r["dax_dump_len"] and hashlib.sha256(bx).hexdigest() == r["dax_dump"]
+        assert len(bs) == r["das_dump_len"] and hashlib.sha256(bs).hexdigest() == r["das_dump"]
+        assert Q.dax_dump(Q.dax_load(bx)) == bx and Q.das_dump(Q.das_load(bs)) == bs
+
+
+def test_dumps_vs_live_reference(Q):
+    """Bigger steps than the fixtures (n up to 14, 1-3 qubit gates with gaps): the device encoder's
+    dumps equal the compiled reference's dax_dump / das_dump bytes (oracle/_ref, when shipped)."""
+    from oracle.oracle_py import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref/libqcsim_ref.so not shipped")
+    rng = np.random.default_rng(21)
+    cat = Q.gate_catalog()
+    for t in range(12):
+        n = int(rng.integers(9, 15))
+        pl, q = [], 0
+        while q < n:
+            ar = 1 + int(rng.integers(0, min(n - q, 3)))
+            fits = [c for c in cat if c.arity == ar]
+            info = fits[int(rng.integers(0, len(fits)))]
+            pl.append(Q.Placement(Q.gate_catalog_lookup(info.name, Q.canonical_params(info.name)), q))
+            q += ar + int(rng.integers(0, 3))
+        st = Q.CircuitStep.of_gates(pl)
+        ref_pl = [(p.qubit_list(), p.gate.matrix) for p in pl]
+        assert Q.dax_dump(Q.step_matrix_dax(st, n)) == Reference.step_dump(n, ref_pl, das=False), t
+        assert Q.das_dump(Q.step_matrix_das(st, n)) == Reference.step_dump(n, ref_pl, das=True), t
 
 
 def test_encoder_general_placements_and_mvm(Q, oracle):
