@@ -35,6 +35,8 @@
  * Complex numbers are interleaved double pairs (re, im), the byte layout of
  * std::complex<double>.  Qubit q is bit (n-1-q) of the basis index (core.hpp:64-66).
  */
+#include <pthread.h>
+#include <unistd.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -237,28 +239,78 @@ long orc_step_row_capacity(int n, int np, const int* arity, const int* qubits, c
  * ascending column order of value * in[col], accumulated from (0,0) (dax.cpp:98-101).
  * in/out are 2*2^n doubles and must not alias.
  */
+struct apply_job {
+    const orc_step* st;
+    const double* in;
+    double* out;
+    uint64_t r0, r1;
+    long cap;
+    int rc;
+};
+
+static void* apply_rows(void* arg) {
+    struct apply_job* j = (struct apply_job*)arg;
+    orc_entry* buf = (orc_entry*)malloc(sizeof(orc_entry) * (size_t)j->cap);
+    if (!buf) { j->rc = ORC_ERR_CAPACITY; return NULL; }
+    for (uint64_t r = j->r0; r < j->r1; ++r) {
+        const long cnt = row_entries(j->st, r, buf, j->cap);
+        double ar = 0.0, ai = 0.0;
+        for (long e = 0; e < cnt; ++e) {
+            double pr, pi;
+            cmul(buf[e].re, buf[e].im, j->in[2 * buf[e].col], j->in[2 * buf[e].col + 1], &pr, &pi);
+            ar = ar + pr;
+            ai = ai + pi;
+        }
+        j->out[2 * r] = ar;
+        j->out[2 * r + 1] = ai;
+    }
+    free(buf);
+    j->rc = ORC_OK;
+    return NULL;
+}
+
+/* Worker threads for the row loop of orc_apply_step: ORC_THREADS, else the online cores (<= 64).
+ * Rows are independent and each row's arithmetic is unchanged, so the result is the same bytes
+ * at any thread count (the reference's per-row accumulation order, dax.cpp:98-101). */
+static int apply_threads(uint64_t dim) {
+    const char* v = getenv("ORC_THREADS");
+    long t = v ? atol(v) : sysconf(_SC_NPROCESSORS_ONLN);
+    if (t < 1) t = 1;
+    if (t > 64) t = 64;
+    if (dim < ((uint64_t)1 << 16)) t = 1;
+    return (int)t;
+}
+
 int orc_apply_step(int n, int np, const int* arity, const int* qubits, const double* mats,
                    const double* in, double* out) {
     orc_step st;
     int rc = build_step(n, np, arity, qubits, mats, &st);
     if (rc != ORC_OK) return rc;
     const long cap = row_capacity(&st);
-    orc_entry* buf = (orc_entry*)malloc(sizeof(orc_entry) * (size_t)cap);
-    if (!buf) return ORC_ERR_CAPACITY;
     const uint64_t dim = (uint64_t)1 << n;
-    for (uint64_t r = 0; r < dim; ++r) {
-        const long cnt = row_entries(&st, r, buf, cap);
-        double ar = 0.0, ai = 0.0;
-        for (long e = 0; e < cnt; ++e) {
-            double pr, pi;
-            cmul(buf[e].re, buf[e].im, in[2 * buf[e].col], in[2 * buf[e].col + 1], &pr, &pi);
-            ar = ar + pr;
-            ai = ai + pi;
-        }
-        out[2 * r] = ar;
-        out[2 * r + 1] = ai;
+    const int nt = apply_threads(dim);
+    struct apply_job jobs[64];
+    pthread_t tid[64];
+    for (int t = 0; t < nt; ++t) {
+        jobs[t].st = &st;
+        jobs[t].in = in;
+        jobs[t].out = out;
+        jobs[t].r0 = dim / (uint64_t)nt * (uint64_t)t;
+        jobs[t].r1 = t + 1 == nt ? dim : dim / (uint64_t)nt * (uint64_t)(t + 1);
+        jobs[t].cap = cap;
+        jobs[t].rc = ORC_OK;
     }
-    free(buf);
+    if (nt == 1) {
+        apply_rows(&jobs[0]);
+        return jobs[0].rc;
+    }
+    int started = 0;
+    for (; started < nt; ++started)
+        if (pthread_create(&tid[started], NULL, apply_rows, &jobs[started]) != 0) break;
+    for (int t = started; t < nt; ++t) apply_rows(&jobs[t]); /* could not start: run inline */
+    for (int t = 0; t < started; ++t) pthread_join(tid[t], NULL);
+    for (int t = 0; t < nt; ++t)
+        if (jobs[t].rc != ORC_OK) return jobs[t].rc;
     return ORC_OK;
 }
 

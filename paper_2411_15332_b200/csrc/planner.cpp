@@ -164,19 +164,35 @@ void merge_single_qubit(int n, std::vector<FOp>& ops) {
     std::vector<int> open(std::size_t(n), -1);  // index in `out` of the chain head on each bit
     std::vector<FOp> out;
     out.reserve(ops.size());
+    // a butterfly (RH's H^n, unnormalised [[1, 1], [1, -1]]) joins a one-qubit GATE next to it on
+    // its bit (C4/C1: H^n then the RY layer): the product is one 2x2 of the gate's kind (real stays
+    // real), and the butterfly no longer needs a register round of its own.  Butterflies do not
+    // merge with each other or with diagonals, so the sign-step programs of Grover-like
+    // circuits (butterfly pairs around sign steps, C3) keep their structure.
+    static const cplx kB[4] = {cplx(1.0, 0.0), cplx(1.0, 0.0), cplx(1.0, 0.0), cplx(-1.0, 0.0)};
+    static const bool no_wht_merge = knob("QCS_NO_WHT_MERGE");  // A/B switch
+    auto is_wht = [](const FOp& x) { return x.kind == TOP_WHT; };
+    auto is_gate1 = [](const FOp& x) { return x.kind == TOP_GATE && x.src.k == 1 && x.K == 1 && x.ctrl_mask == 0; };
     for (FOp& f : ops) {
-        const int bit = single_qubit_bit(f);
-        if (bit >= 0 && open[std::size_t(bit)] >= 0) {
-            FOp& head = out[std::size_t(open[std::size_t(bit)])];
+        int bit = single_qubit_bit(f);
+        if (bit < 0 && is_wht(f) && !no_wht_merge) bit = f.tpos[0];
+        const int hi = bit >= 0 ? open[std::size_t(bit)] : -1;
+        bool merge = hi >= 0;
+        if (merge) {
+            const FOp& head = out[std::size_t(hi)];
+            if (is_wht(f) || is_wht(head)) merge = (is_wht(f) && is_gate1(head)) || (is_wht(head) && is_gate1(f));
+        }
+        if (merge) {
+            FOp& head = out[std::size_t(hi)];
+            const cplx* a = is_wht(f) ? kB : f.src.m.data();      // later
+            const cplx* b = is_wht(head) ? kB : head.src.m.data();  // earlier
             GateOp g;
             g.k = 1;
             g.pos[0] = bit;
             g.m.resize(4);
             for (int r = 0; r < 2; ++r)
                 for (int c = 0; c < 2; ++c)
-                    g.m[std::size_t(r * 2 + c)] =
-                        f.src.m[std::size_t(r * 2)] * head.src.m[std::size_t(c)] +
-                        f.src.m[std::size_t(r * 2 + 1)] * head.src.m[std::size_t(2 + c)];
+                    g.m[std::size_t(r * 2 + c)] = a[r * 2] * b[c] + a[r * 2 + 1] * b[2 + c];
             FOp merged;
             if (make_fop(g, merged)) {
                 head = std::move(merged);
@@ -367,7 +383,8 @@ bool missed_tile_program(const std::vector<FOp>& ops, const std::vector<int>& li
 // pass, plus the plan-wide TileOp array (shared-memory gates, sign steps, 3-bit diagonals).
 namespace {
 
-// Pivoted gates for the specialised kernels: a 2x2 row (a, b) with pivot a (the larger entry) is
+// Pivoted gates for the specialised kernels: a 2x2 row (a, b) with pivot a (its diagonal entry
+// unless that one is zero or tiny) is
 // a * (x_piv + (b / a) x_other) -- one fused multiply-add per component for a real ratio, two for
 // a complex one, instead of two / four -- and the row scale a commutes to the end of the round
 // when no later operation of the round targets the gate's bit, where it joins the round's
@@ -447,7 +464,13 @@ void pivot_pass(PassParams& P, int& npool) {
                 cplx scale[2], rho[2];
                 for (int r = 0; r < 2; ++r) {
                     const cplx a0(c[2 * r].x, c[2 * r].y), a1(c[2 * r + 1].x, c[2 * r + 1].y);
-                    const int pv = std::abs(a1) > std::abs(a0) ? 1 : 0;
+                    // pivot on the diagonal entry (row r on column r) unless it is zero or tiny next
+                    // to the other entry: with a fused multiply-add the row's error stays ~1 ulp of
+                    // |a0 x0| + |a1 x1| whichever nonzero entry pivots, and a fixed orientation keeps
+                    // the generated source -- and so the compiled kernel -- independent of the
+                    // angles (a variational circuit with new angles reuses its kernels)
+                    const double ad = std::abs(r ? a1 : a0), ao = std::abs(r ? a0 : a1);
+                    const int pv = (ad > 0.0 && ad >= 0x1p-20 * ao) ? r : 1 - r;
                     scale[r] = pv ? a1 : a0;
                     rho[r] = (pv ? a0 : a1) / scale[r];
                     piv |= unsigned(pv) << (4 * fb + r);
