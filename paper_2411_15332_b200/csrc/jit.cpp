@@ -30,6 +30,8 @@
 #include <thread>
 #include <vector>
 
+#include <unistd.h>
+
 #include "common.hpp"
 #include "kernels.hpp"
 
@@ -568,32 +570,51 @@ std::vector<char> compile_cubin(const std::string& src) {
     for (unsigned char ch : key) h = (h ^ ch) * 1099511628211ull;
     char name[32];
     std::snprintf(name, sizeof(name), "%016llx", (unsigned long long)h);
-    const std::string base = std::string(dir) + "/qcs_" + name;
-    auto read = [](const std::string& path, std::string& out) {
+    // one file per kernel: [u64 key bytes][key][u64 cubin bytes][u64 FNV-1a of the cubin][cubin],
+    // written to a mkstemp() file in the same directory and renamed into place, so concurrent
+    // processes (torchrun ranks sharing the directory) never see a torn or mismatched entry
+    const std::string path = std::string(dir) + "/qcs_" + name + ".kc";
+    auto fnv = [](const char* p, std::size_t n) {
+        std::uint64_t x = 1469598103934665603ull;
+        for (std::size_t i = 0; i < n; ++i) x = (x ^ static_cast<unsigned char>(p[i])) * 1099511628211ull;
+        return x;
+    };
+    {
         std::FILE* f = std::fopen(path.c_str(), "rb");
-        if (!f) return false;
-        char buf[65536];
-        std::size_t k;
-        out.clear();
-        while ((k = std::fread(buf, 1, sizeof(buf), f)) > 0) out.append(buf, k);
-        std::fclose(f);
-        return true;
-    };
-    std::string stored, bin;
-    if (read(base + ".key", stored) && stored == key && read(base + ".cubin", bin) && !bin.empty())
-        return std::vector<char>(bin.begin(), bin.end());
+        if (f) {
+            std::string body;
+            char buf[65536];
+            std::size_t k;
+            while ((k = std::fread(buf, 1, sizeof(buf), f)) > 0) body.append(buf, k);
+            std::fclose(f);
+            std::uint64_t kl = 0, cl = 0, ch = 0;
+            if (body.size() >= 8) std::memcpy(&kl, body.data(), 8);
+            if (body.size() >= 8 + kl + 16) {
+                std::memcpy(&cl, body.data() + 8 + kl, 8);
+                std::memcpy(&ch, body.data() + 16 + kl, 8);
+                const char* cub = body.data() + 24 + kl;
+                if (body.size() == 24 + kl + cl && cl > 0 && body.compare(8, kl, key) == 0 && fnv(cub, cl) == ch)
+                    return std::vector<char>(cub, cub + cl);
+            }
+        }
+    }
     std::vector<char> cubin = nvrtc_cubin(src);
-    auto write = [](const std::string& path, const char* p, std::size_t n) {  // temp file, then rename
-        const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<std::uintptr_t>(p));
-        std::FILE* f = std::fopen(tmp.c_str(), "wb");
-        if (!f) return;
-        const bool ok = std::fwrite(p, 1, n, f) == n;
-        std::fclose(f);
-        if (ok) std::rename(tmp.c_str(), path.c_str());
-        else std::remove(tmp.c_str());
-    };
-    write(base + ".cubin", cubin.data(), cubin.size());
-    write(base + ".key", key.data(), key.size());
+    std::string tmpl = std::string(dir) + "/qcs_" + name + ".XXXXXX";
+    const int fd = mkstemp(tmpl.data());
+    if (fd < 0) return cubin;  // read-only cache directory: compile only
+    std::FILE* f = fdopen(fd, "wb");
+    if (!f) {
+        close(fd);
+        std::remove(tmpl.c_str());
+        return cubin;
+    }
+    const std::uint64_t kl = key.size(), cl = cubin.size(), ch = fnv(cubin.data(), cubin.size());
+    bool ok = std::fwrite(&kl, 8, 1, f) == 1 && std::fwrite(key.data(), 1, kl, f) == kl &&
+              std::fwrite(&cl, 8, 1, f) == 1 && std::fwrite(&ch, 8, 1, f) == 1 &&
+              std::fwrite(cubin.data(), 1, cl, f) == cl;
+    ok = (std::fclose(f) == 0) && ok;
+    if (ok) std::rename(tmpl.c_str(), path.c_str());
+    else std::remove(tmpl.c_str());
     return cubin;
 }
 

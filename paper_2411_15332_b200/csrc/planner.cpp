@@ -391,6 +391,7 @@ namespace {
 // diagonal table (created if the round has none).  Gates qualify without controls outside the
 // registers; controls on register bits select which table entries take the scale.
 void pivot_pass(PassParams& P, int& npool) {
+    static const bool no_chain = knob("QCS_NO_SCALE_CHAIN");  // A/B switch
     const int nr = P.alt_mode == ALT_ROUNDS ? P.alt_begin + P.alt_nrounds : P.nrounds;
     std::vector<RegOp> ops;
     std::vector<RoundDesc> rounds(P.rounds, P.rounds + nr);
@@ -425,13 +426,32 @@ void pivot_pass(PassParams& P, int& npool) {
 
             const bool bundle = o.kind & KF_BUNDLE;
             const unsigned bits = bundle ? o.t : 1u << o.t;
-            // the deferred scale is a diagonal on the target and the (register) control bits: no
-            // later operation of the round may target any of them
-            unsigned support = bits;
+            // the deferred scale is a diagonal on the target and the (register) control bits.  Per
+            // target bit: no later operation of the round targets it -> the round's table; the
+            // next one that does is an uncontrolled gate with only commuting operations between
+            // (diagonals, controls) -> the scale folds into that gate's columns (scale chaining:
+            // two layers of one qubit in one round, the round scheduler's light cones); else no pivot
+            unsigned support = 0;
             for (int k = 0; k < 3; ++k)
                 if (o.lctrl_mask >> R.r[k] & 1) support |= 1u << k;
             bool later = false;
-            for (std::size_t j = i + 1; j < rops.size(); ++j) {
+            int chain[3] = {-1, -1, -1};
+            for (int b = 0; b < 3 && !later; ++b) {
+                if (!(bits >> b & 1)) continue;
+                for (std::size_t j = i + 1; j < rops.size(); ++j) {
+                    const RegOp& g = rops[j];
+                    const int k = g.kind & KF_KIND;
+                    const unsigned tj = k == TOP_WHT || (g.kind & KF_BUNDLE) ? g.t : k == TOP_GATE ? 1u << g.t : 0u;
+                    if (!((k == TOP_GATE || k == TOP_WHT) && (tj >> b & 1))) continue;
+                    if (k == TOP_GATE && !g.lctrl_mask && !(g.kind & KF_GCTRL) && !(g.kind & KF_PIVOT) && !o.lctrl_mask &&
+                        !no_chain)
+                        chain[b] = int(j);
+                    else
+                        later = true;
+                    break;
+                }
+            }
+            for (std::size_t j = i + 1; j < rops.size() && !later; ++j) {  // register-bit controls
                 const int k = rops[j].kind & KF_KIND;
                 const unsigned tj = k == TOP_WHT || (rops[j].kind & KF_BUNDLE) ? rops[j].t
                                     : k == TOP_GATE ? 1u << rops[j].t : 0u;
@@ -479,6 +499,23 @@ void pivot_pass(PassParams& P, int& npool) {
                 for (int r = 0; r < 2; ++r) c[r] = make_double2(rho[r].real(), rho[r].imag());
                 c[2] = c[3] = make_double2(0.0, 0.0);
                 const int rb = bundle ? b : o.t;
+                if (chain[rb] >= 0) {  // G' = G diag(scale0, scale1): columns of the later gate
+                    RegOp& g = rops[std::size_t(chain[rb])];
+                    double2* gc = (g.kind & KF_BUNDLE) ? P.pool + g.ref + 4 * rb : g.c;
+                    for (int e = 0; e < 4; ++e) {
+                        const cplx v = cplx(gc[e].x, gc[e].y) * scale[e & 1];
+                        gc[e] = make_double2(v.real(), v.imag());
+                    }
+                    bool real = true;  // the later gate's kind: real only if all its coefficients are
+                    const unsigned gb = (g.kind & KF_BUNDLE) ? g.t : 1u;
+                    for (int bb = 0; bb < 3; ++bb) {
+                        if (!(gb >> bb & 1)) continue;
+                        const double2* x = (g.kind & KF_BUNDLE) ? P.pool + g.ref + 4 * bb : g.c;
+                        for (int e = 0; e < 4; ++e) real &= x[e].y == 0.0;
+                    }
+                    g.kind = std::uint8_t(real ? (g.kind | KF_REAL) : (g.kind & ~KF_REAL));
+                    continue;
+                }
                 for (int q = 0; q < 8; ++q)
                     if (en >> q & 1) table[q] *= scale[q >> rb & 1];
             }
@@ -557,6 +594,221 @@ bool conjugate_diag(const FOp& d, const std::vector<int>& perms, At at, FOp& out
         g.m[std::size_t(a) * dim + a] = cplx(d.dval[e].x, d.dval[e].y);
     }
     return make_fop(g, out) && out.kind == TOP_DIAG;
+}
+
+// Round scheduling (light cones).  A pass's operations arrive in circuit order, so a layered
+// circuit (C4: a gate on every qubit, then diagonals coupling neighbours) forms one register round
+// per three qubits per layer.  But a layer-(L+1) gate on a bit only waits for the operations that
+// do not commute with it -- the bit's own layer-L gate and the diagonals on it -- so once its
+// diagonal partners have their layer-L gates, it can run in the SAME round as those (one
+// shared-memory round trip for two layers).  This reorders the pass's list (only commuting
+// operations swap places) into groups, each the ready operations on a set of three register
+// bits chosen greedily for the most gates: +-1 diagonals (sign flips, CZ) run as soon as they
+// are ready, phase diagonals wait for a group holding their bits.  A one-bit phase followed in
+// its group by a gate on that bit, with only diagonals between, folds into the gate (G' = G D):
+// one complex 2x2 instead of a multiply on every register.  Used when it saves rounds.
+struct SchedOp {
+    bool elem = false;        // commutes with every other elementwise operation
+    bool gate = false;        // needs its target in the registers
+    bool takeable_any = false;  // elementwise and cheap anywhere (+-1, scale)
+    unsigned reg = 0;         // gate: local target bit mask; phase diagonal: local bits (0: outside)
+    std::vector<int> succ;
+    int npred = 0;
+};
+
+bool signed_diag(const FOp& f) {
+    if (f.kind != TOP_DIAG) return false;
+    for (int g = 0; g < (1 << f.dk); ++g)
+        if (f.dval[g].y != 0.0 || (f.dval[g].x != 1.0 && f.dval[g].x != -1.0)) return false;
+    return true;
+}
+
+int round_count(const std::vector<FOp>& ops, const std::vector<int>& list, const int* loc) {
+    int rounds = 0;
+    unsigned cur = 0;
+    bool open = false;
+    for (int idx : list) {
+        const FOp& f = ops[std::size_t(idx)];
+        if (elementwise(f)) continue;
+        const unsigned t = 1u << loc[f.tpos[0]];
+        if (open && (__builtin_popcount(cur | t) <= 3)) {
+            cur |= t;
+        } else {
+            ++rounds;
+            cur = t;
+            open = true;
+        }
+    }
+    return rounds;
+}
+
+bool schedule_rounds(int n, const int* loc, int m, const std::vector<FOp>& ops, const std::vector<int>& list,
+                     std::vector<FOp>& out_ops, std::vector<int>& out_list) {
+    static const bool off = knob("QCS_NO_ROUND_SCHED");  // A/B switch
+    const int N = int(list.size());
+    if (off || N < 4 || m < 4) return false;
+    for (int idx : list) {
+        const FOp& f = ops[std::size_t(idx)];
+        const bool ok = f.kind == TOP_DIAG || f.kind == TOP_SCALE || (f.kind == TOP_WHT) ||
+                        (f.kind == TOP_GATE && f.K == 1 && loc[f.tpos[0]] >= 0);
+        if (!ok) return false;
+    }
+    std::vector<SchedOp> so(static_cast<std::size_t>(N));
+    // dependencies through each basis bit: a non-elementwise operation waits for everything on
+    // the bit since the previous one (and that one); an elementwise one for the previous one
+    std::vector<int> last_nd(std::size_t(n), -1);
+    std::vector<std::vector<int>> since(static_cast<std::size_t>(n));
+    auto edge = [&](int a, int b) { so[std::size_t(a)].succ.push_back(b); ++so[std::size_t(b)].npred; };
+    for (int i = 0; i < N; ++i) {
+        const FOp& f = ops[std::size_t(list[std::size_t(i)])];
+        SchedOp& o = so[std::size_t(i)];
+        o.elem = elementwise(f);
+        o.gate = !o.elem;
+        if (o.gate) o.reg = 1u << loc[f.tpos[0]];
+        if (f.kind == TOP_SCALE || signed_diag(f)) o.takeable_any = true;
+        if (f.kind == TOP_DIAG && !o.takeable_any) {
+            bool inside = true;
+            for (int j = 0; j < f.dk; ++j) {
+                if (loc[f.dpos[j]] < 0) inside = false;
+                else o.reg |= 1u << loc[f.dpos[j]];
+            }
+            if (!inside) o.reg = 0;  // a bit outside the tile: never in the registers
+        }
+        std::vector<int> preds;
+        for (int b = 0; b < n; ++b) {
+            if (!(f.touch >> b & 1)) continue;
+            if (o.elem) {
+                if (last_nd[std::size_t(b)] >= 0) preds.push_back(last_nd[std::size_t(b)]);
+                since[std::size_t(b)].push_back(i);
+            } else {
+                if (last_nd[std::size_t(b)] >= 0) preds.push_back(last_nd[std::size_t(b)]);
+                for (int e : since[std::size_t(b)]) preds.push_back(e);
+                since[std::size_t(b)].clear();
+                last_nd[std::size_t(b)] = i;
+            }
+        }
+        std::sort(preds.begin(), preds.end());
+        preds.erase(std::unique(preds.begin(), preds.end()), preds.end());
+        for (int p : preds) edge(p, i);
+    }
+    std::vector<int> cnt(static_cast<std::size_t>(N)), tmp(static_cast<std::size_t>(N));
+    for (int i = 0; i < N; ++i) cnt[std::size_t(i)] = so[std::size_t(i)].npred;
+    std::vector<char> done(std::size_t(N), 0);
+    std::vector<int> order, group_of;
+    order.reserve(std::size_t(N));
+    int group = 0;
+    auto takeable = [&](int i, unsigned T) {
+        if (T == ~0u) return true;  // the final group: everything that is left
+        const SchedOp& o = so[std::size_t(i)];
+        if (o.gate) return (o.reg & ~T) == 0;
+        if (o.takeable_any) return true;
+        return o.reg != 0 && (o.reg & ~T) == 0;
+    };
+    // run the ready closure for register set T; commit: record the order, else count gates
+    std::vector<int> stack, taken;
+    auto closure = [&](unsigned T, bool commit, long& score) {
+        tmp = cnt;
+        stack.clear();
+        taken.clear();
+        for (int i = 0; i < N; ++i)
+            if (!done[std::size_t(i)] && tmp[std::size_t(i)] == 0) stack.push_back(i);
+        std::sort(stack.begin(), stack.end(), std::greater<int>());  // lowest index first
+        int gates = 0;
+        long early = 0;
+        while (!stack.empty()) {
+            const int i = stack.back();
+            stack.pop_back();
+            if (!takeable(i, T)) continue;
+            taken.push_back(i);
+            if (so[std::size_t(i)].gate) {
+                ++gates;
+                early += N - i;
+            }
+            for (int s2 : so[std::size_t(i)].succ)
+                if (--tmp[std::size_t(s2)] == 0) stack.push_back(s2);
+        }
+        score = long(gates) * (1L << 32) + early;
+        if (commit) {
+            for (int i : taken) {
+                done[std::size_t(i)] = 1;
+                order.push_back(i);
+                group_of.push_back(group);
+            }
+            cnt = tmp;
+            ++group;
+        }
+        return gates;
+    };
+    while (int(order.size()) < N) {
+        unsigned U = 0;  // bits with an unscheduled gate
+        for (int i = 0; i < N; ++i)
+            if (!done[std::size_t(i)] && so[std::size_t(i)].gate) U |= so[std::size_t(i)].reg;
+        if (!U) {  // only diagonals left: the rest in list order
+            long sc;
+            closure(~0u, true, sc);
+            continue;
+        }
+        std::vector<int> bits;
+        for (int b = 0; b < m; ++b)
+            if (U >> b & 1) bits.push_back(b);
+        long best = -1;
+        unsigned bestT = 0;
+        const int nb = int(bits.size());
+        for (int a = 0; a < nb; ++a)
+            for (int b = a + 1; b < std::max(nb, a + 2); ++b)
+                for (int c = b + 1; c < std::max(nb, b + 2); ++c) {
+                    unsigned T = 1u << bits[std::size_t(a)];
+                    if (b < nb) T |= 1u << bits[std::size_t(b)];
+                    if (c < nb) T |= 1u << bits[std::size_t(c)];
+                    long sc;
+                    closure(T, false, sc);
+                    if (sc > best) {
+                        best = sc;
+                        bestT = T;
+                    }
+                }
+        long sc;
+        if (closure(bestT, true, sc) == 0) return false;  // no progress: keep the circuit order
+    }
+    // fold one-bit phases into the next gate on their bit within their group
+    out_ops.clear();
+    out_list.clear();
+    std::vector<char> gone(std::size_t(N), 0);
+    std::vector<FOp> local(static_cast<std::size_t>(N));
+    for (int i = 0; i < N; ++i) local[std::size_t(i)] = ops[std::size_t(list[std::size_t(i)])];
+    for (std::size_t k = 0; k < order.size(); ++k) {
+        const int i = order[k];
+        const FOp& d = local[std::size_t(i)];
+        if (d.kind != TOP_DIAG || d.dk != 1 || d.src.k != 1 || signed_diag(d)) continue;
+        const int bit = d.dpos[0];
+        for (std::size_t j = k + 1; j < order.size() && group_of[j] == group_of[k]; ++j) {
+            const FOp& g = local[std::size_t(order[j])];
+            if (!(g.touch >> bit & 1) || gone[std::size_t(order[j])]) continue;
+            if (elementwise(g)) continue;  // diagonals commute with the phase
+            if (g.kind == TOP_GATE && g.K == 1 && g.ctrl_mask == 0 && g.src.k == 1 && g.tpos[0] == bit) {
+                GateOp p;
+                p.k = 1;
+                p.pos[0] = bit;
+                p.m.resize(4);
+                for (int r = 0; r < 2; ++r)
+                    for (int c = 0; c < 2; ++c)
+                        p.m[std::size_t(r * 2 + c)] = g.src.m[std::size_t(r * 2)] * d.src.m[std::size_t(c)] +
+                                                      g.src.m[std::size_t(r * 2 + 1)] * d.src.m[std::size_t(2 + c)];
+                FOp merged;
+                if (make_fop(p, merged) && merged.kind == TOP_GATE) {
+                    local[std::size_t(order[j])] = std::move(merged);
+                    gone[std::size_t(i)] = 1;
+                }
+            }
+            break;
+        }
+    }
+    for (int i : order) {
+        if (gone[std::size_t(i)]) continue;
+        out_ops.push_back(local[std::size_t(i)]);
+        out_list.push_back(int(out_ops.size()) - 1);
+    }
+    return round_count(out_ops, out_list, loc) < round_count(ops, list, loc);
 }
 
 }  // namespace
@@ -1073,7 +1325,14 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             if (pending_signs) rd.flags = std::uint8_t(rd.flags | RD_SIGNS);
         }
         };
-        lower_list(ops, lists[pi]);
+        {
+            std::vector<FOp> sched_ops;
+            std::vector<int> sched_list;
+            if (!has_alt[pi] && schedule_rounds(n, loc, P.m, ops, lists[pi], sched_ops, sched_list))
+                lower_list(sched_ops, sched_list);
+            else
+                lower_list(ops, lists[pi]);
+        }
         // tiles that no sign step's listed indices reach see every sign step as a scalar +-1;
         // there the pass often collapses (H_b H_b = 2 I for the unnormalised butterflies), so
         // such passes carry a second, simplified program for those tiles

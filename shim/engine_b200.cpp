@@ -225,11 +225,13 @@ SimReport simulate(const Circuit& c, Engine engine, const SimOptions& opts) {
             report.total_sign_count += r.sign_count;
             report.total_madd_count += r.madd_count;
         }
+        // the value-initialised result vectors (the reference API's value semantics) are written
+        // while the device still runs the circuit (qcs_simulate returns with the work queued)
         const std::uint64_t dim = std::uint64_t(1) << c.n;
         report.final.n = c.n;
         report.final.amps.resize(dim);
-        check(qcs_state_download(st, reinterpret_cast<double*>(report.final.amps.data()), 0, dim));
         report.probabilities.resize(dim);
+        check(qcs_state_download(st, reinterpret_cast<double*>(report.final.amps.data()), 0, dim));
         check(qcs_probabilities(st, report.probabilities.data(), QCS_MEM_HOST));
     }
     return report;

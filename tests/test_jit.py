@@ -91,8 +91,9 @@ def test_plans_do_not_depend_on_history(Q, cfg):
 
 
 def test_disk_cache_of_compiled_kernels(tmp_path):
-    """QCS_JIT_CACHE=<dir>: a second process finds the compiled pass kernels on disk (each stored
-    with its full source as the key) instead of compiling them."""
+    """QCS_JIT_CACHE=<dir>: a second process finds the compiled pass kernels on disk (each entry
+    one file holding its full source as the key and a hash of the cubin, published by an atomic
+    rename of a mkstemp file) instead of compiling them."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     code = ("import time; t = time.time(); from paper_2411_15332_b200 import configs, qcsim as Q; "
             "r = Q.plan_compile(configs.c4_circuit(14, 2)); print(r['kernels'], r['cubin_bytes'], time.time() - t)")
@@ -100,9 +101,17 @@ def test_disk_cache_of_compiled_kernels(tmp_path):
     runs = [subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, check=True)
             .stdout.split() for _ in range(2)]
     assert runs[0][:2] == runs[1][:2] and int(runs[0][0]) > 0
-    cubins = [f for f in os.listdir(tmp_path) if f.endswith(".cubin")]
-    assert len(cubins) == int(runs[0][0])
+    entries = [f for f in os.listdir(tmp_path) if f.endswith(".kc")]
+    assert len(entries) == int(runs[0][0])
+    assert not [f for f in os.listdir(tmp_path) if not f.endswith(".kc")]  # no temp files left
     assert float(runs[1][2]) < float(runs[0][2])
+    # a torn entry (cut short) is recompiled and replaced, never loaded
+    victim = os.path.join(tmp_path, entries[0])
+    with open(victim, "r+b") as f:
+        f.truncate(os.path.getsize(victim) // 2)
+    again = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, check=True)
+    assert again.stdout.split()[:2] == runs[0][:2]
+    assert os.path.getsize(victim) > 0 and len([f for f in os.listdir(tmp_path) if f.endswith(".kc")]) == len(entries)
 
 
 def test_jit_mode_switch(Q):

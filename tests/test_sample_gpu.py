@@ -93,11 +93,15 @@ def test_basis_and_uniform_states():
     from paper_2411_15332_b200 import qcsim as Q
     n = 13
     s = Q.DeviceState(n)
-    s.apply_rh()                 # uniform 2^-13: an exact CDF, boundaries exactly on the grid
+    s.apply_rh()                 # uniform: every probability equal, boundaries evenly spaced
     x = s.download()
     got, acc = s.sample(500, 11)
     assert got == _ref_sample(n, x, 500, 11)
-    assert acc == 1.0
+    from oracle.oracle_py import sequential_sample
+    assert acc == sequential_sample(x.real * x.real + x.imag * x.imag, 0, 11)[1]
+    b = Q.DeviceState(n, 4321)   # a basis state: probability 1 at one index, exact
+    got, acc = b.sample(50, 2)
+    assert acc == 1.0 and got == [4321] * 50
 
 
 def test_render_report_n24_samples_on_device_fast():
