@@ -273,13 +273,22 @@ void split_phases(std::vector<FOp>& ops) {
 Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
     Plan plan;
     const int M = std::min(max_bits, n);
+    static const bool no_seed = knob("QCS_NO_TILE_SEARCH");  // A/B switch
     std::vector<int> remaining(ops.size());
     for (std::size_t i = 0; i < ops.size(); ++i) remaining[i] = int(i);
-    while (!remaining.empty()) {
+    // One pass grown greedily in operation order from the tile bits `seed` (bits 0..2 always):
+    // an operation joins when it commutes with everything skipped before it and its targets fit.
+    struct Grown {
         u64 S = 0;
+        std::vector<int> chosen, skipped;
+        int gates = 0;
+        bool signs = false;
+    };
+    auto grow = [&](u64 seed) {
+        Grown g;
+        u64 S = seed;
         for (int b = 0; b < std::min(3, n); ++b) S |= u64(1) << b;
         int used = __builtin_popcountll(S);
-        std::vector<int> chosen, skipped;
         u64 nd_block = 0, d_block = 0;  // supports of skipped non-diagonal / diagonal ops
         // once a sign step is in the pass, later non-elementwise ops must target bits the pass
         // used before it: then on the tiles the sign step misses, the pass mirrors around it
@@ -308,12 +317,14 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
                     }
                 }
             }
-            if (take && int(chosen.size()) >= kPassMaxOps - 4) take = false;
+            if (take && int(g.chosen.size()) >= kPassMaxOps - 4) take = false;
             if (take) {
                 if (f.kind == TOP_SIGN) signed_pass = true;
-                chosen.push_back(idx);
+                g.signs |= f.kind == TOP_SIGN;
+                if (!elementwise(f)) ++g.gates;
+                g.chosen.push_back(idx);
             } else {
-                skipped.push_back(idx);
+                g.skipped.push_back(idx);
                 (f.diagonal ? d_block : nd_block) |= f.touch;
             }
         }
@@ -323,8 +334,50 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
                 S |= u64(1) << b;
                 ++used;
             }
-        plan.passes.push_back(PlannedPass{S, chosen});
-        remaining.swap(skipped);
+        g.S = S;
+        return g;
+    };
+    while (!remaining.empty()) {
+        Grown best = grow(0);
+        // Tile search: the circuit-order tile fills with the first new bits it meets, which for a
+        // layered circuit is a run of qubits whose light cone the neighbouring runs cut short.
+        // Seeding the tile with the targets of a later ready gate instead (up to 48 candidates)
+        // and keeping the pass with the most gates finds tiles whose light cones reach further
+        // (fewer passes).  Passes with sign steps keep the circuit-order tile (their skip and
+        // mirror programs depend on it).
+        if (!no_seed && !best.signs && M >= 6) {
+            // seed j: the first new target bits met from the j-th remaining gate on (as many as
+            // the tile takes), i.e. the tile a pass starting at that gate would fill
+            std::vector<u64> seeds;
+            u64 low = 0;
+            for (int b = 0; b < std::min(3, n); ++b) low |= u64(1) << b;
+            std::vector<std::size_t> starts;
+            for (std::size_t p = 0; p < remaining.size() && starts.size() < 48; ++p)
+                if (!elementwise(ops[std::size_t(remaining[p])])) starts.push_back(p);
+            for (std::size_t st : starts) {
+                u64 seed = low;
+                for (std::size_t p = st; p < remaining.size(); ++p) {
+                    const FOp& f = ops[std::size_t(remaining[p])];
+                    if (elementwise(f)) continue;
+                    u64 t = 0;
+                    for (int i = 0; i < f.K; ++i) t |= u64(1) << f.tpos[i];
+                    if (__builtin_popcountll(seed | t) > M) break;
+                    seed |= t;
+                }
+                if (std::find(seeds.begin(), seeds.end(), seed) == seeds.end()) seeds.push_back(seed);
+                // and the gate's own targets alone (the rest filled in circuit order)
+                const FOp& f = ops[std::size_t(remaining[st])];
+                u64 t = low;
+                for (int i = 0; i < f.K; ++i) t |= u64(1) << f.tpos[i];
+                if (std::find(seeds.begin(), seeds.end(), t) == seeds.end()) seeds.push_back(t);
+            }
+            for (u64 seed : seeds) {
+                Grown g = grow(seed);
+                if (!g.signs && g.gates > best.gates) best = std::move(g);
+            }
+        }
+        plan.passes.push_back(PlannedPass{best.S, best.chosen});
+        remaining.swap(best.skipped);
     }
     return plan;
 }
