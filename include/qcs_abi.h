@@ -248,6 +248,9 @@ typedef struct qcs_plan_info {
     int64_t skip_passes;    /* ... where that program is the identity: only the reached tiles move */
     int64_t paired_passes;  /* passes of a pair around a skip pass that composes to a scalar: they
                                run only on the tiles the skip pass reaches */
+    int64_t fp64_ops;       /* FP64 instructions (DFMA/DMUL/DADD, per thread) the tile passes execute,
+                               counted from their specialised kernels over the tiles that compute */
+    int64_t sweep_amps;     /* amplitudes the tile passes load and store (HBM traffic / 32 B) */
 } qcs_plan_info;
 int qcs_plan_stats(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
                    qcs_plan_info* out);

@@ -43,7 +43,7 @@ class qcs_step_report(C.Structure):
 class qcs_plan_info(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("ops", "passes", "tile_passes", "single_passes", "rounds",
                                          "smem_rounds", "reg_ops", "max_tile_bits", "alt_passes",
-                                         "skip_passes", "paired_passes")]
+                                         "skip_passes", "paired_passes", "fp64_ops", "sweep_amps")]
 
 
 _P = C.c_void_p

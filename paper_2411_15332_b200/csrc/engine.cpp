@@ -273,10 +273,9 @@ void run_single(qcs_state* s, const FOp& f, const u64* flips_dev, u64 flip_cnt) 
 
 void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low);
 
-void plan_fused(int n, const std::vector<FOp>& ops, Lowered& low) {
-    plan_fused_passes(n, ops, low);
-    // support: from a basis state, an amplitude can only become nonzero by flipping bits that
-    // non-diagonal operations target (gates, butterflies); diagonals and scales never do
+// support: from a basis state, an amplitude can only become nonzero by flipping bits that
+// non-diagonal operations target (gates, butterflies); diagonals and scales never do
+void compute_reached(const std::vector<FOp>& ops, Lowered& low) {
     low.reached.assign(low.passes.size(), 0);
     u64 reached = 0;
     for (std::size_t i = 0; i < low.passes.size(); ++i) {
@@ -288,6 +287,11 @@ void plan_fused(int n, const std::vector<FOp>& ops, Lowered& low) {
             for (int k = 0; k < f.K; ++k) reached |= u64(1) << f.tpos[k];
         }
     }
+}
+
+void plan_fused(int n, const std::vector<FOp>& ops, Lowered& low) {
+    plan_fused_passes(n, ops, low);
+    compute_reached(ops, low);
 }
 
 void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low) {
@@ -310,6 +314,56 @@ void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low) {
 // writes every tile, else by a fill kernel first.  jit: per pass, the specialised kernel (kept by
 // cached plans); cached: the cached plan's id (never reused, unlike its address), whose tables
 // need no upload when plan_buf holds them; 0 for an uncached plan.
+// Support tracking from a basis state |init> (init >= 0): tiles outside the support reached
+// before a pass are zero (no load), tiles a pass leaves zero and the next reads as zero are not
+// written, and the reset folds into the first pass.  Returns false when the reset could not be
+// folded (the caller writes |init> first).  Shared by execute_fused and plan_stats.
+bool apply_support(int n, Lowered& low, std::int64_t init) {
+    bool folded = init < 0;
+    if (!low.passes.empty()) low.passes[0].init = 0;
+    // from a basis state: tiles outside the support reached before a pass are zero (no load)
+    const u64 full = n >= 64 ? ~u64(0) : (u64(1) << n) - 1;
+    for (std::size_t i = 0; i < low.passes.size() && n >= 3; ++i) {
+        PassParams& P = low.passes[i];
+        P.zmask = P.zval = 0;
+        if (!(init >= 0) || low.pass_ops[i].size() < 2) continue;
+        u64 tile = 0;
+        for (int b = 0; b < P.m; ++b) tile |= u64(1) << P.bits[b];
+        P.zmask = full & ~tile & ~low.reached[i];
+        P.zval = u64(init) & P.zmask;
+    }
+    // a tile that is zero after this pass and that the next pass (running every tile) reads as
+    // zero need not be written at all
+    static const bool no_skip = std::getenv("QCS_NO_TILE_SKIP") != nullptr;  // A/B switch
+    static const bool no_zero = std::getenv("QCS_NO_ZERO_INPUT") != nullptr;
+    if (no_zero)
+        for (auto& P : low.passes) P.zmask = P.zval = 0;
+    for (std::size_t i = 0; i + 1 < low.passes.size() && n >= 3 && !no_skip; ++i) {
+        PassParams& P = low.passes[i];
+        const PassParams& Q = low.passes[i + 1];
+        P.smask = P.sval = 0;
+        if (!Q.zmask || low.pass_ops[i].size() < 2 || low.pass_ops[i + 1].size() < 2 || Q.list_cnt ||
+            Q.alt_mode == ALT_SKIP)
+            continue;
+        u64 tile = 0;
+        for (int b = 0; b < P.m; ++b) tile |= u64(1) << P.bits[b];
+        P.smask = Q.zmask & ~tile;
+        P.sval = Q.zval & ~tile;
+    }
+    if (!low.passes.empty()) low.passes.back().smask = low.passes.back().sval = 0;
+    static const bool no_fold = std::getenv("QCS_NO_INIT_FOLD") != nullptr;  // A/B switch
+    if (init >= 0) {
+        const bool fold = !no_fold && !low.passes.empty() && low.pass_ops[0].size() >= 2 && n >= 3 && low.passes[0].list_cnt == 0 &&
+                          low.passes[0].alt_mode != ALT_SKIP;
+        if (fold) {
+            low.passes[0].init = 1;
+            low.passes[0].init_index = u64(init);
+            folded = true;
+        }
+    }
+    return folded;
+}
+
 void execute_fused(qcs_state* s, const std::vector<FOp>& ops, Lowered& low, std::int64_t* init,
                    std::vector<void*>* jit = nullptr, std::uint64_t cached = 0) {
     const int n = s->n;
@@ -347,49 +401,9 @@ void execute_fused(qcs_state* s, const std::vector<FOp>& ops, Lowered& low, std:
     const auto* big_dev = reinterpret_cast<const TileOp*>(base);
     const auto* flips_dev = reinterpret_cast<const u64*>(base + f_off);
     const auto* tables_dev = reinterpret_cast<const u64*>(base + t_off);
-    if (!low.passes.empty()) low.passes[0].init = 0;
-    // from a basis state: tiles outside the support reached before a pass are zero (no load)
-    const u64 full = n >= 64 ? ~u64(0) : (u64(1) << n) - 1;
-    for (std::size_t i = 0; i < low.passes.size() && n >= 3; ++i) {
-        PassParams& P = low.passes[i];
-        P.zmask = P.zval = 0;
-        if (!(init && *init >= 0) || low.pass_ops[i].size() < 2) continue;
-        u64 tile = 0;
-        for (int b = 0; b < P.m; ++b) tile |= u64(1) << P.bits[b];
-        P.zmask = full & ~tile & ~low.reached[i];
-        P.zval = u64(*init) & P.zmask;
-    }
-    // a tile that is zero after this pass and that the next pass (running every tile) reads as
-    // zero need not be written at all
-    static const bool no_skip = std::getenv("QCS_NO_TILE_SKIP") != nullptr;  // A/B switch
-    static const bool no_zero = std::getenv("QCS_NO_ZERO_INPUT") != nullptr;
-    if (no_zero)
-        for (auto& P : low.passes) P.zmask = P.zval = 0;
-    for (std::size_t i = 0; i + 1 < low.passes.size() && n >= 3 && !no_skip; ++i) {
-        PassParams& P = low.passes[i];
-        const PassParams& Q = low.passes[i + 1];
-        P.smask = P.sval = 0;
-        if (!Q.zmask || low.pass_ops[i].size() < 2 || low.pass_ops[i + 1].size() < 2 || Q.list_cnt ||
-            Q.alt_mode == ALT_SKIP)
-            continue;
-        u64 tile = 0;
-        for (int b = 0; b < P.m; ++b) tile |= u64(1) << P.bits[b];
-        P.smask = Q.zmask & ~tile;
-        P.sval = Q.zval & ~tile;
-    }
-    if (!low.passes.empty()) low.passes.back().smask = low.passes.back().sval = 0;
-    static const bool no_fold = std::getenv("QCS_NO_INIT_FOLD") != nullptr;  // A/B switch
-    if (init && *init >= 0) {
-        const bool fold = !no_fold && !low.passes.empty() && low.pass_ops[0].size() >= 2 && n >= 3 && low.passes[0].list_cnt == 0 &&
-                          low.passes[0].alt_mode != ALT_SKIP;
-        if (fold) {
-            low.passes[0].init = 1;
-            low.passes[0].init_index = u64(*init);
-        } else {
-            fill_basis(s->amps, u64(1) << n, u64(*init), s->stream);
-        }
-        *init = -1;
-    }
+    const std::int64_t init_index = init ? *init : -1;
+    if (!apply_support(n, low, init_index)) fill_basis(s->amps, u64(1) << n, u64(init_index), s->stream);
+    if (init) *init = -1;
     if (jit && jit->size() != low.passes.size()) jit->assign(low.passes.size(), nullptr);
     for (std::size_t i = 0; i < low.passes.size(); ++i) {
         const auto& po = low.pass_ops[i];
@@ -684,7 +698,7 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
 }
 
 namespace {
-void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out) {
+void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out, std::int64_t init = -1) {
     if (ops.empty()) return;
     out->ops += std::int64_t(ops.size());
     if (n < 3) {
@@ -694,6 +708,8 @@ void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out) {
     }
     Lowered low;
     lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
+    compute_reached(ops, low);
+    apply_support(n, low, init);  // from |init> (opts->reset), as execute_fused runs the plan
     const bool dump = std::getenv("QCS_PLAN_DUMP") != nullptr;  // planner debugging: rounds and ops
     for (std::size_t i = 0; i < low.passes.size(); ++i) {
         if (dump) dump_pass(stderr, low.passes[i], low.pass_ops[i].size());
@@ -704,6 +720,21 @@ void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out) {
         }
         const PassParams& p = low.passes[i];
         ++out->tile_passes;
+        {  // the tiles that compute: the listed ones, one for a pass from |init>, a 2^-|zmask| share
+            double tiles = p.list_cnt ? double(p.list_cnt) : std::ldexp(1.0, n - p.m);
+            double moved = tiles;
+            if (p.init) {
+                tiles = 1.0;
+                moved = p.smask ? moved * std::ldexp(1.0, -__builtin_popcountll(p.smask)) : moved;
+                moved = 0.5 * moved;  // loads nothing; stores what the next pass reads
+            } else if (p.zmask) {
+                tiles *= std::ldexp(1.0, -__builtin_popcountll(p.zmask));
+            }
+            const double f = tiles * pass_fp64_per_tile(p);
+            if (dump) std::fprintf(stderr, "  fp64/amp %.2f  tiles %.0f\n", f / std::ldexp(1.0, n), tiles);
+            out->fp64_ops += std::int64_t(f);
+            out->sweep_amps += std::int64_t(moved * std::ldexp(1.0, p.m));
+        }
         if (p.alt_mode != ALT_NONE) ++out->alt_passes;
         if (p.alt_mode == ALT_SKIP) ++out->skip_passes;
         if (p.alt_mode == ALT_NONE && p.list_cnt) ++out->paired_passes;
@@ -735,7 +766,7 @@ void plan_stats(int n, const qcs_step* steps, int nsteps, int engine, const qcs_
     if (o.fuse) {
         merge_single_qubit(n, ops);
         split_phases(ops);
-        add_plan_stats(n, ops, out);
+        add_plan_stats(n, ops, out, o.reset ? std::int64_t(o.initial) : -1);
     }
 }
 

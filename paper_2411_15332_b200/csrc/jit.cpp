@@ -56,6 +56,12 @@ struct Out {
 };
 
 
+// FP64 instructions (DFMA / DMUL / DADD, per thread) the generated code executes per group of 8
+// amplitudes, accumulated while a pass's source is generated (pass_fp64_per_tile): the
+// roofline's compute side for the FP64-bound passes (bench.py)
+thread_local double g_fp64 = 0.0;
+void fp64(double k) { g_fp64 += k; }
+
 bool knob_swaps() {
     static const bool on = [] { const char* v = std::getenv("QCS_JIT_SWAPS"); return !v || std::atoi(v) != 0; }();
     return on;
@@ -105,7 +111,15 @@ std::string const_bits(bool c0, bool c1, int dk, int p0, int p1) {
 // 2x2 forms of tile_device.cuh.
 void emit_gate(Out& o, int kb, int t, const double2* c, const std::string& coef, unsigned en, int G, unsigned piv) {
     const unsigned all = (1u << G) - 1;
+    auto pairs = [&](unsigned e) {
+        int k = 0;
+        for (int q = 0; q < G; ++q)
+            if (!(q >> t & 1) && (e >> q & 1)) ++k;
+        return k;
+    };
     if (kb & KF_PIVOT) {  // piv: this bit's 4 pivot flags
+        const int per_row = (kb & KF_REAL) ? 2 : 4;
+        fp64(double(pairs(en & all)) * (((piv >> 2 & 1) ? 0 : per_row) + ((piv >> 3 & 1) ? 0 : per_row)));
         if (en & all)
             o("      gate1p<%d, %d, %d, %d, %d, %d, 0x%xu>(v, (%s)[0], (%s)[1]);\n", t, int(piv & 1), int(piv >> 1 & 1),
               int(piv >> 2 & 1), int(piv >> 3 & 1), (kb & KF_REAL) ? 1 : 0, en & all, coef.c_str(), coef.c_str());
@@ -120,6 +134,7 @@ void emit_gate(Out& o, int kb, int t, const double2* c, const std::string& coef,
         return;
     }
     const char* g = (kb & KF_REAL) ? "gate1r" : "gate1";
+    fp64(double(pairs(en & all)) * ((kb & KF_REAL) ? 8 : 16));
     if ((en & all) == all) o("      %s<%d, false>(v, %s, 0xffffu);\n", g, t, coef.c_str());
     else if (en) o("      %s<%d, true>(v, %s, 0x%xu);\n", g, t, coef.c_str(), en);
 }
@@ -348,10 +363,14 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
               const_bits(c0, c1, op.dk, op.dpos[0], op.dpos[1]).c_str(), gmask);
         } else if (kind == TOP_WHT) {
             for (int b = 0; b < W; ++b)
-                if (op.t >> b & 1) o("      butterfly<%d>(v);\n", b);
+                if (op.t >> b & 1) {
+                    o("      butterfly<%d>(v);\n", b);
+                    fp64(16);
+                }
         } else if (kind == TOP_SCALE) {
             o("      { const double sc = P.ops[%d].c[0].x;\n", oi);
             o("        for (int q = 0; q < %d; ++q) v[q] = make_double2(v[q].x * sc, v[q].y * sc); }\n", G);
+            fp64(2 * G);
         } else if (kind == TOP_GATE && (kb & KF_BUNDLE)) {
             for (int b = 0; b < W; ++b)
                 if (op.t >> b & 1) emit_gate(o, kb, b, P.pool + op.ref + 4 * b, "P.pool + " + std::to_string(op.ref + 4 * b),
@@ -370,6 +389,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
         } else if (kind == TOP_DTAB) {
             for (int q = 0; q < G; ++q) {
                 if (op.dskip >> q & 1) continue;
+                fp64(P.pool[op.ref + q].y == 0.0 ? 2 : 4);
                 if (P.pool[op.ref + q].y == 0.0)  // real entry (e.g. only gate row scales): 2 FP64
                     o("      { const double s = P.pool[%d].x; v[%d] = make_double2(v[%d].x * s, v[%d].y * s); }\n", op.ref + q,
                       q, q, q);
@@ -378,6 +398,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
             }
         } else if (kind == TOP_DIAG && accumulate && group_const(op)) {
             // a phase constant over the group: into the group's scalar, applied once at the end
+            fp64(4);
             if (op.dk == 1) {
                 o("      { const int g = int((g0 >> %d) & 1);\n", op.dpos[0]);
                 o("        if (!((%uu >> g) & 1u)) gs = cmul_f(g ? P.ops[%d].c[1] : P.ops[%d].c[0], gs); }\n",
@@ -390,6 +411,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
                   oi);
             }
         } else if (kind == TOP_DIAG) {
+            fp64(4 * G);
             if (op.dk == 1 && op.dreg[0] == 0xff) {
                 o("      { const int g = int((g0 >> %d) & 1);\n", op.dpos[0]);
                 o("        if (!((%uu >> g) & 1u)) { const double2 d = g ? P.ops[%d].c[1] : P.ops[%d].c[0];\n",
@@ -418,6 +440,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
             o("      { const TileOp& so = big[%d];\n", op.ref);
             o("        if (!(sign_hit >> %u & 1u)) {\n", unsigned(op.sidx) & 31u);
             o("          if (so.flip_rest) { for (int q = 0; q < %d; ++q) v[q] = neg_exact(v[q]); }\n", G);
+            fp64(8 * G);
             o("        } else {\n");
             o("          const u64* f = flipped + so.flip_off;\n");
             for (int q = 0; q < G; ++q) {
@@ -432,6 +455,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
     }
     if (accumulate)
         for (int q = 0; q < G; ++q) o("      v[%d] = cmul_f(gs, v[%d]);\n", q, q);
+    if (accumulate) fp64(4 * G);
     if (R.flags & RD_SIGNS) o("      flip_signs1(v, negacc);\n");
     if (direct) {  // straight to HBM: logical index store(lb ^ off[q]) of the tile
         o("      { const unsigned sd = sd_t ^ %s;\n", kexpr(sk).c_str());
@@ -502,6 +526,18 @@ std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
     }
     o("}\n");
     return o.s;
+}
+
+// FP64 instructions per tile of the pass's main program as its specialised kernel runs it
+// (per thread, summed over the tile's 2^m / 8 groups)
+double fp64_per_tile(const PassParams& P) {
+    PassParams Q = P;
+    if (Q.alt_mode == ALT_ROUNDS) Q.alt_mode = ALT_NONE;  // the main program only
+    g_fp64 = 0.0;
+    (void)pass_source(Q, 0xffu, 256);
+    const double per_group = g_fp64;
+    g_fp64 = 0.0;
+    return per_group * double((1u << P.m) >> 3);
 }
 
 void nvrtc_check(nvrtcResult r, const char* what) {
@@ -765,6 +801,8 @@ std::size_t jit_compile_only(const PassParams& p) {
     tile_pass_shape(p, F, threads);
     return compile_cubin(pass_source(p, F, threads)).size();
 }
+
+double pass_fp64_per_tile(const PassParams& p) { return fp64_per_tile(p); }
 
 bool launch_tile_pass_jit(double2* amps, const PassParams& p, unsigned F, const TileOp* big_dev,
                           const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, const TmapParam& tmap,

@@ -194,6 +194,7 @@ bool launch_tile_pass_jit(double2* amps, const struct PassParams& p, unsigned F,
                           const std::uint64_t* flipped_dev, const std::uint64_t* tables_dev, const TmapParam& tmap,
                           unsigned tiles, unsigned threads, std::size_t smem, std::size_t smem_max, cudaStream_t st,
                           void** jit_slot = nullptr);
+double pass_fp64_per_tile(const struct PassParams& p);  // FP64 instructions per tile, specialised form (jit.cpp)
 int jit_mode();                      // 0 off, 1 passes with enough work (default), 2 every tile pass, 3 = 2 + pivots
 bool jit_pivot(int n, const struct PassParams& p);  // lower this pass's gates to the pivoted form
 bool jit_virtual(int n, int m, bool skip_pass);      // lower this pass's X-like gates to relabellings

@@ -631,7 +631,8 @@ def plan_stats(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOpt
     pass, round counts.  B200-specific; the reference has no planner."""
     opts = opts or SimOptions()
     arr, keep = _steps(c.steps)
-    o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)))
+    # from |initial>, as simulate() runs it (support tracking, the reset folded into pass 1)
+    o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)), 1, int(c.initial))
     info = L.qcs_plan_info()
     _check(L.lib().qcs_plan_stats(c.n, arr, len(c.steps), int(engine), C.byref(o), C.byref(info)))
     return {f: int(getattr(info, f)) for f, _ in L.qcs_plan_info._fields_}
