@@ -264,6 +264,15 @@ int qcs_set_jit_mode(int mode);
 int qcs_get_jit_mode(void);
 int qcs_plan_compile(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
                      int64_t* kernels, int64_t* cubin_bytes);
+/* Host-only addressing proof of that plan's specialised kernels (no compile): for every register
+ * round, the shared-memory addresses of every thread, group iteration and register -- under
+ * every combination of runtime relabelling terms -- must cover the tile's slots exactly once
+ * (in bounds, a permutation), and a relabelled last round's direct HBM stores likewise.
+ * QCS_ERR_SIM with the failing round on a violation; *passes = passes checked.  B200-specific
+ * (compute-sanitizer is not available on the GPU pool; this replaces its memcheck for these
+ * accesses). */
+int qcs_plan_verify(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
+                    int64_t* passes);
 
 /* ------------------------------------------------------------------ compressed structures
  * The device gate encoder: materialise step_matrix_dax / step_matrix_das (engine.hpp:38-39)

@@ -101,6 +101,8 @@ SIGNATURES = {
     "qcs_get_jit_mode": (C.c_int, []),
     "qcs_plan_compile": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "qcs_plan_verify": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
+                                  C.POINTER(C.c_int64)]),
     "qcs_step_dax": (C.c_int, [C.c_int, C.POINTER(qcs_placement), C.c_int, C.c_int, _P, _P, _P, C.c_uint64,
                                C.c_int, _U64]),
     "qcs_step_das": (C.c_int, [C.c_int, C.POINTER(qcs_placement), C.c_int, C.c_int, _P, _P, _P, C.c_uint64,

@@ -457,6 +457,15 @@ int qcs_plan_compile(int n, const qcs_step* steps, int num_steps, int engine, co
     });
 }
 
+int qcs_plan_verify(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
+                    int64_t* passes) {
+    return guarded([&] {
+        need(passes, "passes");
+        int64_t bytes = 0;
+        qcs::plan_compile(n, steps, num_steps, engine, opts, passes, &bytes, true);
+    });
+}
+
 // ---------------------------------------------------------------- compressed structures
 
 int qcs_step_dax(int n, const qcs_placement* placements, int num_placements, int device, uint64_t* rows,

@@ -771,7 +771,7 @@ void plan_stats(int n, const qcs_step* steps, int nsteps, int engine, const qcs_
 }
 
 void plan_compile(int n, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
-                  std::int64_t* kernels, std::int64_t* cubin_bytes) {
+                  std::int64_t* kernels, std::int64_t* cubin_bytes, bool verify_only) {
     validate_circuit(n, steps, nsteps);
     if (engine < QCS_ENGINE_DENSE || engine > QCS_ENGINE_RH_DAX) raise(QCS_ERR_ARG, "unknown engine");
     qcs_sim_options o{QCS_SIGN_LOGARITHM, 0, 1, 0, 0};
@@ -785,7 +785,7 @@ void plan_compile(int n, const qcs_step* steps, int nsteps, int engine, const qc
         lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
         for (std::size_t i = 0; i < low.passes.size(); ++i) {
             if (low.pass_ops[i].size() == 1) continue;
-            *cubin_bytes += std::int64_t(jit_compile_only(low.passes[i]));
+            *cubin_bytes += std::int64_t(jit_compile_only(low.passes[i], verify_only));
             ++*kernels;
         }
         ops.clear();

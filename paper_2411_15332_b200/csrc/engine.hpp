@@ -65,7 +65,7 @@ void apply_split(qcs_state* s, void* peer, int self_bit, int nsel, const int* se
 void plan_stats(int n, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
                 qcs_plan_info* out);
 void plan_compile(int n, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
-                  std::int64_t* kernels, std::int64_t* cubin_bytes);
+                  std::int64_t* kernels, std::int64_t* cubin_bytes, bool verify_only = false);
 void memory_report(int n, const qcs_step* steps, int nsteps, int engine, qcs_step_report* reports);
 void validate_circuit(int n, const qcs_step* steps, int nsteps);
 

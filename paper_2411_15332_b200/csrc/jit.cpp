@@ -62,6 +62,18 @@ struct Out {
 thread_local double g_fp64 = 0.0;
 void fp64(double k) { g_fp64 += k; }
 
+// Addressing proof (QCS_JIT_VERIFY=1 or qcs_plan_compile's verify mode): while a round is
+// generated, its address arithmetic is also evaluated for every thread, group iteration and
+// register, under every combination of the runtime relabelling terms, and must address each of
+// the tile's 2^m shared-memory slots exactly once (in bounds, a permutation) -- and likewise
+// the direct HBM stores of a relabelled last round.  compute-sanitizer is closed on this GPU
+// pool; this checks the one place where a bad shared-memory index could come from.
+bool verify_on() {
+    static const bool on = [] { const char* v = std::getenv("QCS_JIT_VERIFY"); return v && std::atoi(v) != 0; }();
+    return on;
+}
+thread_local bool g_verify = false;
+
 bool knob_swaps() {
     static const bool on = [] { const char* v = std::getenv("QCS_JIT_SWAPS"); return !v || std::atoi(v) != 0; }();
     return on;
@@ -305,6 +317,68 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
         }
         return e;
     };
+    if (g_verify || verify_on()) {
+        const unsigned tsz = 1u << P.m;
+        auto swz1 = [](unsigned j) { return j ^ ((j >> 3) & 7u); };
+        auto sw = [&](unsigned g) {  // lb_t of thread t: zeros at the register bits, then the swap
+            for (int i = 0; i < W; ++i) g = ((g >> R.r[i]) << (R.r[i] + 1)) | (g & ((1u << R.r[i]) - 1));
+            if (swap_a >= 0 && ((g >> swap_a) ^ (g >> swap_b)) & 1u) g ^= (1u << swap_a) | (1u << swap_b);
+            return g;
+        };
+        auto kx = [](const std::vector<unsigned>& v, unsigned k) {
+            unsigned x = 0;
+            for (std::size_t j = 0; j < v.size(); ++j)
+                if (k >> j & 1) x ^= v[j];
+            return x;
+        };
+        // the runtime relabelling terms XOR a tile-uniform constant into every address: a
+        // permutation of the tile stays one when each term lies inside the tile, so check that
+        // and prove the rest with the terms off
+        for (const auto& term : map.rt)
+            if (term.second >= tsz) raise(QCS_ERR_SIM, "internal: a runtime relabelling term leaves the tile");
+        for (const auto& term : store.rt)
+            if (term.second >= tsz) raise(QCS_ERR_SIM, "internal: a runtime relabelling term leaves the tile");
+        const std::size_t nrt = 0, nst = 0;
+        const unsigned nthreads = threads > ngroups ? ngroups : threads;
+        for (unsigned combo = 0; combo < (1u << nrt); ++combo) {
+            unsigned rtv = 0;
+            (void)combo;
+            std::vector<unsigned char> seen(tsz, 0);
+            for (unsigned t = 0; t < nthreads; ++t) {
+                const unsigned lbt = sw(t);
+                const unsigned plt = map.apply(lbt) ^ rtv;  // affine_expr(lb_t) ^ offset_expr
+                for (unsigned k = 0; k < iters; ++k) {
+                    const unsigned slb = swz1(plt ^ kx(pk, k));
+                    for (int q = 0; q < G; ++q) {
+                        const unsigned pos = slb ^ swz1(map.apply(off[q]) ^ map.b);
+                        if (pos >= tsz || seen[pos]++)
+                            raise(QCS_ERR_SIM, "internal: round " + std::to_string(ri) +
+                                                   " addresses a shared-memory slot twice or out of the tile");
+                    }
+                }
+            }
+        }
+        if (direct) {  // the last round's stores straight to HBM: a permutation of the tile too
+            for (unsigned combo = 0; combo < (1u << nst); ++combo) {
+                unsigned rtv = 0;
+                (void)combo;
+                std::vector<unsigned char> seen(tsz, 0);
+                for (unsigned t = 0; t < nthreads; ++t) {
+                    const unsigned sdt = store.apply(sw(t)) ^ rtv;
+                    for (unsigned k = 0; k < iters; ++k) {
+                        const unsigned sd = sdt ^ kx(sk, k);
+                        for (int q = 0; q < G; ++q) {
+                            const unsigned cq = store.apply(off[q]) ^ store.b;
+                            const unsigned loc = ((sd ^ cq) & 7u) | ((sd >> 3) << 3 ^ (cq >> 3) << 3);
+                            if (loc >= tsz || seen[loc]++)
+                                raise(QCS_ERR_SIM, "internal: direct stores of round " + std::to_string(ri) +
+                                                       " hit an amplitude twice or leave the tile");
+                        }
+                    }
+                }
+            }
+        }
+    }
     std::string lbx = "t";
     for (int i = 0; i < W; ++i) lbx = "insert_zero(" + lbx + ", " + std::to_string(R.r[i]) + ")";
     o("    unsigned lb_t = %s;\n", lbx.c_str());
@@ -796,9 +870,20 @@ void jit_prepare(int n, const std::vector<PassParams>& passes, const std::vector
         if (!g_cache.count(todo[i])) load(todo[i], cubins[i]);
 }
 
-std::size_t jit_compile_only(const PassParams& p) {
+std::size_t jit_compile_only(const PassParams& p, bool verify_only) {
     unsigned F = 0, threads = 0;
     tile_pass_shape(p, F, threads);
+    if (verify_only) {  // generate with the addressing proof on, no NVRTC
+        g_verify = true;
+        try {
+            (void)pass_source(p, F, threads);
+        } catch (...) {
+            g_verify = false;
+            throw;
+        }
+        g_verify = false;
+        return 0;
+    }
     return compile_cubin(pass_source(p, F, threads)).size();
 }
 

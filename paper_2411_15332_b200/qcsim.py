@@ -638,6 +638,18 @@ def plan_stats(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOpt
     return {f: int(getattr(info, f)) for f, _ in L.qcs_plan_info._fields_}
 
 
+def plan_verify(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOptions] = None) -> int:
+    """Host-only addressing proof of the plan's specialised kernels (qcs_plan_verify): raises
+    SimError if any register round's shared-memory addressing is not a permutation of its tile.
+    Returns the number of passes checked.  B200-specific."""
+    opts = opts or SimOptions()
+    arr, keep = _steps(c.steps)
+    o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)), 1, int(c.initial))
+    k = C.c_int64()
+    _check(L.lib().qcs_plan_verify(c.n, arr, len(c.steps), int(engine), C.byref(o), C.byref(k)))
+    return int(k.value)
+
+
 def set_jit_mode(mode: int) -> None:
     """0: every fused pass runs on the interpreter kernel; 1 (default): passes with enough work
     run as kernels specialised to their operation list (compiled once per structure, NVRTC);

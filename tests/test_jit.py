@@ -75,6 +75,30 @@ def test_generated_sources_compile(Q, cfg):
         assert r["cubin_bytes"] > 0
 
 
+def test_addressing_proof(Q, cfg):
+    """qcs_plan_verify (host only): every register round of every specialised pass kernel of the
+    BASELINE families and of random whole-catalog circuits, in every jit mode that changes the
+    generated code (relabellings, pivots), addresses each shared-memory slot of its tile exactly
+    once -- in bounds and a permutation -- for every thread, group iteration and register; and a
+    relabelled last round's direct HBM stores cover the tile exactly once.  (compute-sanitizer is
+    closed on the GPU pool; this is the memcheck of the generated kernels' data accesses.)"""
+    old = Q.jit_mode()
+    try:
+        for mode in (1, 3):
+            Q.set_jit_mode(mode)
+            checked = 0
+            for n in (12, 16, 20, 24, 28, 32):
+                checked += Q.plan_verify(cfg.c4_circuit(n, 10))
+                checked += Q.plan_verify(cfg.c5_circuit(max(n, 16), 20, global_qubits=2))
+                checked += Q.plan_verify(cfg.c3_circuit(n) if n >= 16 else cfg.c1_circuit())
+            for seed in range(6):
+                checked += Q.plan_verify(random_catalog_circuit(Q, seed, 13 + seed, 40))
+            checked += Q.plan_verify(sign_sandwich(Q, 15))
+            assert checked > 300
+    finally:
+        Q.set_jit_mode(old)
+
+
 def test_plans_do_not_depend_on_history(Q, cfg):
     """The same circuit plans the same way whatever was planned before (a read past the
     operation list once made relabelled plans depend on heap contents)."""
