@@ -26,7 +26,7 @@ COMMON = ["-O3", "-std=c++20", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC"
 COMMON += os.environ.get("QCS_EXTRA_NVCC", "").split()
 
 SOURCES = ["gates.cpp", "ops.cpp", "planner.cpp", "engine.cpp", "abi.cpp", "timing.cpp",
-           "gate_kernels.cu", "tile_kernels.cu", "state_kernels.cu", "encode_kernels.cu", "peer_kernels.cu", "sample_kernels.cu",
+           "gate_kernels.cu", "tile_kernels.cu", "state_kernels.cu", "encode_kernels.cu", "peer_kernels.cu", "sample_kernels.cu", "dense_kernels.cu",
            "jit.cpp"]
 # embedded into the library for the run-time (NVRTC) pass kernels, jit.cpp
 JIT_HEADERS = [("kJitSrcKernels", "kernels.hpp"), ("kJitSrcDevice", "tile_device.cuh")]

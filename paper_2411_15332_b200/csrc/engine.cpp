@@ -612,6 +612,70 @@ void plan_key(int n, int engine, const qcs_sim_options& o, const qcs_step* steps
 }
 }  // namespace
 
+namespace {
+
+// The Matrix method (engine == dense): step_matrix_dense on the device, then dense_mvm into a
+// scratch vector, copied back in place -- byte for byte the reference's dense engine
+// (engine.cpp:126-133, :180-188; core.cpp:55-87).  Steps with a placement the reference cannot
+// express (non-contiguous or reversed qubits) return false: the caller runs that step through
+// the fused kernels (same operator; no reference bytes exist to match).
+bool run_dense_step(qcs_state* s, const qcs_step& st) {
+    const int n = s->n;
+    const u64 dim = u64(1) << n;
+    DenseFold fold{};
+    if (st.kind == QCS_STEP_GATES) {
+        std::vector<const qcs_placement*> at(std::size_t(n), nullptr);
+        for (int j = 0; j < st.num_placements; ++j) {
+            const qcs_placement& p = st.placements[j];
+            for (int k = 1; k < p.arity; ++k)
+                if (p.qubits[k] != p.qubits[0] + k) return false;
+            at[std::size_t(p.qubits[0])] = &p;
+        }
+        int off = 0;
+        for (int q = 0; q < n;) {
+            if (fold.nfactors >= 32) raise(QCS_ERR_CAPACITY, "dense engine: too many factors");
+            const qcs_placement* p = at[std::size_t(q)];
+            const int k = p ? p->arity : 1;
+            const int d = 1 << k;
+            if (off + d * d > 512) raise(QCS_ERR_CAPACITY, "dense engine: factors too large");
+            fold.arity[fold.nfactors] = k;
+            fold.offset[fold.nfactors] = off;
+            for (int e = 0; e < d * d; ++e)
+                fold.mat[off + e] = p ? make_double2(p->matrix[2 * e], p->matrix[2 * e + 1])
+                                      : make_double2((e == 0 || e == 3) ? 1.0 : 0.0, 0.0);
+            off += d * d;
+            ++fold.nfactors;
+            q += k;
+        }
+    }
+    double2* mat = nullptr;
+    double2* out = nullptr;
+    QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mat), dim * dim * sizeof(double2), s->stream));
+    QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out), dim * sizeof(double2), s->stream));
+    u64* flips = nullptr;
+    if (st.kind == QCS_STEP_DIAG) {
+        std::vector<u64> f(st.flipped, st.flipped + st.num_flipped);
+        std::sort(f.begin(), f.end());
+        f.erase(std::unique(f.begin(), f.end()), f.end());
+        QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flips), std::max<std::size_t>(1, f.size()) * sizeof(u64),
+                                 s->stream));
+        if (!f.empty())
+            QCS_CUDA(cudaMemcpyAsync(flips, f.data(), f.size() * sizeof(u64), cudaMemcpyHostToDevice, s->stream));
+        dense_diag(mat, n, flips, f.size(), st.flip_rest, s->stream);
+        QCS_CUDA(cudaStreamSynchronize(s->stream));  // the host list must outlive the copy
+    } else {
+        dense_build(mat, n, fold, s->stream);
+    }
+    dense_mvm(mat, s->amps, out, n, s->stream);
+    QCS_CUDA(cudaMemcpyAsync(s->amps, out, dim * sizeof(double2), cudaMemcpyDeviceToDevice, s->stream));
+    QCS_CUDA(cudaFreeAsync(mat, s->stream));
+    QCS_CUDA(cudaFreeAsync(out, s->stream));
+    if (flips) QCS_CUDA(cudaFreeAsync(flips, s->stream));
+    return true;
+}
+
+}  // namespace
+
 void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const qcs_sim_options* opts,
               qcs_step_report* reports) {
     const int n = s->n;
@@ -629,7 +693,8 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
     // device plan buffer still holds its tables, their upload
     std::vector<unsigned char> key;
     static const bool no_cache = std::getenv("QCS_NO_PLAN_CACHE") != nullptr;  // A/B switch
-    if (o.fuse && !no_cache) {
+    const bool matrix_method = engine == QCS_ENGINE_DENSE;
+    if (o.fuse && !no_cache && !matrix_method) {
         plan_key(n, engine, o, steps, nsteps, key);
         if (!s->plan_cache) s->plan_cache = new PlanCache;
         if (CachedPlan* hit = s->plan_cache->find(key)) {
@@ -647,7 +712,7 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
         r.stage = st.stage;
         r.dense_bytes = dense_step_bytes(n);
         const bool use_rh = engine == QCS_ENGINE_RH_DAX && is_hadamard_all(st, n);
-        if (!o.fuse) ops.clear();
+        if (!o.fuse || matrix_method) ops.clear();
         append_step_ops(n, st, use_rh, ops);
         if (use_rh) {
             r.structure = QCS_STRUCT_RH;
@@ -675,11 +740,24 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
                 r.madd_count = nnz;         // engine.cpp:191, :199
             }
         }
-        if (!o.fuse) run_fused(s, ops, &init);  // one step: fused only within the step
+        if (matrix_method) {
+            if (init >= 0) {
+                fill_basis(s->amps, dim, u64(init), s->stream);
+                init = -1;
+            }
+            if (run_dense_step(s, st)) {
+                ops.clear();
+            } else {  // a placement the reference cannot place: this step through the fused kernels
+                run_fused(s, ops, &init);
+                ops.clear();
+            }
+        } else if (!o.fuse) {
+            run_fused(s, ops, &init);  // one step: fused only within the step
+        }
         reps[std::size_t(i)] = r;
     }
     if (reports) std::copy(reps.begin(), reps.end(), reports);
-    if (o.fuse) {
+    if (o.fuse && !matrix_method) {
         merge_single_qubit(n, ops);
         split_phases(ops);
         if (!ops.empty() && no_cache) {

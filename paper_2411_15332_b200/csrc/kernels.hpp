@@ -45,6 +45,19 @@ struct GateDesc {
 // Kernel classes chosen by the host from the descriptor (for launch shape / specialisation).
 void launch_gate(double2* amps, int n, const GateDesc& d, cudaStream_t st);
 
+// ---------------------------------------------------------------- the Matrix method (dense engine)
+// step_matrix_dense's factors in fold order (most significant qubit first): factor f covers
+// arity[f] index bits, its 2^k x 2^k row-major entries at mat[offset[f]].
+struct DenseFold {
+    int nfactors;
+    int arity[32];
+    int offset[32];
+    double2 mat[512];
+};
+void dense_build(double2* m, int n, const DenseFold& fold, cudaStream_t st);
+void dense_diag(double2* m, int n, const std::uint64_t* flipped_dev, std::uint64_t nf, int rest, cudaStream_t st);
+void dense_mvm(const double2* m, const double2* x, double2* out, int n, cudaStream_t st);
+
 // ---------------------------------------------------------------- diagonal sign step
 // negate amplitudes whose index is (listed XOR flip_rest); `flipped` is a sorted device array.
 void launch_diag_sign(double2* amps, int n, const std::uint64_t* flipped_dev, std::uint64_t nflip,

@@ -431,6 +431,14 @@ class DeviceState:
         _check(L.lib().qcs_sample(self._h, seed & 0xFFFFFFFFFFFFFFFF, count, out, C.byref(tot)))
         return list(out)[:count], tot.value
 
+    def rh_mvm(self, value: float, method: "SignMethod" = None, block_size: int = 0):
+        """rh_mvm(RhMatrix{n, value}, s, method, &stats, block_size) in place (qcs_rh_mvm,
+        rh.hpp:64-66): returns (sign_count, madd_count) as RhMvmStats."""
+        m = int(SignMethod.logarithm if method is None else method)
+        sc, mc = C.c_uint64(), C.c_uint64()
+        _check(L.lib().qcs_rh_mvm(self._h, self.n, float(value), m, int(block_size), C.byref(sc), C.byref(mc)))
+        return int(sc.value), int(mc.value)
+
     def gather(self, indices) -> np.ndarray:
         idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
         out = np.empty(idx.size, np.complex128)
@@ -778,6 +786,60 @@ def rh_mvm(s: DeviceState) -> DeviceState:
     out.copy_from(s)
     out.apply_rh()
     return out
+
+
+def dense_cap() -> int:  # core.hpp:38-44 (the dense engine's element cap)
+    return int(L.lib().qcs_dense_cap())
+
+
+def set_dense_cap(cap: int) -> None:
+    _check(L.lib().qcs_set_dense_cap(int(cap)))
+
+
+class DeviceEncoded:
+    """A step's DAX or DAS structure materialised in DEVICE memory by the device encoder
+    (qcs_step_dax / qcs_step_das with QCS_MEM_DEVICE), for the device MVMs -- the reference's
+    step_matrix_* + *_mvm pipeline (engine.cpp:192-199) without host round trips."""
+
+    def __init__(self, step: CircuitStep, n: int, das: bool, device: int = 0):
+        import torch
+        self.n, self.das, self.device = n, das, device
+        arr, keep = _placements(step.placements)
+        fn = L.lib().qcs_step_das if das else L.lib().qcs_step_dax
+        cnt = C.c_uint64()
+        rc = fn(n, arr, len(step.placements), device, None, None, None, 0, L.QCS_MEM_DEVICE, C.byref(cnt))
+        if rc not in (L.QCS_OK, L.QCS_ERR_CAPACITY):
+            _check(rc)
+        k = int(cnt.value)
+        dev = torch.device("cuda", device)
+        self.a = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
+        self.b = torch.empty(max(k, 1), dtype=torch.uint8 if das else torch.int64, device=dev)
+        self.v = torch.empty(max(k, 1), dtype=torch.complex128, device=dev)
+        _check(fn(n, arr, len(step.placements), device, C.c_void_p(self.a.data_ptr()), C.c_void_p(self.b.data_ptr()),
+                  C.c_void_p(self.v.data_ptr()), k, L.QCS_MEM_DEVICE, C.byref(cnt)))
+        self.count = int(cnt.value)
+        torch.cuda.synchronize(dev)
+
+    def mvm(self, s: "DeviceState", out: "DeviceState") -> None:
+        """out = M s (dax.cpp:96-103 / das.cpp:131-150) on the device entries."""
+        ptr = lambda t: C.c_void_p(t.data_ptr())
+        if self.das:
+            _check(L.lib().qcs_das_mvm(ptr(self.a), ptr(self.b), ptr(self.v), self.count, L.QCS_MEM_DEVICE,
+                                       s.handle, out.handle))
+        else:
+            _check(L.lib().qcs_dax_mvm(ptr(self.a), ptr(self.b), ptr(self.v), self.count, L.QCS_MEM_DEVICE,
+                                       s.handle, out.handle))
+
+    def close(self) -> None:
+        self.a = self.b = self.v = None
+
+
+def step_matrix_dax_device(step: CircuitStep, n: int, device: int = 0) -> DeviceEncoded:
+    return DeviceEncoded(step, n, False, device)
+
+
+def step_matrix_das_device(step: CircuitStep, n: int, device: int = 0) -> DeviceEncoded:
+    return DeviceEncoded(step, n, True, device)
 
 
 def rh_build_value(n: int) -> float:  # rh.cpp:18-21
