@@ -543,7 +543,9 @@ void pivot_pass(PassParams& P, int& npool) {
                     // the generated source -- and so the compiled kernel -- independent of the
                     // angles (a variational circuit with new angles reuses its kernels)
                     const double ad = std::abs(r ? a1 : a0), ao = std::abs(r ? a0 : a1);
-                    const int pv = (ad > 0.0 && ad >= 0x1p-20 * ao) ? r : 1 - r;
+                    static const bool larger = knob("QCS_PIVOT_LARGER");  // A/B: round-1 rule
+                    const int pv = larger ? (std::abs(a1) > std::abs(a0) ? 1 : 0)
+                                          : ((ad > 0.0 && ad >= 0x1p-20 * ao) ? r : 1 - r);
                     scale[r] = pv ? a1 : a0;
                     rho[r] = (pv ? a0 : a1) / scale[r];
                     piv |= unsigned(pv) << (4 * fb + r);
@@ -1381,7 +1383,12 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
         {
             std::vector<FOp> sched_ops;
             std::vector<int> sched_list;
-            if (!has_alt[pi] && schedule_rounds(n, loc, P.m, ops, lists[pi], sched_ops, sched_list))
+            // passes whose X-like gates become virtual relabellings keep their order: the
+            // relabellings need no register bits, and the scheduler's round count would not see that
+            bool perms = false;
+            if (virt_pass)
+                for (int idx : lists[pi]) perms |= is_perm(ops[std::size_t(idx)]);
+            if (!has_alt[pi] && !perms && schedule_rounds(n, loc, P.m, ops, lists[pi], sched_ops, sched_list))
                 lower_list(sched_ops, sched_list);
             else
                 lower_list(ops, lists[pi]);
