@@ -337,6 +337,25 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
         g.S = S;
         return g;
     };
+    // dims of the tile's TMA tensor map (tile_tensor_map): bits 0..2, then every run of tile bits
+    // (split at 8 bits) and every run of other bits; > 5 falls back to per-thread cp.async tiles,
+    // which cost the pass ~15% more instructions (address arithmetic per 16 bytes)
+    auto tma_dims = [&](u64 S) {
+        int rank = 1;
+        for (int b = 3; b < n;) {
+            const bool in = S >> b & 1;
+            int e = b;
+            while (e < n && bool(S >> e & 1) == in) ++e;
+            rank += in ? (e - b + 7) / 8 : 1;
+            b = e;
+        }
+        return rank;
+    };
+    static const double tma_weight = [] {
+        const char* v = std::getenv("QCS_TILE_TMA_WEIGHT");
+        return v ? std::atof(v) : 0.85;
+    }();
+    auto score = [&](const Grown& g) { return double(g.gates) * (tma_dims(g.S) > 5 ? tma_weight : 1.0); };
     while (!remaining.empty()) {
         Grown best = grow(0);
         // Tile search: the circuit-order tile fills with the first new bits it meets, which for a
@@ -371,9 +390,14 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
                 for (int i = 0; i < f.K; ++i) t |= u64(1) << f.tpos[i];
                 if (std::find(seeds.begin(), seeds.end(), t) == seeds.end()) seeds.push_back(t);
             }
+            double best_score = score(best);
             for (u64 seed : seeds) {
                 Grown g = grow(seed);
-                if (!g.signs && g.gates > best.gates) best = std::move(g);
+                const double sc = score(g);
+                if (!g.signs && sc > best_score) {
+                    best_score = sc;
+                    best = std::move(g);
+                }
             }
         }
         plan.passes.push_back(PlannedPass{best.S, best.chosen});
