@@ -177,7 +177,8 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
     std::uint8_t alt_mode;
     std::uint16_t alt_begin, alt_nrounds;
     std::uint32_t hi_off;     // this pass's table of run offsets (tile bits 3..m-1) in the plan's tables
-    int tma_rank;             // > 0: the tile moves as one TMA box of this rank (set at launch)
+    int tma_rank;             // > 0: the tile moves as TMA boxes of this rank (set at launch)
+    std::uint8_t tma_iter;    // the top tma_iter local tile bits are iterated: 2^tma_iter boxes per tile
     std::uint8_t tma_gap_pos[5], tma_gap_len[5];  // box dims over bits outside the tile: coordinate bits
     int nruns;                // the basis bits outside the tile, as runs: a tile index deposits into them
     std::uint8_t run_pos[16], run_len[16];

@@ -113,7 +113,18 @@ __device__ __forceinline__ void tma_store(const TmapParam* map, const int (&c)[5
                 : "memory");
             break;
     }
+}
+__device__ __forceinline__ void tma_store_commit_wait() {
     asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+// coordinates of box i of a tile whose top `iter` local bits are iterated: the tile base with i
+// deposited into those bits, read out per gap dimension
+__device__ __forceinline__ void tma_box_coords(const PassParams& P, u64 base, unsigned i, int (&cc)[5]) {
+    u64 g = base;
+    for (int k = 0; k < int(P.tma_iter); ++k)
+        if (i >> k & 1) g |= u64(1) << P.bits[P.m - int(P.tma_iter) + k];
+    for (int d = 0; d < 5; ++d)
+        cc[d] = (d < P.tma_rank && P.tma_gap_len[d]) ? int((g >> P.tma_gap_pos[d]) & ((u64(1) << P.tma_gap_len[d]) - 1)) : 0;
 }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\nfence.mbarrier_init.release.cluster;\n" ::"r"(smem_u32(bar))
@@ -481,7 +492,16 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
         if (t == 0) {
             mbar_init(c.bar);
             mbar_expect_tx(c.bar, sz * 16u);
-            tma_load(c.sm, &tmap, c.tc, P.tma_rank, c.bar);
+            if (!P.tma_iter) {
+                tma_load(c.sm, &tmap, c.tc, P.tma_rank, c.bar);
+            } else {  // one box per value of the iterated top local bits, contiguous in shared memory
+                const unsigned nb = 1u << P.tma_iter, chunk = sz >> P.tma_iter;
+                for (unsigned i = 0; i < nb; ++i) {
+                    int cc[5];
+                    tma_box_coords(P, base, i, cc);
+                    tma_load(c.sm + i * chunk, &tmap, cc, P.tma_rank, c.bar);
+                }
+            }
         }
     }
     cp_async_wait_all();  // the run-offset table
@@ -508,7 +528,19 @@ __device__ __forceinline__ void tile_end(double2* a, const PassParams& P, const 
     if (P.tma_rank) {  // the tile back as one TMA box
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();
-        if (t == 0) tma_store(&tmap, c.tc, P.tma_rank, c.sm);
+        if (t == 0) {
+            if (!P.tma_iter) {
+                tma_store(&tmap, c.tc, P.tma_rank, c.sm);
+            } else {
+                const unsigned nb = 1u << P.tma_iter, chunk = sz >> P.tma_iter;
+                for (unsigned i = 0; i < nb; ++i) {
+                    int cc[5];
+                    tma_box_coords(P, c.base, i, cc);
+                    tma_store(&tmap, cc, P.tma_rank, c.sm + i * chunk);
+                }
+            }
+            tma_store_commit_wait();
+        }
     } else if (t < sz) {
         const u64 gt = c.base | (t & 7u) | c.hi_tab[t >> 3];
         const unsigned rs = bt >> 3;

@@ -295,8 +295,33 @@ bool tile_tensor_map(double2* amps, int n, PassParams& p, CUtensorMap* map) {
             cudaGetLastError();
     }
     if (!encode || n > 36 || p.m < 3) return false;
+    // the boxes cover the lowest m - iter local bits; the top `iter` ones are iterated (one box per
+    // value, contiguous in shared memory): the fewest iterated bits that bring the map to <= 5
+    // dims, with boxes of at least 64 amplitudes (1 KB)
+    auto dims = [&](u64 S) {
+        int rank = 1;
+        for (int b = 3; b < n;) {
+            const bool in = S >> b & 1;
+            int e = b;
+            while (e < n && bool(S >> e & 1) == in) ++e;
+            if (!in && e - b > 31) return 99;
+            rank += in ? (e - b + 7) / 8 : 1;
+            b = e;
+        }
+        return rank;
+    };
+    static const bool no_iter = std::getenv("QCS_NO_TMA_ITER") != nullptr;  // A/B switch
+    // at most a few big boxes: many small ones (C5's scattered tiles: 32+ boxes of 1-2 KB) were
+    // slower than the per-thread cp.async tile (877 vs 819 ms per C5-family circuit at n=32)
+    static const int max_iter = [] { const char* v = std::getenv("QCS_TMA_MAX_ITER"); return v ? std::atoi(v) : 2; }();
+    int iter = 0;
     u64 tile = 0;
     for (int b = 0; b < p.m; ++b) tile |= u64(1) << p.bits[b];
+    while (dims(tile) > 5) {
+        if (no_iter || iter >= max_iter || p.m - iter - 1 < 6) return false;
+        tile &= ~(u64(1) << p.bits[p.m - 1 - iter]);
+        ++iter;
+    }
     cuuint64_t gdim[5], gstride[4];
     cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
     int rank = 1;
@@ -331,6 +356,7 @@ bool tile_tensor_map(double2* amps, int n, PassParams& p, CUtensorMap* map) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     p.tma_rank = rank;
+    p.tma_iter = std::uint8_t(iter);
     for (int d = 0; d < 5; ++d) {
         p.tma_gap_pos[d] = gpos[d];
         p.tma_gap_len[d] = glen[d];
@@ -361,6 +387,7 @@ void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev
     const std::size_t smem = tile_smem(p.m);
     TmapParam tmap{};
     p.tma_rank = 0;
+    p.tma_iter = 0;
     if (QCS_TILE_TMA) tile_tensor_map(amps, n, p, reinterpret_cast<CUtensorMap*>(&tmap));
     const u64 tiles = p.list_cnt ? u64(p.list_cnt) : u64(1) << (n - p.m);
     if (tiles > 0x7fffffffull) raise(QCS_ERR_CAPACITY, "too many tiles for one launch");
