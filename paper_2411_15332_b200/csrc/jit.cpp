@@ -117,12 +117,123 @@ std::string const_bits(bool c0, bool c1, int dk, int p0, int p1) {
     return e;
 }
 
+// Lazy +-1 sign flips (round 2).  The CZ ring between a round's two layers and the Z-like parts
+// of gates leave registers negated; the interpreter (and round 1) xor-ed the sign bits of all
+// eight registers before every later gate (~4 integer instructions per amplitude per flush).
+// Here the pending signs are tracked while the round is generated -- a compile-time mask `ct`
+// plus runtime terms that are linear in the register index (group-constant phase bits times a
+// register bit: rs0..rs2, or all registers: rsc) -- and consumed for free where the arithmetic
+// allows: a pivoted gate takes a pair's sign difference as the sign of its ratio (an operand
+// negation in the DFMA; a runtime difference flips the ratio once per group) and passes the
+// signs on to its outputs; the round's diagonal table takes them as signed entries.  Anything
+// else (butterflies, non-pivoted gates, sign steps, the round's end) flushes them first.  Sign
+// flips are exact, so the results are bit for bit those of flushing early.
+// Measured on B200 (tools/gpu_r02p.sh, three alternating repetitions): C4 n=32 276.5 ms with the
+// track, 268.5 ms without -- slower: the ratio flips and signed table entries sit on the FMA
+// critical path where the xor flushes did not.  Kept as an option (QCS_JIT_LAZY_SIGNS=1).
+bool knob_lazy_signs() {
+    static const bool on = [] { const char* v = std::getenv("QCS_JIT_LAZY_SIGNS"); return v && std::atoi(v) != 0; }();
+    return on;
+}
+
+struct SignTrack {
+    unsigned ct = 0;           // compile-time: registers negated
+    bool rt[4] = {};           // runtime terms pending in rs0, rs1, rs2 (registers with bit b set), rsc (all)
+    bool any() const { return ct || rt[0] || rt[1] || rt[2] || rt[3]; }
+};
+const char* const kRs[4] = {"rs0", "rs1", "rs2", "rsc"};
+
+// the runtime part of register q's sign as a source expression ("" when none)
+std::string rt_parity(const SignTrack& st, int q) {
+    std::string e;
+    for (int b = 0; b < 4; ++b)
+        if (st.rt[b] && (b == 3 || (q >> b & 1))) e += (e.empty() ? "" : " ^ ") + std::string(kRs[b]);
+    return e;
+}
+
+void sign_reset_rt(Out& o, SignTrack& st) {
+    for (int b = 0; b < 4; ++b)
+        if (st.rt[b]) {
+            o("      %s = 0u;\n", kRs[b]);
+            st.rt[b] = false;
+        }
+}
+
+// apply every pending sign to the registers (xor of sign bits) and clear the track
+void sign_flush(Out& o, SignTrack& st) {
+    if (!st.any()) return;
+    std::string m = std::to_string(st.ct) + "u";
+    static const unsigned pat[4] = {0xaau, 0xccu, 0xf0u, 0xffu};
+    for (int b = 0; b < 4; ++b)
+        if (st.rt[b]) m += " ^ ((0u - " + std::string(kRs[b]) + ") & " + std::to_string(pat[b]) + "u)";
+    o("      flip_mask(v, %s);\n", m.c_str());
+    st.ct = 0;
+    sign_reset_rt(o, st);
+}
+
+// a +-1 diagonal whose flipped registers are byte cg of smask when the group-constant phase
+// bits spell cg: the cg-independent part joins ct; each runtime part must be affine-linear in the
+// register index (then it becomes rs terms); false (nothing emitted) otherwise
+bool sign_add(Out& o, SignTrack& st, unsigned long long smask, bool c0, bool c1, int dk, int p0, int p1) {
+    auto byte = [&](int cg) { return unsigned(smask >> (8 * cg)) & 0xffu; };
+    std::string ue, we;  // cg bit 1 and bit 0 as runtime 0/1 expressions
+    char buf[64];
+    if (dk == 2 && c0) { std::snprintf(buf, sizeof(buf), "unsigned((g0 >> %d) & 1)", p0); ue = buf; }
+    if (dk == 2 && c1) { std::snprintf(buf, sizeof(buf), "unsigned((g0 >> %d) & 1)", p1); we = buf; }
+    if (dk == 1 && c0) { std::snprintf(buf, sizeof(buf), "unsigned((g0 >> %d) & 1)", p0); we = buf; }
+    const unsigned f0 = byte(0);
+    struct Term { unsigned m; std::string e; };
+    std::vector<Term> terms;
+    if (!we.empty()) terms.push_back({byte(1) ^ f0, we});
+    if (!ue.empty()) terms.push_back({byte(2) ^ f0, ue});
+    if (!we.empty() && !ue.empty()) terms.push_back({byte(3) ^ byte(2) ^ byte(1) ^ f0, "(" + ue + " & " + we + ")"});
+    struct Lin { bool a0, a[3]; };
+    std::vector<Lin> lins;
+    for (const Term& t : terms) {
+        Lin l{};
+        l.a0 = t.m & 1u;
+        for (int b = 0; b < 3; ++b) l.a[b] = ((t.m >> (1 << b)) & 1u) != l.a0;
+        for (int q = 0; q < 8; ++q) {
+            bool v = l.a0;
+            for (int b = 0; b < 3; ++b) v ^= l.a[b] && (q >> b & 1);
+            if (v != bool(t.m >> q & 1u)) return false;
+        }
+        lins.push_back(l);
+    }
+    st.ct ^= f0;
+    for (std::size_t i = 0; i < terms.size(); ++i) {
+        if (!terms[i].m) continue;
+        for (int b = 0; b < 3; ++b)
+            if (lins[i].a[b]) {
+                o("      %s ^= %s;\n", kRs[b], terms[i].e.c_str());
+                st.rt[b] = true;
+            }
+        if (lins[i].a0) {
+            o("      rsc ^= %s;\n", terms[i].e.c_str());
+            st.rt[3] = true;
+        }
+    }
+    return true;
+}
+
 // A one-target gate on register bit t of the registers in `en` (a literal mask): X-like gates
 // (exactly [[0, 1], [1, 0]]) are register swaps -- no arithmetic, value-identical to the
 // interpreter's 0*x0 + 1*x1 up to the sign of an exact zero -- the others the real or complex
 // 2x2 forms of tile_device.cuh.
-void emit_gate(Out& o, int kb, int t, const double2* c, const std::string& coef, unsigned en, int G, unsigned piv) {
+void emit_gate(Out& o, int kb, int t, const double2* c, const std::string& coef, unsigned en, int G, unsigned piv,
+               SignTrack* st = nullptr) {
     const unsigned all = (1u << G) - 1;
+    // pending signs: a pivoted or swap gate on all registers consumes / permutes them; any other
+    // gate needs them applied first
+    auto swap_bits = [&](unsigned m) {  // exchange the sign bits of each pair along t
+        unsigned r = m;
+        for (int q = 0; q < G; ++q)
+            if (!(q >> t & 1)) {
+                const unsigned a = m >> q & 1u, b = m >> (q | (1 << t)) & 1u;
+                r = (r & ~((1u << q) | (1u << (q | (1 << t))))) | (b << q) | (a << (q | (1 << t)));
+            }
+        return r;
+    };
     auto pairs = [&](unsigned e) {
         int k = 0;
         for (int q = 0; q < G; ++q)
@@ -132,13 +243,51 @@ void emit_gate(Out& o, int kb, int t, const double2* c, const std::string& coef,
     if (kb & KF_PIVOT) {  // piv: this bit's 4 pivot flags
         const int per_row = (kb & KF_REAL) ? 2 : 4;
         fp64(double(pairs(en & all)) * (((piv >> 2 & 1) ? 0 : per_row) + ((piv >> 3 & 1) ? 0 : per_row)));
+        const int P0 = int(piv & 1), P1 = int(piv >> 1 & 1);
+        if (st && st->any() && (en & all) != all && !(P0 == 0 && P1 == 1)) sign_flush(o, *st);
+        unsigned neg = 0;
+        std::string r0 = "(" + coef + ")[0]", r1 = "(" + coef + ")[1]";
+        if (st && st->any()) {
+            for (int q = 0; q < G; ++q)
+                if (!(q >> t & 1) && ((st->ct >> q) ^ (st->ct >> (q | (1 << t)))) & 1u) neg |= 1u << q;
+            if (st->rt[t]) {  // the runtime sign difference of every pair along t: flip the ratios
+                r0 = "flipd2(" + r0 + ", " + kRs[t] + ")";
+                r1 = "flipd2(" + r1 + ", " + kRs[t] + ")";
+            }
+        }
         if (en & all)
-            o("      gate1p<%d, %d, %d, %d, %d, %d, 0x%xu>(v, (%s)[0], (%s)[1]);\n", t, int(piv & 1), int(piv >> 1 & 1),
-              int(piv >> 2 & 1), int(piv >> 3 & 1), (kb & KF_REAL) ? 1 : 0, en & all, coef.c_str(), coef.c_str());
+            o("      gate1p<%d, %d, %d, %d, %d, %d, 0x%xu, 0x%xu>(v, %s, %s);\n", t, P0, P1, int(piv >> 2 & 1),
+              int(piv >> 3 & 1), (kb & KF_REAL) ? 1 : 0, en & all, neg, r0.c_str(), r1.c_str());
+        if (st && st->any()) {  // the outputs carry the sign of their row's pivot input
+            if (P0 == 1 && P1 == 0) {
+                st->ct = swap_bits(st->ct);
+                if (st->rt[t]) { o("      rsc ^= %s;\n", kRs[t]); st->rt[3] = true; }
+            } else if (P0 == 0 && P1 == 0) {
+                for (int q = 0; q < G; ++q)
+                    if (!(q >> t & 1)) st->ct = (st->ct & ~(1u << (q | (1 << t)))) | ((st->ct >> q & 1u) << (q | (1 << t)));
+                if (st->rt[t]) { o("      %s = 0u;\n", kRs[t]); st->rt[t] = false; }
+            } else if (P0 == 1 && P1 == 1) {
+                for (int q = 0; q < G; ++q)
+                    if (!(q >> t & 1)) st->ct = (st->ct & ~(1u << q)) | ((st->ct >> (q | (1 << t)) & 1u) << q);
+                if (st->rt[t]) {
+                    o("      rsc ^= %s; %s = 0u;\n", kRs[t], kRs[t]);
+                    st->rt[3] = true;
+                    st->rt[t] = false;
+                }
+            }
+        }
         return;
     }
     const bool swap = c[0].x == 0.0 && c[0].y == 0.0 && c[3].x == 0.0 && c[3].y == 0.0 && c[1].x == 1.0 &&
                       c[1].y == 0.0 && c[2].x == 1.0 && c[2].y == 0.0 && knob_swaps();
+    if (st && st->any()) {
+        if (swap && (en & all) == all) {  // a register swap permutes the pending signs
+            st->ct = swap_bits(st->ct);
+            if (st->rt[t]) { o("      rsc ^= %s;\n", kRs[t]); st->rt[3] = true; }
+        } else {
+            sign_flush(o, *st);
+        }
+    }
     if (swap) {
         for (int q = 0; q < G; ++q)
             if (!(q >> t & 1) && (en >> q & 1))
@@ -414,15 +563,39 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
     const bool accumulate = nconst >= 2 && has_pivot(P);
     if (accumulate) o("      double2 gs = make_double2(1.0, 0.0);\n");
     o("      (void)g0; (void)negacc;\n");
+    const bool lazy = knob_lazy_signs();
+    SignTrack st;
+    SignTrack* stp = lazy ? &st : nullptr;
+    if (lazy) o("      unsigned rs0 = 0u, rs1 = 0u, rs2 = 0u, rsc = 0u;\n      (void)rs0; (void)rs1; (void)rs2; (void)rsc;\n");
     for (int oi = ob; oi < te; ++oi) {
         const RegOp& op = P.ops[oi];
         const int kb = op.kind, kind = kb & KF_KIND;
         if (kind == TOP_PERM) raise(QCS_ERR_SIM, "internal: relabelling inside a round");
-        if (kb & KF_FLUSH) o("      flip_signs1(v, negacc);\n");
+        if (!lazy && (kb & KF_FLUSH)) o("      flip_signs1(v, negacc);\n");
+        // lazy signs: operations that neither commute with pending flips nor consume them
+        if (lazy && (kind == TOP_WHT || kind == TOP_SIGN || (kind == TOP_GATE && (kb & KF_GCTRL)))) sign_flush(o, st);
         const bool gc = kb & KF_GCTRL;
         if (gc) o("      if ((base & 0x%llxull) == 0x%llxull) {\n", (unsigned long long)op.gctrl_mask,
                   (unsigned long long)op.gctrl_val);
-        if (kind == TOP_DIAG && (kb & KF_SIGNED) && (kb & KF_BUNDLE)) {
+        if (lazy && kind == TOP_DIAG && (kb & KF_SIGNED)) {
+            // +-1 diagonals into the sign track; a pattern that is not affine in the register
+            // index (never in the BASELINE circuits) is applied at once
+            auto one = [&](unsigned long long sm, bool c0, bool c1, int dk, int p0, int p1) {
+                if (sign_add(o, st, sm, c0, c1, dk, p0, p1)) return;
+                o("      flip_mask(v, unsigned(0x%llxull >> (%d * (%s))) & 0x%llxu);\n", sm, G,
+                  const_bits(c0, c1, dk, p0, p1).c_str(), gmask);
+            };
+            if (kb & KF_BUNDLE) {
+                st.ct ^= unsigned(op.smask & gmask);
+                for (int i = 0; i < op.t; ++i) {
+                    SignEntry e;
+                    std::memcpy(&e, &P.pool[op.ref + i], sizeof(e));
+                    one(e.smask, e.cmask & 1u, e.cmask & 2u, e.dk, e.p0, e.p1);
+                }
+            } else {
+                one(op.smask, op.dreg[0] == 0xff, op.dk == 2 && op.dreg[1] == 0xff, op.dk, op.dpos[0], op.dpos[1]);
+            }
+        } else if (kind == TOP_DIAG && (kb & KF_SIGNED) && (kb & KF_BUNDLE)) {
             o("      { unsigned acc = 0x%llxu;\n", (unsigned long long)(op.smask & gmask));
             for (int i = 0; i < op.t; ++i) {
                 SignEntry e;
@@ -448,7 +621,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
         } else if (kind == TOP_GATE && (kb & KF_BUNDLE)) {
             for (int b = 0; b < W; ++b)
                 if (op.t >> b & 1) emit_gate(o, kb, b, P.pool + op.ref + 4 * b, "P.pool + " + std::to_string(op.ref + 4 * b),
-                                             (1u << G) - 1, G, (op.dtab >> (4 * b)) & 15u);
+                                             (1u << G) - 1, G, (op.dtab >> (4 * b)) & 15u, stp);
         } else if (kind == TOP_GATE) {
             // controls on register bits select registers (a literal mask); controls on the other
             // tile bits are one condition per group
@@ -457,9 +630,34 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
             unsigned en = 0;
             for (int q = 0; q < G; ++q)
                 if ((off[q] & cmr) == cvr) en |= 1u << q;
+            if (cmn && lazy) sign_flush(o, st);  // a per-group condition: the track cannot follow it
             if (cmn) o("      if ((lb & %uu) == %uu) {\n", cmn, cvn);
-            emit_gate(o, kb, op.t, op.c, "P.ops[" + std::to_string(oi) + "].c", en, G, op.dtab & 15u);
+            emit_gate(o, kb, op.t, op.c, "P.ops[" + std::to_string(oi) + "].c", en, G, op.dtab & 15u, cmn ? nullptr : stp);
             if (cmn) o("      }\n");
+        } else if (kind == TOP_DTAB && lazy && st.any()) {
+            // the round's diagonal table takes the pending signs as signed entries
+            for (int q = 0; q < G; ++q) {
+                const bool cs = st.ct >> q & 1u;
+                const std::string rp = rt_parity(st, q);
+                if (op.dskip >> q & 1) {  // entry exactly 1: only the sign, if any
+                    if (cs || !rp.empty())
+                        o("      v[%d] = flipd2(v[%d], %s);\n", q, q, (std::string(cs ? "1u" : "0u") + (rp.empty() ? "" : " ^ " + rp)).c_str());
+                    continue;
+                }
+                fp64(P.pool[op.ref + q].y == 0.0 ? 2 : 4);
+                if (P.pool[op.ref + q].y == 0.0) {
+                    std::string sx = std::string(cs ? "-" : "") + "P.pool[" + std::to_string(op.ref + q) + "].x";
+                    if (!rp.empty()) sx = "flipd(" + sx + ", " + rp + ")";
+                    o("      { const double s = %s; v[%d] = make_double2(v[%d].x * s, v[%d].y * s); }\n", sx.c_str(), q, q, q);
+                } else {
+                    std::string e = "P.pool[" + std::to_string(op.ref + q) + "]";
+                    if (cs) e = "make_double2(-" + e + ".x, -" + e + ".y)";
+                    if (!rp.empty()) e = "flipd2(" + e + ", " + rp + ")";
+                    o("      v[%d] = cmul_f(%s, v[%d]);\n", q, e.c_str(), q);
+                }
+            }
+            st.ct = 0;
+            sign_reset_rt(o, st);
         } else if (kind == TOP_DTAB) {
             for (int q = 0; q < G; ++q) {
                 if (op.dskip >> q & 1) continue;
@@ -530,7 +728,8 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
     if (accumulate)
         for (int q = 0; q < G; ++q) o("      v[%d] = cmul_f(gs, v[%d]);\n", q, q);
     if (accumulate) fp64(4 * G);
-    if (R.flags & RD_SIGNS) o("      flip_signs1(v, negacc);\n");
+    if (!lazy && (R.flags & RD_SIGNS)) o("      flip_signs1(v, negacc);\n");
+    if (lazy) sign_flush(o, st);
     if (direct) {  // straight to HBM: logical index store(lb ^ off[q]) of the tile
         o("      { const unsigned sd = sd_t ^ %s;\n", kexpr(sk).c_str());
         o("        const u64 gs = base | hi_tab[sd >> 3];\n");

@@ -189,11 +189,16 @@ __device__ __forceinline__ void gate1r(double2 (&v)[8], const double2* c, unsign
 
 // Pivoted form (specialised kernels, KF_PIVOT): row r = x[piv_r] + rho_r * x[other] on the
 // register pairs along bit T of the registers in EN; the row scales sit in the round's table.
-template <int T, bool P0, bool P1, bool Z0, bool Z1, bool REAL, unsigned EN>
-__device__ __forceinline__ void gate1p(double2 (&v)[8], double2 rho0, double2 rho1) {
+// NEG bit q: the pair (q, q | 1 << T) holds registers of opposite pending sign (lazy +-1 flips,
+// jit.cpp SignTrack): both rows use -rho (a free operand negation in the DFMAs).
+template <int T, bool P0, bool P1, bool Z0, bool Z1, bool REAL, unsigned EN, unsigned NEG = 0u>
+__device__ __forceinline__ void gate1p(double2 (&v)[8], double2 rho0_, double2 rho1_) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         if ((q & (1 << T)) || !((EN >> q) & 1u)) continue;
+        const bool ng = (NEG >> q) & 1u;
+        const double2 rho0 = ng ? make_double2(-rho0_.x, -rho0_.y) : rho0_;
+        const double2 rho1 = ng ? make_double2(-rho1_.x, -rho1_.y) : rho1_;
         const double2 x0 = v[q], x1 = v[q | (1 << T)];
         const double2 p0 = P0 ? x1 : x0, o0 = P0 ? x0 : x1, p1 = P1 ? x1 : x0, o1 = P1 ? x0 : x1;
         double2 n0 = p0, n1 = p1;
@@ -204,6 +209,21 @@ __device__ __forceinline__ void gate1p(double2 (&v)[8], double2 rho0, double2 rh
         v[q] = n0;
         v[q | (1 << T)] = n1;
     }
+}
+
+// x with its sign flipped when bit 0 of s is set (sign-bit xor: exact, no FP64 instruction)
+__device__ __forceinline__ double2 flipd2(double2 x, unsigned s) {
+    const long long m = (long long)(s & 1u) << 63;
+    return make_double2(__longlong_as_double(__double_as_longlong(x.x) ^ m),
+                        __longlong_as_double(__double_as_longlong(x.y) ^ m));
+}
+__device__ __forceinline__ double flipd(double x, unsigned s) {
+    return __longlong_as_double(__double_as_longlong(x) ^ ((long long)(s & 1u) << 63));
+}
+// negate the registers in mask (bit q: register q)
+__device__ __forceinline__ void flip_mask(double2 (&v)[8], unsigned mask) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = flipd2(v[q], mask >> q);
 }
 
 // Apply and clear the pending +-1 flips (bit q of negacc: negate register q) by xor of the sign
