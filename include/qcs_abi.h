@@ -179,6 +179,11 @@ int qcs_state_distance(qcs_state* a, qcs_state* b, double* max_abs, double* l2);
  * probabilities, core.cpp:30-34) and the k <= 16 largest probabilities as qcs_topk gives them
  * (indices[0] is the argmax).  Host outputs; synchronous. */
 int qcs_summary(qcs_state* s, int k, double* norm, uint64_t* indices, double* probabilities);
+/* qcs_summary in two halves: _begin enqueues the pass and its read-back on the state's stream
+ * and returns at once; _end waits for it and returns the same values.  Lets a serving loop
+ * queue request i+1 while request i's summary is still on the device.  One pending per state. */
+int qcs_summary_begin(qcs_state* s, int k);
+int qcs_summary_end(qcs_state* s, double* norm, uint64_t* indices, double* probabilities);
 /* render_report's seeded sampling (circuit_io.cpp:114-128), index-exact: std::mt19937_64(seed),
  * `count` draws of uniform_real_distribution<double>(0, acc), each the std::lower_bound of the
  * draw in the SEQUENTIAL rounded prefix sum of the probabilities (acc += p_i).  The device

@@ -88,6 +88,8 @@ SIGNATURES = {
     "qcs_gather": (C.c_int, [_P, _U64, C.c_uint64, _D]),
     "qcs_state_distance": (C.c_int, [_P, _P, _D, _D]),
     "qcs_summary": (C.c_int, [_P, C.c_int, _D, _U64, _D]),
+    "qcs_summary_begin": (C.c_int, [_P, C.c_int]),
+    "qcs_summary_end": (C.c_int, [_P, _D, _U64, _D]),
     "qcs_sample": (C.c_int, [_P, C.c_uint64, C.c_uint64, _U64, _D]),
     "qcs_rh_mvm": (C.c_int, [_P, C.c_int, C.c_double, C.c_int, C.c_uint64, _U64, _U64]),
     "qcs_simulate": (C.c_int, [_P, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),

@@ -395,6 +395,35 @@ int qcs_sample(qcs_state* s, uint64_t seed, uint64_t count, uint64_t* out, doubl
     });
 }
 
+int qcs_summary_begin(qcs_state* s, int k) {
+    return guarded([&] {
+        need(s, "state");
+        if (k < 1 || k > 16) qcs::raise(QCS_ERR_ARG, "top-k supports 1 <= k <= 16");
+        if (s->summary_k) qcs::raise(QCS_ERR_ARG, "a summary of this state is already pending");
+        qcs::DeviceGuard g(s->device);
+        if (!s->summary_host) QCS_CUDA(cudaHostAlloc(&s->summary_host, qcs::topk_host_bytes(16), cudaHostAllocDefault));
+        if (!s->summary_done) QCS_CUDA(cudaEventCreateWithFlags(&s->summary_done, cudaEventDisableTiming));
+        qcs::topk_begin(s->amps, uint64_t(1) << s->n, k, true, s->summary_host, s->stream);
+        QCS_CUDA(cudaEventRecord(s->summary_done, s->stream));
+        s->summary_k = k;
+    });
+}
+
+int qcs_summary_end(qcs_state* s, double* norm, uint64_t* indices, double* probabilities) {
+    return guarded([&] {
+        need(s, "state");
+        need(norm, "norm");
+        need(indices, "indices");
+        need(probabilities, "probabilities");
+        if (!s->summary_k) qcs::raise(QCS_ERR_ARG, "no summary of this state is pending");
+        qcs::DeviceGuard g(s->device);
+        const int k = s->summary_k;
+        s->summary_k = 0;
+        QCS_CUDA(cudaEventSynchronize(s->summary_done));
+        qcs::topk_finish(s->summary_host, k, true, indices, probabilities, norm);
+    });
+}
+
 int qcs_gather(qcs_state* s, const uint64_t* indices, uint64_t count, double* out) {
     return guarded([&] {
         need(s, "state");

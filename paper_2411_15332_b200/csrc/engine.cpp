@@ -119,6 +119,8 @@ qcs_state::~qcs_state() {
         if (st.done) cudaEventDestroy(st.done);
     }
     if (scratch) cudaFree(scratch);
+    if (summary_host) cudaFreeHost(summary_host);
+    if (summary_done) cudaEventDestroy(summary_done);
     for (auto& e : events)
         if (e) cudaEventDestroy(e);
     if (owns_mem && amps) cudaFree(amps);

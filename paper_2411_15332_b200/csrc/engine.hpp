@@ -32,6 +32,10 @@ struct qcs_state {
     qcs::PlanCache* plan_cache = nullptr;   // recently simulated circuits: their lowered plans (engine.cpp)
     std::uint64_t plan_loaded = 0;          // id of the cached plan whose tables plan_buf holds (0: none)
     cudaEvent_t events[8] = {};
+    // qcs_summary_begin / _end: the pinned read-back of the summary's block candidates
+    void* summary_host = nullptr;
+    int summary_k = 0;              // k of the pending summary (0: none)
+    cudaEvent_t summary_done = nullptr;
     qcs::LaunchTimer* timer = nullptr;   // per-launch timing (qcs_timing_enable)
     ~qcs_state();
 };

@@ -252,6 +252,9 @@ void argmax(const double2* amps, std::uint64_t dim, std::uint64_t* idx, double* 
             cudaStream_t st);
 // k <= 16 largest probabilities, descending, ties to the lower index; norm (optional): the
 // state's norm from the same pass (sqrt of the summed probabilities)
+std::size_t topk_host_bytes(int k);
+void topk_begin(const double2* amps, std::uint64_t dim, int k, bool with_norm, void* host, cudaStream_t st);
+void topk_finish(const void* host, int k, bool with_norm, std::uint64_t* idx, double* p, double* norm);
 void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st,
           double* norm = nullptr);
 // seeded sampling with the reference's sequential CDF (sample_kernels.cu)

@@ -366,35 +366,50 @@ void fill_random(double2* amps, std::uint64_t dim, std::uint64_t seed, cudaStrea
     check_launch("k_fill_random");
 }
 
-void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st,
-          double* norm) {
+// The one-pass summary in two halves, so a caller can keep the device busy meanwhile:
+// topk_begin enqueues the reduction and the read-back of the block candidates (and block sums)
+// into `host` (pinned, topk_host_bytes(k) bytes) on stream st; topk_finish merges them once the
+// stream has reached that point.
+std::size_t topk_host_bytes(int k) { return sizeof(ArgMax) * std::size_t(kSMs * 2) * std::size_t(k) + sizeof(double) * kSMs * 2; }
+
+void topk_begin(const double2* amps, std::uint64_t dim, int k, bool with_norm, void* host, cudaStream_t st) {
     if (k < 1 || k > kTopK) raise(QCS_ERR_ARG, "top-k supports 1 <= k <= 16");
     const int blocks = kSMs * 2;
     ArgMax* part = nullptr;
     const std::size_t pbytes = sizeof(ArgMax) * blocks * k;
     QCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), pbytes + sizeof(double) * blocks, st));
-    double* psum = norm ? reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(part) + pbytes) : nullptr;
+    double* psum = with_norm ? reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(part) + pbytes) : nullptr;
     k_topk_partial<<<blocks, 256, 0, st>>>(amps, dim, k, part, psum);
     check_launch("k_topk_partial");
-    std::vector<ArgMax> h(std::size_t(blocks) * k);
-    std::vector<double> hs(norm ? blocks : 0);
-    QCS_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(ArgMax) * h.size(), cudaMemcpyDeviceToHost, st));
-    if (norm) QCS_CUDA(cudaMemcpyAsync(hs.data(), psum, sizeof(double) * blocks, cudaMemcpyDeviceToHost, st));
+    QCS_CUDA(cudaMemcpyAsync(host, part, pbytes + (with_norm ? sizeof(double) * blocks : 0), cudaMemcpyDeviceToHost, st));
     QCS_CUDA(cudaFreeAsync(part, st));
-    QCS_CUDA(cudaStreamSynchronize(st));
-    if (norm) {
+}
+
+void topk_finish(const void* host, int k, bool with_norm, std::uint64_t* idx, double* p, double* norm) {
+    const int blocks = kSMs * 2;
+    const auto* h = static_cast<const ArgMax*>(host);
+    if (with_norm && norm) {
+        const auto* hs = reinterpret_cast<const double*>(static_cast<const unsigned char*>(host) + sizeof(ArgMax) * blocks * k);
         double acc = 0.0;
-        for (double v : hs) acc += v;  // fixed block order: deterministic for a given n
+        for (int i = 0; i < blocks; ++i) acc += hs[i];  // fixed block order: deterministic for a given n
         *norm = std::sqrt(acc);
     }
     std::vector<ArgMax> c;
-    for (const ArgMax& x : h)
-        if (x.i != ~u64(0)) c.push_back(x);
+    for (int i = 0; i < blocks * k; ++i)
+        if (h[i].i != ~u64(0)) c.push_back(h[i]);
     std::sort(c.begin(), c.end(), [](const ArgMax& x, const ArgMax& y) { return x.p != y.p ? x.p > y.p : x.i < y.i; });
     for (int j = 0; j < k; ++j) {
         idx[j] = j < int(c.size()) ? c[j].i : ~u64(0);
         p[j] = j < int(c.size()) ? c[j].p : 0.0;
     }
+}
+
+void topk(const double2* amps, std::uint64_t dim, int k, std::uint64_t* idx, double* p, cudaStream_t st,
+          double* norm) {
+    std::vector<unsigned char> host(topk_host_bytes(k));
+    topk_begin(amps, dim, k, norm != nullptr, host.data(), st);
+    QCS_CUDA(cudaStreamSynchronize(st));
+    topk_finish(host.data(), k, norm != nullptr, idx, p, norm);
 }
 
 std::size_t reduce_scratch_bytes() { return sizeof(ArgMax) * (kRedBlocks + 1) + 64; }

@@ -422,6 +422,20 @@ class DeviceState:
         _check(L.lib().qcs_summary(self._h, k, C.byref(nrm), idx, pr))
         return nrm.value, list(idx), list(pr)
 
+    def summary_begin(self, k: int = 16) -> None:
+        """The summary pass and its read-back, queued on the state's stream (qcs_summary_begin)."""
+        _check(L.lib().qcs_summary_begin(self._h, k))
+        self._summary_k = k
+
+    def summary_end(self):
+        """Wait for summary_begin's result: (norm, [top-k indices], [probabilities])."""
+        k = getattr(self, "_summary_k", 16)
+        nrm = C.c_double()
+        idx = (C.c_uint64 * k)()
+        pr = (C.c_double * k)()
+        _check(L.lib().qcs_summary_end(self._h, C.byref(nrm), idx, pr))
+        return nrm.value, list(idx), list(pr)
+
     def sample(self, count: int, seed: int):
         """render_report's seeded samples (circuit_io.cpp:114-128), drawn on the device: returns
         ([indices], acc) with acc the sequential sum of the probabilities.  Index-exact against

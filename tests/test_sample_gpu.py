@@ -134,3 +134,21 @@ def test_large_state_samples_consistent_with_probabilities():
     assert abs(acc - 1.0) < 1e-9
     amps = rep.final.gather(sorted(set(got)))
     assert np.all(np.abs(amps) > 0)
+
+
+def test_summary_begin_end_equals_summary():
+    """qcs_summary_begin/_end (the split form a serving loop uses) returns what qcs_summary does,
+    and refuses a second pending summary or an end without a begin."""
+    from paper_2411_15332_b200 import qcsim as Q
+    x = _random_state(14, 9)
+    s = Q.DeviceState.from_numpy(x)
+    want = s.summary(16)
+    s.summary_begin(16)
+    with pytest.raises(ValueError):  # QCS_ERR_ARG
+        s.summary_begin(16)
+    assert s.summary_end() == want
+    with pytest.raises(ValueError):
+        s.summary_end()
+    s.summary_begin(5)
+    got = s.summary_end()
+    assert got[1] == want[1][:5] and got[2] == want[2][:5] and got[0] == want[0]
