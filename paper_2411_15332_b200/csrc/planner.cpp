@@ -281,6 +281,7 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
     struct Grown {
         u64 S = 0;
         std::vector<int> chosen, skipped;
+        std::size_t stop = ~std::size_t(0);  // remaining[stop..] were not scanned (all skipped)
         int gates = 0;
         bool signs = false;
     };
@@ -295,7 +296,13 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
         // and collapses (missed_tile_program), e.g. Grover's H..H Z0 H..H
         bool signed_pass = false;
         u64 pre_sign = 0;
-        for (int idx : remaining) {
+        const u64 full = n >= 64 ? ~u64(0) : (u64(1) << n) - 1;
+        for (std::size_t pos = 0; pos < remaining.size(); ++pos) {
+            const int idx = remaining[pos];
+            if ((nd_block & full) == full) {  // every bit waits on a skipped gate: nothing else can join
+                g.stop = pos;  // the rest stays skipped (appended for the winner only)
+                break;
+            }
             const FOp& f = ops[std::size_t(idx)];
             const bool conflict = (f.touch & nd_block) || (!f.diagonal && (f.touch & d_block));
             bool take = false;
@@ -401,6 +408,8 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
             }
         }
         plan.passes.push_back(PlannedPass{best.S, best.chosen});
+        if (best.stop < remaining.size())
+            best.skipped.insert(best.skipped.end(), remaining.begin() + std::ptrdiff_t(best.stop), remaining.end());
         remaining.swap(best.skipped);
     }
     return plan;
