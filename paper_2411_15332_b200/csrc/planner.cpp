@@ -640,6 +640,39 @@ void pivot_pass(PassParams& P, int& npool) {
     P.nops = int(ops.size());
 }
 
+// Table normalisation (round 2): every round's diagonal table but the pass's last is divided by
+// its entry 0 -- which becomes exactly 1 and is skipped (one complex multiply per 8 amplitudes
+// less) -- and the product of those entries, a scalar that commutes with everything, joins the
+// pass's last table.  Passes with sign-step programs or tile lists keep their tables.
+void normalize_tables(PassParams& P) {
+    static const bool off = knob("QCS_NO_TABLE_NORM");  // A/B switch
+    if (off || P.alt_mode != ALT_NONE || P.list_cnt) return;
+    std::vector<int> tabs;
+    for (int i = 0; i < P.nops; ++i)
+        if ((P.ops[i].kind & KF_KIND) == TOP_DTAB) tabs.push_back(i);
+    if (tabs.size() < 2) return;
+    cplx carry(1.0, 0.0);
+    auto entry = [&](const RegOp& t, int q) { return cplx(P.pool[t.ref + q].x, P.pool[t.ref + q].y); };
+    auto store = [&](RegOp& t, int q, cplx v) {
+        P.pool[t.ref + q] = make_double2(v.real(), v.imag());
+        const std::uint8_t bit = std::uint8_t(1u << q);
+        t.dskip = std::uint8_t(v == cplx(1.0, 0.0) ? (t.dskip | bit) : (t.dskip & ~bit));
+    };
+    for (std::size_t k = 0; k + 1 < tabs.size(); ++k) {
+        RegOp& t = P.ops[tabs[k]];
+        const cplx f = entry(t, 0);
+        if (f == cplx(1.0, 0.0) || std::abs(f) == 0.0 || !std::isfinite(f.real()) || !std::isfinite(f.imag())) continue;
+        const cplx nc = carry * f;
+        if (!std::isfinite(nc.real()) || std::abs(nc) == 0.0) continue;
+        for (int q = 1; q < 8; ++q) store(t, q, entry(t, q) / f);
+        store(t, 0, cplx(1.0, 0.0));
+        carry = nc;
+    }
+    if (carry == cplx(1.0, 0.0)) return;
+    RegOp& last = P.ops[tabs.back()];
+    for (int q = 0; q < 8; ++q) store(last, q, entry(last, q) * carry);
+}
+
 }  // namespace
 
 namespace {
@@ -1491,7 +1524,10 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             out.tables.insert(out.tables.end(), forced[pi].begin(), forced[pi].end());
         }
         P.nops = nops;
-        if (jit_pivot(n, P)) pivot_pass(P, npool);
+        if (jit_pivot(n, P)) {
+            pivot_pass(P, npool);
+            normalize_tables(P);
+        }
         out.passes.push_back(P);
         out.pass_ops.push_back(lists[pi]);
         out.single_flip_off.push_back(flip_off);
