@@ -60,7 +60,8 @@ struct Out {
 // amplitudes, accumulated while a pass's source is generated (pass_fp64_per_tile): the
 // roofline's compute side for the FP64-bound passes (bench.py)
 thread_local double g_fp64 = 0.0;
-void fp64(double k) { g_fp64 += k; }
+thread_local double g_fp64_groups = 1.0;  // groups per tile of the round being generated
+void fp64(double k) { g_fp64 += k * g_fp64_groups; }
 
 // Addressing proof (QCS_JIT_VERIFY=1 or qcs_plan_compile's verify mode): while a round is
 // generated, its address arithmetic is also evaluated for every thread, group iteration and
@@ -403,18 +404,19 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
     if (te < oe && !last) raise(QCS_ERR_SIM, "internal: trailing relabelling outside a pass's last round");
     const bool relabel = !map.identity(P.m);
     const bool direct = last && (relabel || te < oe);
-    constexpr int W = 3, G = 1 << W;
+    const int W = round_width(R), G = 1 << W;  // 3 or 4 register bits (RD_W4)
     const unsigned long long gmask = (1ull << G) - 1;
     const unsigned ngroups = (1u << P.m) >> W;
+    g_fp64_groups = double(ngroups);
     unsigned off[16] = {};
     unsigned regmask = 0;
-    for (int i = 0; i < W; ++i) regmask |= 1u << R.r[i];
+    for (int i = 0; i < W; ++i) regmask |= 1u << round_reg(R, i);
     for (int q = 0; q < G; ++q)
         for (int i = 0; i < W; ++i)
-            if (q >> i & 1) off[q] |= 1u << R.r[i];
+            if (q >> i & 1) off[q] |= 1u << round_reg(R, i);
     auto swz = [](unsigned j) { return j ^ ((j >> 3) & 7u); };
     o("  {  // round %d: register bits", ri);
-    for (int i = 0; i < W; ++i) o(" %d", R.r[i]);
+    for (int i = 0; i < W; ++i) o(" %d", round_reg(R, i));
     o("\n");
     // Thread order: the 8 threads of one 16-byte shared-memory phase differ in gb's low 3 bits,
     // i.e. in the round's lowest 3 non-register tile bits.  Their bank group is bits 0..2 XOR
@@ -445,7 +447,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
     // its relabelled position are linear in gb, and gb = t + k * threads: the thread's part is
     // computed once per round, each iteration adds a constant.
     auto deposit = [&](unsigned g) {
-        for (int i = 0; i < W; ++i) g = ((g >> R.r[i]) << (R.r[i] + 1)) | (g & ((1u << R.r[i]) - 1));
+        for (int i = 0; i < W; ++i) g = ((g >> round_reg(R, i)) << (round_reg(R, i) + 1)) | (g & ((1u << round_reg(R, i)) - 1));
         if (swap_a >= 0 && ((g >> swap_a) ^ (g >> swap_b)) & 1u) g ^= (1u << swap_a) | (1u << swap_b);
         return g;
     };
@@ -470,7 +472,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
         const unsigned tsz = 1u << P.m;
         auto swz1 = [](unsigned j) { return j ^ ((j >> 3) & 7u); };
         auto sw = [&](unsigned g) {  // lb_t of thread t: zeros at the register bits, then the swap
-            for (int i = 0; i < W; ++i) g = ((g >> R.r[i]) << (R.r[i] + 1)) | (g & ((1u << R.r[i]) - 1));
+            for (int i = 0; i < W; ++i) g = ((g >> round_reg(R, i)) << (round_reg(R, i) + 1)) | (g & ((1u << round_reg(R, i)) - 1));
             if (swap_a >= 0 && ((g >> swap_a) ^ (g >> swap_b)) & 1u) g ^= (1u << swap_a) | (1u << swap_b);
             return g;
         };
@@ -529,7 +531,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
         }
     }
     std::string lbx = "t";
-    for (int i = 0; i < W; ++i) lbx = "insert_zero(" + lbx + ", " + std::to_string(R.r[i]) + ")";
+    for (int i = 0; i < W; ++i) lbx = "insert_zero(" + lbx + ", " + std::to_string(round_reg(R, i)) + ")";
     o("    unsigned lb_t = %s;\n", lbx.c_str());
     if (swap_a >= 0)
         o("    { const unsigned d = ((lb_t >> %d) ^ (lb_t >> %d)) & 1u; lb_t ^= (d << %d) | (d << %d); }\n", swap_a,
@@ -563,7 +565,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
     const bool accumulate = nconst >= 2 && has_pivot(P);
     if (accumulate) o("      double2 gs = make_double2(1.0, 0.0);\n");
     o("      (void)g0; (void)negacc;\n");
-    const bool lazy = knob_lazy_signs();
+    const bool lazy = knob_lazy_signs() && W == 3;  // the track is written for 8 registers
     SignTrack st;
     SignTrack* stp = lazy ? &st : nullptr;
     if (lazy) o("      unsigned rs0 = 0u, rs1 = 0u, rs2 = 0u, rsc = 0u;\n      (void)rs0; (void)rs1; (void)rs2; (void)rsc;\n");
@@ -606,7 +608,21 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
             o("        negacc ^= acc; }\n");
         } else if (kind == TOP_DIAG && (kb & KF_SIGNED)) {
             const bool c0 = op.dreg[0] == 0xff, c1 = op.dk == 2 && op.dreg[1] == 0xff;
-            o("      negacc ^= unsigned(0x%llxull >> (%d * (%s))) & 0x%llxu;\n", (unsigned long long)op.smask, G,
+            unsigned long long sm = op.smask;  // byte cg: the registers that flip when the constant bits spell cg
+            if (W == 4) {  // 16 registers: the 16-bit masks from the phase bits (dskip = the -1 entries)
+                sm = 0;
+                for (int cg = 0; cg < 4; ++cg)
+                    for (int q = 0; q < G; ++q) {
+                        int g = 0;
+                        for (int i = 0; i < op.dk; ++i) {
+                            const int bit = op.dreg[i] < W ? (q >> op.dreg[i]) & 1
+                                                           : (i == 0 && op.dk == 2 ? (cg >> 1) & 1 : cg & 1);
+                            g |= bit << (op.dk - 1 - i);
+                        }
+                        if (op.dskip >> g & 1) sm |= 1ull << (16 * cg + q);
+                    }
+            }
+            o("      negacc ^= unsigned(0x%llxull >> (%d * (%s))) & 0x%llxu;\n", sm, G,
               const_bits(c0, c1, op.dk, op.dpos[0], op.dpos[1]).c_str(), gmask);
         } else if (kind == TOP_WHT) {
             for (int b = 0; b < W; ++b)
@@ -659,8 +675,9 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
             st.ct = 0;
             sign_reset_rt(o, st);
         } else if (kind == TOP_DTAB) {
+            const unsigned skipm = W == 4 ? unsigned(op.smask) : unsigned(op.dskip);
             for (int q = 0; q < G; ++q) {
-                if (op.dskip >> q & 1) continue;
+                if (skipm >> q & 1) continue;
                 fp64(P.pool[op.ref + q].y == 0.0 ? 2 : 4);
                 if (P.pool[op.ref + q].y == 0.0)  // real entry (e.g. only gate row scales): 2 FP64
                     o("      { const double s = P.pool[%d].x; v[%d] = make_double2(v[%d].x * s, v[%d].y * s); }\n", op.ref + q,
@@ -704,6 +721,24 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
                 o("      { const int cb = int((g0 >> %d) & 1);\n", op.dpos[ci]);
                 o("        const double2 e0 = %s, e1 = %s;\n", entry(0, "cb").c_str(), entry(1, "cb").c_str());
                 for (int q = 0; q < G; ++q) o("        v[%d] = cmul_f(e%d, v[%d]);\n", q, (q >> rb) & 1, q);
+                o("      }\n");
+            } else if (W == 4) {  // 16 registers: the entry index per register, constant bits at run time
+                std::string cgx = "0";
+                for (int i = 0; i < op.dk; ++i)
+                    if (op.dreg[i] >= W)
+                        cgx += " | (int((g0 >> " + std::to_string(op.dpos[i]) + ") & 1) << " + std::to_string(op.dk - 1 - i) + ")";
+                o("      { const int cg = %s; (void)cg;\n", cgx.c_str());
+                for (int q = 0; q < G; ++q) {
+                    int rp = 0;
+                    for (int i = 0; i < op.dk; ++i)
+                        if (op.dreg[i] < W) rp |= ((q >> op.dreg[i]) & 1) << (op.dk - 1 - i);
+                    if (op.dk <= 2)
+                        o("        { const int g = cg | %d; if (!((%uu >> g) & 1u)) v[%d] = cmul_f(P.ops[%d].c[g], v[%d]); }\n", rp,
+                          unsigned(op.dskip), q, oi, q);
+                    else
+                        o("        { const int g = cg | %d; if (!((%uu >> g) & 1u)) v[%d] = cmul_f(big[%d].val[0][g], v[%d]); }\n",
+                          rp, unsigned(op.dskip), q, op.ref, q);
+                }
                 o("      }\n");
             } else {
                 o("      diag_op(v, P.ops[%d], big, g0);\n", oi);
@@ -776,7 +811,11 @@ void emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threa
 std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
     Out o;
     static const int minb_env = [] { const char* v = std::getenv("QCS_JIT_MINB"); return v ? std::atoi(v) : 0; }();
-    const int minb = minb_env > 0 ? minb_env : (F & 8u) ? 2 : 3;  // resident tiles per SM
+    static const int w4_minb = [] { const char* v = std::getenv("QCS_W4_MINB"); return v ? std::atoi(v) : 2; }();
+    bool w4 = false;
+    for (int r = 0; r < P.nrounds; ++r) w4 |= (P.rounds[r].flags & RD_W4) != 0;
+    // resident tiles per SM: 3 (80 registers) for 8-register rounds; 16-register rounds need ~100
+    const int minb = minb_env > 0 ? minb_env : w4 ? w4_minb : (F & 8u) ? 2 : 3;
     o("#include \"tile_device.cuh\"\n");
     o("using namespace qcs;\nusing namespace qcs::tile;\n");
     o("extern \"C\" __global__ void __launch_bounds__(%u, %d)\n", threads, minb);
@@ -808,9 +847,9 @@ double fp64_per_tile(const PassParams& P) {
     if (Q.alt_mode == ALT_ROUNDS) Q.alt_mode = ALT_NONE;  // the main program only
     g_fp64 = 0.0;
     (void)pass_source(Q, 0xffu, 256);
-    const double per_group = g_fp64;
+    const double per_tile = g_fp64;  // each round's per-group counts times its groups per tile
     g_fp64 = 0.0;
-    return per_group * double((1u << P.m) >> 3);
+    return per_tile;
 }
 
 void nvrtc_check(nvrtcResult r, const char* what) {
@@ -981,7 +1020,14 @@ JitKernel& compile(const std::string& src) {
 
 
 // worth a compile (~0.5 s, once per structure): enough tiles x rounds of work
+bool has_w4(const PassParams& p) {
+    for (int r = 0; r < p.nrounds; ++r)
+        if (p.rounds[r].flags & RD_W4) return true;
+    return false;
+}
+
 bool wanted(const PassParams& p, double tiles) {
+    if (has_w4(p)) return true;  // 16-register rounds exist only in the specialised form
     const int mode = jit_mode();
     if (mode == 0) return false;
     return mode >= 2 || has_pivot(p) || (tiles * double(p.nrounds) >= 32768.0 && p.nrounds >= 2);

@@ -152,11 +152,16 @@ struct RegOp {
 
 constexpr int RD_SMEM = 1;    // gates on 2-3 targets, run straight on shared memory
 constexpr int RD_SIGNS = 2;   // register round ending with pending +-1 sign flips
+constexpr int RD_W4 = 4;      // specialised kernels only: 4 register bits (16 amplitudes per group),
+                              // the fourth local bit in flags bits 4..7
 struct RoundDesc {
-    std::uint8_t flags;       // RD_*
+    std::uint8_t flags;       // RD_* (bits 4..7: the fourth register bit of an RD_W4 round)
     std::uint8_t r[3];        // local tile bits held in registers (ascending)
     std::uint16_t op_begin, op_count;
 };
+// register bits of a round and their local tile bits (r[3] lives in the flags byte)
+inline constexpr int round_width(const RoundDesc& R) { return (R.flags & RD_W4) ? 4 : 3; }
+inline constexpr int round_reg(const RoundDesc& R, int i) { return i < 3 ? int(R.r[i]) : int(R.flags >> 4); }
 
 #ifndef QCS_PASS_MAX_OPS
 #define QCS_PASS_MAX_OPS 200

@@ -22,6 +22,12 @@ bool knob(const char* name) {
     return v && *v && *v != '0';
 }
 const bool kNoTables = knob("QCS_NO_DTAB");
+// 16-amplitude register rounds (4 register bits) in the specialised kernels: a third fewer rounds
+// for C4 (59 -> 39), measured 265.8 -> 260.5 ms (tools/gpu_r02w.sh); QCS_JIT_W4=0 turns them off
+bool knob_w4() {
+    static const bool on = [] { const char* v = std::getenv("QCS_JIT_W4"); return !v || std::atoi(v) != 0; }();
+    return on;
+}
 const bool kNoReal = knob("QCS_NO_REAL");
 inline bool is_zero(const cplx& v) { return v.real() == 0.0 && v.imag() == 0.0; }
 inline bool is_one(const cplx& v) { return v.real() == 1.0 && v.imag() == 0.0; }
@@ -495,16 +501,17 @@ void pivot_pass(PassParams& P, int& npool) {
             trailing.insert(trailing.begin(), rops.back());
             rops.pop_back();
         }
+        const int W = round_width(R), G = 1 << W;
         unsigned regmask = 0;
-        for (int i = 0; i < 3; ++i) regmask |= 1u << R.r[i];
+        for (int i = 0; i < W; ++i) regmask |= 1u << round_reg(R, i);
         // the round's table: the existing one (the last operation) or a new one
         int tab = -1;
         if (!rops.empty() && (rops.back().kind & KF_KIND) == TOP_DTAB) tab = int(rops.size()) - 1;
-        cplx table[8];
-        for (int q = 0; q < 8; ++q)
+        cplx table[16];
+        for (int q = 0; q < G; ++q)
             table[q] = tab >= 0 ? cplx(P.pool[rops[std::size_t(tab)].ref + q].x, P.pool[rops[std::size_t(tab)].ref + q].y)
                                 : cplx(1.0, 0.0);
-        const bool room = tab >= 0 || (npool + 8 <= kPassPool && int(ops.size() + rops.size()) + 1 < kPassMaxOps);
+        const bool room = tab >= 0 || (npool + G <= kPassPool && int(ops.size() + rops.size()) + 1 < kPassMaxOps);
         bool changed = false;
         for (std::size_t i = 0; i < rops.size() && room; ++i) {
             RegOp& o = rops[i];
@@ -518,11 +525,11 @@ void pivot_pass(PassParams& P, int& npool) {
             // (diagonals, controls) -> the scale folds into that gate's columns (scale chaining:
             // two layers of one qubit in one round, the round scheduler's light cones); else no pivot
             unsigned support = 0;
-            for (int k = 0; k < 3; ++k)
-                if (o.lctrl_mask >> R.r[k] & 1) support |= 1u << k;
+            for (int k = 0; k < W; ++k)
+                if (o.lctrl_mask >> round_reg(R, k) & 1) support |= 1u << k;
             bool later = false;
-            int chain[3] = {-1, -1, -1};
-            for (int b = 0; b < 3 && !later; ++b) {
+            int chain[4] = {-1, -1, -1, -1};
+            for (int b = 0; b < W && !later; ++b) {
                 if (!(bits >> b & 1)) continue;
                 for (std::size_t j = i + 1; j < rops.size(); ++j) {
                     const RegOp& g = rops[j];
@@ -546,16 +553,16 @@ void pivot_pass(PassParams& P, int& npool) {
             if (later) continue;
             // registers the gate acts on (register-bit controls)
             unsigned en = 0;
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < G; ++q) {
                 unsigned lq = 0;
-                for (int k = 0; k < 3; ++k)
-                    if (q >> k & 1) lq |= 1u << R.r[k];
+                for (int k = 0; k < W; ++k)
+                    if (q >> k & 1) lq |= 1u << round_reg(R, k);
                 if ((lq & o.lctrl_mask) == o.lctrl_val) en |= 1u << q;
             }
             // every target bit must pivot (a zero row cannot)
-            double2* cs[3] = {nullptr, nullptr, nullptr};
+            double2* cs[4] = {nullptr, nullptr, nullptr, nullptr};
             bool ok = true;
-            for (int b = 0; b < 3; ++b)
+            for (int b = 0; b < W; ++b)
                 if (bits >> b & 1) {
                     cs[b] = bundle ? P.pool + o.ref + 4 * b : o.c;
                     for (int r = 0; r < 2; ++r) ok &= std::abs(cplx(cs[b][2 * r].x, cs[b][2 * r].y)) +
@@ -563,7 +570,7 @@ void pivot_pass(PassParams& P, int& npool) {
                 }
             if (!ok) continue;
             unsigned piv = 0;
-            for (int b = 0; b < 3; ++b) {
+            for (int b = 0; b < W; ++b) {
                 if (!(bits >> b & 1)) continue;
                 double2* c = cs[b];
                 const int fb = bundle ? b : 0;
@@ -596,7 +603,7 @@ void pivot_pass(PassParams& P, int& npool) {
                     }
                     bool real = true;  // the later gate's kind: real only if all its coefficients are
                     const unsigned gb = (g.kind & KF_BUNDLE) ? g.t : 1u;
-                    for (int bb = 0; bb < 3; ++bb) {
+                    for (int bb = 0; bb < W; ++bb) {
                         if (!(gb >> bb & 1)) continue;
                         const double2* x = (g.kind & KF_BUNDLE) ? P.pool + g.ref + 4 * bb : g.c;
                         for (int e = 0; e < 4; ++e) real &= x[e].y == 0.0;
@@ -604,11 +611,11 @@ void pivot_pass(PassParams& P, int& npool) {
                     g.kind = std::uint8_t(real ? (g.kind | KF_REAL) : (g.kind & ~KF_REAL));
                     continue;
                 }
-                for (int q = 0; q < 8; ++q)
+                for (int q = 0; q < G; ++q)
                     if (en >> q & 1) table[q] *= scale[q >> rb & 1];
             }
             bool real = true;
-            for (int b = 0; b < 3; ++b)
+            for (int b = 0; b < W; ++b)
                 if (bits >> b & 1) real &= cs[b][0].y == 0.0 && cs[b][1].y == 0.0;
             o.kind = std::uint8_t((o.kind & ~KF_REAL) | KF_PIVOT | (real ? KF_REAL : 0));
             o.dtab = std::uint16_t(piv);
@@ -619,15 +626,19 @@ void pivot_pass(PassParams& P, int& npool) {
                 RegOp t{};
                 t.kind = TOP_DTAB;
                 t.ref = std::uint16_t(npool);
-                npool += 8;
+                npool += G;
                 rops.push_back(t);
                 tab = int(rops.size()) - 1;
             }
             RegOp& t = rops[std::size_t(tab)];
             t.dskip = 0;
-            for (int q = 0; q < 8; ++q) {
+            t.smask = 0;
+            for (int q = 0; q < G; ++q) {
                 P.pool[t.ref + q] = make_double2(table[q].real(), table[q].imag());
-                if (table[q] == cplx(1.0, 0.0)) t.dskip = std::uint8_t(t.dskip | (1u << q));
+                if (table[q] == cplx(1.0, 0.0)) {
+                    if (q < 8) t.dskip = std::uint8_t(t.dskip | (1u << q));
+                    t.smask |= 1u << q;
+                }
             }
         }
         ops.insert(ops.end(), rops.begin(), rops.end());
@@ -647,30 +658,36 @@ void pivot_pass(PassParams& P, int& npool) {
 void normalize_tables(PassParams& P) {
     static const bool off = knob("QCS_NO_TABLE_NORM");  // A/B switch
     if (off || P.alt_mode != ALT_NONE || P.list_cnt) return;
-    std::vector<int> tabs;
-    for (int i = 0; i < P.nops; ++i)
-        if ((P.ops[i].kind & KF_KIND) == TOP_DTAB) tabs.push_back(i);
+    std::vector<std::pair<int, int>> tabs;  // (op index, registers per group)
+    for (int r = 0; r < P.nrounds; ++r) {
+        const RoundDesc& R = P.rounds[r];
+        if (R.flags & RD_SMEM) continue;
+        for (int i = R.op_begin; i < R.op_begin + R.op_count; ++i)
+            if ((P.ops[i].kind & KF_KIND) == TOP_DTAB) tabs.push_back({i, 1 << round_width(R)});
+    }
     if (tabs.size() < 2) return;
     cplx carry(1.0, 0.0);
     auto entry = [&](const RegOp& t, int q) { return cplx(P.pool[t.ref + q].x, P.pool[t.ref + q].y); };
     auto store = [&](RegOp& t, int q, cplx v) {
         P.pool[t.ref + q] = make_double2(v.real(), v.imag());
-        const std::uint8_t bit = std::uint8_t(1u << q);
-        t.dskip = std::uint8_t(v == cplx(1.0, 0.0) ? (t.dskip | bit) : (t.dskip & ~bit));
+        const bool one = v == cplx(1.0, 0.0);
+        if (q < 8) t.dskip = std::uint8_t(one ? (t.dskip | (1u << q)) : (t.dskip & ~(1u << q)));
+        t.smask = one ? (t.smask | (1u << q)) : (t.smask & ~(1u << q));
     };
     for (std::size_t k = 0; k + 1 < tabs.size(); ++k) {
-        RegOp& t = P.ops[tabs[k]];
+        RegOp& t = P.ops[tabs[k].first];
+        const int G = tabs[k].second;
         const cplx f = entry(t, 0);
         if (f == cplx(1.0, 0.0) || std::abs(f) == 0.0 || !std::isfinite(f.real()) || !std::isfinite(f.imag())) continue;
         const cplx nc = carry * f;
         if (!std::isfinite(nc.real()) || std::abs(nc) == 0.0) continue;
-        for (int q = 1; q < 8; ++q) store(t, q, entry(t, q) / f);
+        for (int q = 1; q < G; ++q) store(t, q, entry(t, q) / f);
         store(t, 0, cplx(1.0, 0.0));
         carry = nc;
     }
     if (carry == cplx(1.0, 0.0)) return;
-    RegOp& last = P.ops[tabs.back()];
-    for (int q = 0; q < 8; ++q) store(last, q, entry(last, q) * carry);
+    RegOp& last = P.ops[tabs.back().first];
+    for (int q = 0; q < tabs.back().second; ++q) store(last, q, entry(last, q) * carry);
 }
 
 }  // namespace
@@ -744,7 +761,7 @@ bool signed_diag(const FOp& f) {
     return true;
 }
 
-int round_count(const std::vector<FOp>& ops, const std::vector<int>& list, const int* loc) {
+int round_count(const std::vector<FOp>& ops, const std::vector<int>& list, const int* loc, int width) {
     int rounds = 0;
     unsigned cur = 0;
     bool open = false;
@@ -752,7 +769,7 @@ int round_count(const std::vector<FOp>& ops, const std::vector<int>& list, const
         const FOp& f = ops[std::size_t(idx)];
         if (elementwise(f)) continue;
         const unsigned t = 1u << loc[f.tpos[0]];
-        if (open && (__builtin_popcount(cur | t) <= 3)) {
+        if (open && (__builtin_popcount(cur | t) <= width)) {
             cur |= t;
         } else {
             ++rounds;
@@ -764,7 +781,7 @@ int round_count(const std::vector<FOp>& ops, const std::vector<int>& list, const
 }
 
 bool schedule_rounds(int n, const int* loc, int m, const std::vector<FOp>& ops, const std::vector<int>& list,
-                     std::vector<FOp>& out_ops, std::vector<int>& out_list) {
+                     std::vector<FOp>& out_ops, std::vector<int>& out_list, int width = 3) {
     static const bool off = knob("QCS_NO_ROUND_SCHED");  // A/B switch
     const int N = int(list.size());
     if (off || N < 4 || m < 4) return false;
@@ -875,19 +892,25 @@ bool schedule_rounds(int n, const int* loc, int m, const std::vector<FOp>& ops, 
         long best = -1;
         unsigned bestT = 0;
         const int nb = int(bits.size());
-        for (int a = 0; a < nb; ++a)
-            for (int b = a + 1; b < std::max(nb, a + 2); ++b)
-                for (int c = b + 1; c < std::max(nb, b + 2); ++c) {
-                    unsigned T = 1u << bits[std::size_t(a)];
-                    if (b < nb) T |= 1u << bits[std::size_t(b)];
-                    if (c < nb) T |= 1u << bits[std::size_t(c)];
-                    long sc;
-                    closure(T, false, sc);
-                    if (sc > best) {
-                        best = sc;
-                        bestT = T;
-                    }
-                }
+        // every subset of min(width, nb) of the bits with pending gates
+        const int k = std::min(width, nb);
+        std::vector<int> pick(static_cast<std::size_t>(k));
+        for (int i = 0; i < k; ++i) pick[std::size_t(i)] = i;
+        for (;;) {
+            unsigned T = 0;
+            for (int i : pick) T |= 1u << bits[std::size_t(i)];
+            long sc;
+            closure(T, false, sc);
+            if (sc > best) {
+                best = sc;
+                bestT = T;
+            }
+            int i = k - 1;
+            while (i >= 0 && pick[std::size_t(i)] == nb - k + i) --i;
+            if (i < 0) break;
+            ++pick[std::size_t(i)];
+            for (int j = i + 1; j < k; ++j) pick[std::size_t(j)] = pick[std::size_t(j - 1)] + 1;
+        }
         long sc;
         if (closure(bestT, true, sc) == 0) return false;  // no progress: keep the circuit order
     }
@@ -929,7 +952,7 @@ bool schedule_rounds(int n, const int* loc, int m, const std::vector<FOp>& ops, 
         out_ops.push_back(local[std::size_t(i)]);
         out_list.push_back(int(out_ops.size()) - 1);
     }
-    return round_count(out_ops, out_list, loc) < round_count(ops, list, loc);
+    return round_count(out_ops, out_list, loc, width) < round_count(ops, list, loc, width);
 }
 
 }  // namespace
@@ -1071,6 +1094,19 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
         int nops = 0, nsign = 0, npool = 0;
         std::uint64_t flip_off = 0, flip_cnt = 0;
         const bool virt_pass = jit_virtual(n, P.m, has_alt[pi] && alts[pi].empty());
+        // 16-amplitude register rounds (4 register bits) for passes the specialised kernels run
+        // with pivots: gates and diagonals only (no sign steps, shared-memory gates, relabellings)
+        int RW = 3;
+        if (knob_w4() && !has_alt[pi] && forced[pi].empty() && P.m >= 8 && (jit_mode() == 1 || jit_mode() == 3)) {
+            bool ok = true;
+            for (int idx : lists[pi]) {
+                const FOp& f = ops[std::size_t(idx)];
+                if (f.kind == TOP_SIGN || (f.kind == TOP_GATE && f.K >= 2) || f.kind == TOP_PERM) ok = false;
+                if (f.kind == TOP_GATE && f.K == 1 && f.nrows == 2 && f.nnz[0] == 1 && f.nnz[1] == 1 && virt_pass) ok = false;
+            }
+            if (ok) RW = 4;
+        }
+        const int RG = 1 << RW;  // registers per group
         // rounds of <= 3 register bits; gates on 2-3 targets get shared-memory rounds
         struct RoundPlan {
             bool smem;
@@ -1156,7 +1192,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             auto& cur = rounds.back();
             if ((t & ~cur.mask) == 0) {
                 cur.ops.push_back(idx);
-            } else if (__builtin_popcount(cur.mask | t) <= 3) {
+            } else if (__builtin_popcount(cur.mask | t) <= RW) {
                 cur.mask |= t;
                 cur.ops.push_back(idx);
             } else {
@@ -1170,19 +1206,24 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
         for (auto& r : rounds) {
             if (P.nrounds >= kPassMaxOps) raise(QCS_ERR_SIM, "internal: too many rounds in a pass");
             unsigned mask = r.mask;
-            // pad to 3 register bits, preferring bits above 2: a round without bits 0..2 can
+            // pad to RW register bits, preferring bits above 2: a round without bits 0..2 can
             // move its amplitudes to and from HBM directly (whole 128-byte runs per warp)
-            for (int b = 3; b < P.m && __builtin_popcount(mask) < 3; ++b) mask |= 1u << b;
-            for (int b = 0; b < P.m && __builtin_popcount(mask) < 3; ++b) mask |= 1u << b;
+            const int rw = r.smem ? 3 : RW;
+            for (int b = 3; b < P.m && __builtin_popcount(mask) < rw; ++b) mask |= 1u << b;
+            for (int b = 0; b < P.m && __builtin_popcount(mask) < rw; ++b) mask |= 1u << b;
             RoundDesc& rd = P.rounds[P.nrounds++];
             rd.flags = r.smem ? RD_SMEM : 0;
             int c = 0;
             for (int b = 0; b < P.m; ++b)
-                if (mask >> b & 1) rd.r[c++] = std::uint8_t(b);
+                if (mask >> b & 1) {
+                    if (c < 3) rd.r[c] = std::uint8_t(b);
+                    else rd.flags = std::uint8_t(rd.flags | RD_W4 | (b << 4));
+                    ++c;
+                }
             auto reg = [&](int pos) -> int {
                 const int l = loc[pos];
-                for (int i = 0; i < 3; ++i)
-                    if (rd.r[i] == l) return i;
+                for (int i = 0; i < round_width(rd); ++i)
+                    if (round_reg(rd, i) == l) return i;
                 return -1;
             };
             rd.op_begin = std::uint16_t(nops);
@@ -1192,7 +1233,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             if (!r.smem) {
                 for (std::size_t i = 0; i < r.ops.size(); ++i) {
                     const FOp& f = at(r.ops[i]);
-                    bool movable = !kNoTables && f.kind == TOP_DIAG && npool + 8 <= kPassPool - 12;
+                    bool movable = !kNoTables && f.kind == TOP_DIAG && npool + RG <= kPassPool - 4 * RW;
                     for (int j = 0; movable && j < f.dk; ++j) movable = loc[f.dpos[j]] >= 0 && reg(f.dpos[j]) >= 0;
                     if (movable) {  // +-1 diagonals stay pending sign flips (cheaper)
                         bool signed_only = true;
@@ -1367,7 +1408,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 }
                 // consecutive +-1 diagonals (CZ rings, Z): one bundled operation; the ones with
                 // no group-constant bit fold into one flip byte at plan time
-                if (o.kind == (TOP_DIAG | KF_SIGNED) && nops > rd.op_begin) {
+                if (o.kind == (TOP_DIAG | KF_SIGNED) && nops > rd.op_begin && RW == 3) {
                     RegOp& prev = P.ops[nops - 1];
                     auto add_entry = [&](const RegOp& x, RegOp& b) {
                         const bool c0 = x.dreg[0] == 0xff, c1 = x.dk == 2 && x.dreg[1] == 0xff;
@@ -1407,10 +1448,10 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                     const bool prev_gate = (prev.kind & ~(KF_BUNDLE | KF_FLUSH | KF_REAL)) == TOP_GATE &&
                                            !prev.lctrl_mask && (prev.kind & KF_REAL) == (o.kind & KF_REAL);
                     const unsigned pmask = (prev.kind & KF_BUNDLE) ? prev.t : (1u << prev.t);
-                    if (prev_gate && !(pmask & (1u << o.t)) && ((prev.kind & KF_BUNDLE) || npool + 12 <= kPassPool)) {
+                    if (prev_gate && !(pmask & (1u << o.t)) && ((prev.kind & KF_BUNDLE) || npool + 4 * RW <= kPassPool)) {
                         if (!(prev.kind & KF_BUNDLE)) {
                             prev.ref = std::uint16_t(npool);
-                            npool += 12;
+                            npool += 4 * RW;
                             for (int k = 0; k < 4; ++k) P.pool[prev.ref + 4 * prev.t + k] = prev.c[k];
                             prev.kind = std::uint8_t(prev.kind | KF_BUNDLE);
                             prev.t = std::uint8_t(1u << prev.t);
@@ -1427,7 +1468,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 RegOp o{};
                 o.kind = TOP_DTAB;
                 o.ref = std::uint16_t(npool);
-                for (int q = 0; q < 8; ++q) {
+                for (int q = 0; q < RG; ++q) {
                     cplx t(1.0, 0.0);
                     for (int idx : tab) {
                         const FOp& f = at(idx);
@@ -1436,9 +1477,12 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                         if (!f.dskip[g]) t *= cplx(f.dval[g].x, f.dval[g].y);
                     }
                     P.pool[npool + q] = make_double2(t.real(), t.imag());
-                    if (t == cplx(1.0, 0.0)) o.dskip = std::uint8_t(o.dskip | (1u << q));
+                    if (t == cplx(1.0, 0.0)) {
+                        if (q < 8) o.dskip = std::uint8_t(o.dskip | (1u << q));
+                        o.smask |= 1u << q;  // the skip mask of all RG entries (16-register rounds)
+                    }
                 }
-                npool += 8;
+                npool += RG;
                 P.ops[nops++] = o;
             }
             for (int idx : trailing) perm_op(at(idx));
@@ -1454,7 +1498,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             bool perms = false;
             if (virt_pass)
                 for (int idx : lists[pi]) perms |= is_perm(ops[std::size_t(idx)]);
-            if (!has_alt[pi] && !perms && schedule_rounds(n, loc, P.m, ops, lists[pi], sched_ops, sched_list))
+            if (!has_alt[pi] && !perms && schedule_rounds(n, loc, P.m, ops, lists[pi], sched_ops, sched_list, RW))
                 lower_list(sched_ops, sched_list);
             else
                 lower_list(ops, lists[pi]);
@@ -1543,8 +1587,10 @@ void dump_pass(std::FILE* f, const PassParams& p, std::size_t nsrc) {
     const int nr = p.alt_mode == ALT_ROUNDS ? p.alt_begin + p.alt_nrounds : p.nrounds;
     for (int r = 0; r < nr; ++r) {
         const RoundDesc& R = p.rounds[r];
-        std::fprintf(f, "  round%s%s regs=%d,%d,%d:", (R.flags & RD_SMEM) ? " smem" : "", r >= p.nrounds ? " alt" : "",
+        std::fprintf(f, "  round%s%s regs=%d,%d,%d", (R.flags & RD_SMEM) ? " smem" : "", r >= p.nrounds ? " alt" : "",
                      R.r[0], R.r[1], R.r[2]);
+        if (R.flags & RD_W4) std::fprintf(f, ",%d", round_reg(R, 3));
+        std::fprintf(f, ":");
         for (int i = R.op_begin; i < R.op_begin + R.op_count; ++i) {
             const RegOp& o = p.ops[i];
             static const char* names[] = {"G", "D", "SIGN", "WHT", "SC", "DTAB", "PERM"};

@@ -156,11 +156,11 @@ __device__ __forceinline__ double2 cmul2_f(double2 a, double2 x0, double2 b, dou
 // One-target gate as a dense 2x2 on the register pairs along bit T; `en` = the registers whose
 // tile-local controls hold (0xff without controls).  One straight-line form for every gate keeps
 // the register allocation of the round loop free of per-kind copies.
-template <int T, bool CTRL>
-__device__ __forceinline__ void gate1(double2 (&v)[8], const double2* c, unsigned en) {
+template <int T, bool CTRL, int NR>
+__device__ __forceinline__ void gate1(double2 (&v)[NR], const double2* c, unsigned en) {
     const double2 a0 = c[0], b0 = c[1], a1 = c[2], b1 = c[3];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NR; ++q) {
         if (q & (1 << T)) continue;
         const double2 x0 = v[q], x1 = v[q | (1 << T)];
         const double2 n0 = cmul2_f(a0, x0, b0, x1), n1 = cmul2_f(a1, x0, b1, x1);
@@ -172,11 +172,11 @@ __device__ __forceinline__ void gate1(double2 (&v)[8], const double2* c, unsigne
 
 // The same with real coefficients (RY, H, X, CNOT, the real factor of a phase-split gate): half
 // the FP64 instructions of the complex form.
-template <int T, bool CTRL>
-__device__ __forceinline__ void gate1r(double2 (&v)[8], const double2* c, unsigned en) {
+template <int T, bool CTRL, int NR>
+__device__ __forceinline__ void gate1r(double2 (&v)[NR], const double2* c, unsigned en) {
     const double a0 = c[0].x, b0 = c[1].x, a1 = c[2].x, b1 = c[3].x;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NR; ++q) {
         if (q & (1 << T)) continue;
         const double2 x0 = v[q], x1 = v[q | (1 << T)];
         const double2 n0 = make_double2(fma(a0, x0.x, b0 * x1.x), fma(a0, x0.y, b0 * x1.y));
@@ -191,10 +191,10 @@ __device__ __forceinline__ void gate1r(double2 (&v)[8], const double2* c, unsign
 // register pairs along bit T of the registers in EN; the row scales sit in the round's table.
 // NEG bit q: the pair (q, q | 1 << T) holds registers of opposite pending sign (lazy +-1 flips,
 // jit.cpp SignTrack): both rows use -rho (a free operand negation in the DFMAs).
-template <int T, bool P0, bool P1, bool Z0, bool Z1, bool REAL, unsigned EN, unsigned NEG = 0u>
-__device__ __forceinline__ void gate1p(double2 (&v)[8], double2 rho0_, double2 rho1_) {
+template <int T, bool P0, bool P1, bool Z0, bool Z1, bool REAL, unsigned EN, unsigned NEG = 0u, int NR>
+__device__ __forceinline__ void gate1p(double2 (&v)[NR], double2 rho0_, double2 rho1_) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NR; ++q) {
         if ((q & (1 << T)) || !((EN >> q) & 1u)) continue;
         const bool ng = (NEG >> q) & 1u;
         const double2 rho0 = ng ? make_double2(-rho0_.x, -rho0_.y) : rho0_;
@@ -221,9 +221,10 @@ __device__ __forceinline__ double flipd(double x, unsigned s) {
     return __longlong_as_double(__double_as_longlong(x) ^ ((long long)(s & 1u) << 63));
 }
 // negate the registers in mask (bit q: register q)
-__device__ __forceinline__ void flip_mask(double2 (&v)[8], unsigned mask) {
+template <int NR>
+__device__ __forceinline__ void flip_mask(double2 (&v)[NR], unsigned mask) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = flipd2(v[q], mask >> q);
+    for (int q = 0; q < NR; ++q) v[q] = flipd2(v[q], mask >> q);
 }
 
 // Apply and clear the pending +-1 flips (bit q of negacc: negate register q) by xor of the sign
@@ -242,10 +243,10 @@ __device__ __forceinline__ void flip_signs(double2 (&v)[NG][8], unsigned (&negac
     }
 }
 
-template <int B>
-__device__ __forceinline__ void butterfly(double2 (&v)[8]) {
+template <int B, int NR>
+__device__ __forceinline__ void butterfly(double2 (&v)[NR]) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NR; ++q) {
         if (q & (1 << B)) continue;
         const double2 a = v[q], b = v[q | (1 << B)];
         v[q] = make_double2(a.x + b.x, a.y + b.y);
@@ -257,16 +258,16 @@ __device__ __forceinline__ void butterfly(double2 (&v)[8]) {
 // q, the others are constant over the thread's group (taken from the group's first element).
 // One-bit diagonal on register bit T: entry 0 on the registers with bit T clear, entry 1 on the
 // others; an entry that is exactly 1 (skip bit) is not applied.
-template <int T>
-__device__ __forceinline__ void diag_reg(double2 (&v)[8], double2 c0, double2 c1, unsigned skip) {
+template <int T, int NR>
+__device__ __forceinline__ void diag_reg(double2 (&v)[NR], double2 c0, double2 c1, unsigned skip) {
     if (!(skip & 1u)) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < NR; ++q)
             if (!(q >> T & 1)) v[q] = cmul_f(c0, v[q]);
     }
     if (!(skip & 2u)) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < NR; ++q)
             if (q >> T & 1) v[q] = cmul_f(c1, v[q]);
     }
 }
@@ -403,9 +404,10 @@ constexpr unsigned long tile_smem(int m) {
 }
 
 // One group of 8 register amplitudes: apply and clear pending +-1 flips (bit q: negate register q)
-__device__ __forceinline__ void flip_signs1(double2 (&v)[8], unsigned& negacc) {
+template <int NR>
+__device__ __forceinline__ void flip_signs1(double2 (&v)[NR], unsigned& negacc) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NR; ++q) {
         const long long m = (long long)((negacc >> q) & 1u) << 63;
         v[q] = make_double2(__longlong_as_double(__double_as_longlong(v[q].x) ^ m),
                             __longlong_as_double(__double_as_longlong(v[q].y) ^ m));
