@@ -1101,7 +1101,7 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             bool ok = true;
             for (int idx : lists[pi]) {
                 const FOp& f = ops[std::size_t(idx)];
-                if (f.kind == TOP_SIGN || (f.kind == TOP_GATE && f.K >= 2) || f.kind == TOP_PERM) ok = false;
+                if (f.kind == TOP_SIGN || (f.kind == TOP_GATE && f.K >= 2)) ok = false;
                 if (f.kind == TOP_GATE && f.K == 1 && f.nrows == 2 && f.nnz[0] == 1 && f.nnz[1] == 1 && virt_pass) ok = false;
             }
             if (ok) RW = 4;
