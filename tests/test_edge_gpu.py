@@ -193,3 +193,42 @@ def test_plan_cache_reuse_and_invalidation(Q, oracle):
     finally:
         Q.set_jit_mode(old)
     st.close()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_light_cone_planner_random_layers(Q, oracle, seed):
+    """The round-2 planner on layered circuits it reorders: random one-qubit catalog gates on
+    every qubit per layer, then diagonal couplings (CZ, CPhase, RZZ, CRZ, CU1) on random pairs --
+    the light-cone round scheduler, 16-register rounds, scale chaining, table normalisation and
+    the tile search all engage.  Against the oracle at n = 14..20, default jit mode and every
+    pass specialised (mode 3)."""
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(14, 21))
+    one = [i for i in Q.gate_catalog() if i.arity == 1]
+    diag2 = ["Controlled-Z", "CPhase", "RZZ", "CRZ", "CU1"]
+    steps = [Q.hadamard_all(n)]
+    for _ in range(int(rng.integers(3, 7))):
+        pl = []
+        for q in range(n):
+            info = one[int(rng.integers(0, len(one)))]
+            pl.append(Q.Placement(Q.gate_catalog_lookup(info.name, list(rng.uniform(0, 2 * np.pi, info.param_count))), q))
+        steps.append(Q.CircuitStep.of_gates(pl))
+        perm = [int(x) for x in rng.permutation(n)]
+        for k in range(0, n - 1, 2):
+            name = diag2[int(rng.integers(0, len(diag2)))]
+            info = next(i for i in Q.gate_catalog() if i.name == name)
+            g = Q.gate_catalog_lookup(name, list(rng.uniform(0, 2 * np.pi, info.param_count)))
+            steps.append(Q.CircuitStep.of_gates([Q.Placement(g, qubits=[perm[k], perm[k + 1]])]))
+    c = Q.Circuit(n, steps, 0)
+    want = oracle_run(oracle, c)
+    old = Q.jit_mode()
+    try:
+        for mode in (1, 3):
+            Q.set_jit_mode(mode)
+            got = Q.simulate(c, Q.Engine.rh_dax).final.download()
+            assert np.abs(got - want).max() <= TOL_AMP, (mode, n)
+            assert np.linalg.norm(got - want) <= TOL_L2, (mode, n)
+    finally:
+        Q.set_jit_mode(old)
+    st = Q.plan_stats(c)
+    assert st["tile_passes"] >= 1 and Q.plan_verify(c) >= 1
