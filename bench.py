@@ -635,6 +635,21 @@ def run_sharded(args, rank, world, local_rank):
     ms = dist.max(ms)
     st = sh.exchange_stats()
     ex_ms = dist.max(st["ms"])
+    launches = 0
+    if not dry:
+        from paper_2411_15332_b200 import _lib
+        l0 = _lib.lib().qcs_kernel_launches()
+    # e2e: host wall clock per step around the public path -- the circuit's operations marshalled
+    # from the host, the sharded run with its exchanges, and a read-back of the shard's norm into
+    # host memory on every rank (max over ranks)
+    t0 = time.perf_counter()
+    norms = []
+    for _ in range(args.steps):
+        step()
+        norms.append(float(torch.linalg.vector_norm(backend.tensor).item()) if not dry else 0.0)
+    e2e_ms = dist.max(1e3 * (time.perf_counter() - t0))
+    if not dry:
+        launches = int(_lib.lib().qcs_kernel_launches() - l0)
     value = updates * args.steps / (ms / 1e3)
     shard_bytes = 16 << (n - g)
     per_step_bytes = st["bytes_sent"] / args.steps
@@ -655,6 +670,11 @@ def run_sharded(args, rank, world, local_rank):
                          "nvlink_frac": (st["bytes_sent"] / (ex_ms / 1e3) / 1e9 / NVLINK_GBPS) if ex_ms > 0 else None,
                          "share_of_step": (ex_ms / ms) if ms > 0 else None},
             "comm_init": dist.init_lines,
+            "e2e": {"value": updates * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": circuit_bytes(c), "d2h_bytes_per_step": 8,
+                    "ms_per_step": e2e_ms / args.steps,
+                    "timer": "host wall clock, max over ranks: operations from the host, sharded run, shard norm read back"},
+            "gpu_launches": launches // max(1, args.steps) * args.steps,
             "clocks": clocks.summary()}
     if dry:
         line["dry_run"] = True
