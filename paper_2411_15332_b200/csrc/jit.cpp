@@ -1121,7 +1121,8 @@ std::size_t jit_compile_only(const PassParams& p, bool verify_only) {
     if (verify_only) {  // generate with the addressing proof on, no NVRTC
         g_verify = true;
         try {
-            (void)pass_source(p, F, threads);
+            const std::string src = pass_source(p, F, threads);
+            if (std::getenv("QCS_JIT_DUMP")) std::fprintf(stderr, "---- qcs_pass (verify)\n%s", src.c_str());
         } catch (...) {
             g_verify = false;
             throw;
