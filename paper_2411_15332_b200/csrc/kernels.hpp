@@ -16,6 +16,7 @@ typedef struct CUstream_st* cudaStream_t;
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #endif
 
 namespace qcs {
@@ -163,6 +164,62 @@ struct RoundDesc {
 inline constexpr int round_width(const RoundDesc& R) { return (R.flags & RD_W4) ? 4 : 3; }
 inline constexpr int round_reg(const RoundDesc& R, int i) { return i < 3 ? int(R.r[i]) : int(R.flags >> 4); }
 
+#ifndef __CUDACC_RTC__  // host-side planning helpers
+// The TMA tensor-map layout of a tile: its bit set S over an n-bit state (bits 0..2 included).
+// Dim 0 is the tile's 8 contiguous amplitudes (16 doubles); every further dim is a run of <= 8
+// tile bits starting at state bit `pos`.  The state bits above a run, up to the next tile bit,
+// ride in the same dim as the high bits of its coordinate (extent 2^len, box 2^inlen), so only
+// the tile's own runs cost dims; a gap too wide for a 31-bit coordinate gets dims of its own
+// (inlen 0, box 1).  Coordinates: (base >> pos) & (2^len - 1), shifted left once for dim 0
+// (whose unit is one double).  Returns the rank; `out` (16 entries, may be null) receives the dims.
+// gap_dims = true: the round-1 layout, one dim per gap as well (A/B: QCS_TMA_GAP_DIMS=1).
+struct TmaDim {
+    int pos, len, inlen;
+};
+inline int tma_layout(std::uint64_t S, int n, TmaDim* out, bool gap_dims) {
+    if ((S & 7u) != 7u) return 99;
+    int rank = 0;
+    auto push = [&](int pos, int len, int inlen) {
+        if (out && rank < 16) out[rank] = TmaDim{pos, len, inlen};
+        ++rank;
+    };
+    auto gap = [&](int from, int to) {  // dims of their own over state bits [from, to)
+        for (int c = from; c < to; c += 31) push(c, to - c < 31 ? to - c : 31, 0);
+    };
+    int b = 3;
+    while (b < n && !(S >> b & 1)) ++b;
+    if (gap_dims || b > 30) {
+        push(0, 3, 3);
+        gap(3, b);
+    } else {
+        push(0, b, 3);
+    }
+    while (b < n) {
+        int e = b, g;
+        while (e < n && (S >> e & 1)) ++e;  // tile bits [b, e)
+        for (g = e; g < n && !(S >> g & 1);) ++g;  // the gap [e, g) above them
+        for (int c = b; c < e;) {
+            const int len = e - c < 8 ? e - c : 8;
+            if (c + len < e) {
+                push(c, len, len);
+            } else if (gap_dims || len + (g - e) > 31) {
+                push(c, len, len);
+                gap(e, g);
+            } else {
+                push(c, len + (g - e), len);
+            }
+            c += len;
+        }
+        b = g;
+    }
+    return rank;
+}
+inline bool tma_gap_dims() {
+    static const bool on = [] { const char* v = std::getenv("QCS_TMA_GAP_DIMS"); return v && std::atoi(v) != 0; }();
+    return on;
+}
+#endif
+
 #ifndef QCS_PASS_MAX_OPS
 #define QCS_PASS_MAX_OPS 200
 #endif
@@ -184,7 +241,7 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
     std::uint32_t hi_off;     // this pass's table of run offsets (tile bits 3..m-1) in the plan's tables
     int tma_rank;             // > 0: the tile moves as TMA boxes of this rank (set at launch)
     std::uint8_t tma_iter;    // the top tma_iter local tile bits are iterated: 2^tma_iter boxes per tile
-    std::uint8_t tma_gap_pos[5], tma_gap_len[5];  // box dims over bits outside the tile: coordinate bits
+    std::uint8_t tma_gap_pos[5], tma_gap_len[5];  // per dim: the state bits its coordinate spans (tma_layout)
     int nruns;                // the basis bits outside the tile, as runs: a tile index deposits into them
     std::uint8_t run_pos[16], run_len[16];
     std::uint32_t list_off, list_cnt;  // list_cnt > 0: run only these tiles (ALT_SKIP passes)

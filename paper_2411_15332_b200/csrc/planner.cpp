@@ -353,17 +353,7 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
     // dims of the tile's TMA tensor map (tile_tensor_map): bits 0..2, then every run of tile bits
     // (split at 8 bits) and every run of other bits; > 5 falls back to per-thread cp.async tiles,
     // which cost the pass ~15% more instructions (address arithmetic per 16 bytes)
-    auto tma_dims = [&](u64 S) {
-        int rank = 1;
-        for (int b = 3; b < n;) {
-            const bool in = S >> b & 1;
-            int e = b;
-            while (e < n && bool(S >> e & 1) == in) ++e;
-            rank += in ? (e - b + 7) / 8 : 1;
-            b = e;
-        }
-        return rank;
-    };
+    auto tma_dims = [&](u64 S) { return tma_layout(S, n, nullptr, tma_gap_dims()); };
     static const double tma_weight = [] {
         const char* v = std::getenv("QCS_TILE_TMA_WEIGHT");
         return v ? std::atof(v) : 0.85;

@@ -117,14 +117,19 @@ __device__ __forceinline__ void tma_store(const TmapParam* map, const int (&c)[5
 __device__ __forceinline__ void tma_store_commit_wait() {
     asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
+// coordinate of dim d of the box at basis index g (tile bits zero): the state bits the dim spans
+// (kernels.hpp tma_layout); dim 0 counts doubles, two per amplitude
+__device__ __forceinline__ int tma_coord(const PassParams& P, u64 g, int d) {
+    if (d >= P.tma_rank || !P.tma_gap_len[d]) return 0;
+    return int(((g >> P.tma_gap_pos[d]) & ((u64(1) << P.tma_gap_len[d]) - 1)) << (d == 0 ? 1 : 0));
+}
 // coordinates of box i of a tile whose top `iter` local bits are iterated: the tile base with i
 // deposited into those bits, read out per gap dimension
 __device__ __forceinline__ void tma_box_coords(const PassParams& P, u64 base, unsigned i, int (&cc)[5]) {
     u64 g = base;
     for (int k = 0; k < int(P.tma_iter); ++k)
         if (i >> k & 1) g |= u64(1) << P.bits[P.m - int(P.tma_iter) + k];
-    for (int d = 0; d < 5; ++d)
-        cc[d] = (d < P.tma_rank && P.tma_gap_len[d]) ? int((g >> P.tma_gap_pos[d]) & ((u64(1) << P.tma_gap_len[d]) - 1)) : 0;
+    for (int d = 0; d < 5; ++d) cc[d] = tma_coord(P, g, d);
 }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\nfence.mbarrier_init.release.cluster;\n" ::"r"(smem_u32(bar))
@@ -483,10 +488,7 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
         c.rb = P.alt_begin;
         c.re = c.rb + P.alt_nrounds;
     }
-    for (int d = 0; d < 5; ++d) c.tc[d] = 0;
-    if (P.tma_rank)
-        for (int d = 1; d < P.tma_rank; ++d)
-            if (P.tma_gap_len[d]) c.tc[d] = int((base >> P.tma_gap_pos[d]) & ((u64(1) << P.tma_gap_len[d]) - 1));
+    for (int d = 0; d < 5; ++d) c.tc[d] = tma_coord(P, base, d);
     if (P.init || (P.zmask && (base & P.zmask) != P.zval)) {
         // the pass starts from |init_index> (zeros and at most one 1), or from a tile the
         // circuit has not reached yet (zeros): nothing to load

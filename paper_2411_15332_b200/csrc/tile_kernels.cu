@@ -298,18 +298,7 @@ bool tile_tensor_map(double2* amps, int n, PassParams& p, CUtensorMap* map) {
     // the boxes cover the lowest m - iter local bits; the top `iter` ones are iterated (one box per
     // value, contiguous in shared memory): the fewest iterated bits that bring the map to <= 5
     // dims, with boxes of at least 64 amplitudes (1 KB)
-    auto dims = [&](u64 S) {
-        int rank = 1;
-        for (int b = 3; b < n;) {
-            const bool in = S >> b & 1;
-            int e = b;
-            while (e < n && bool(S >> e & 1) == in) ++e;
-            if (!in && e - b > 31) return 99;
-            rank += in ? (e - b + 7) / 8 : 1;
-            b = e;
-        }
-        return rank;
-    };
+    auto dims = [&](u64 S) { return tma_layout(S, n, nullptr, tma_gap_dims()); };
     static const bool no_iter = std::getenv("QCS_NO_TMA_ITER") != nullptr;  // A/B switch
     // at most a few big boxes: many small ones (C5's scattered tiles: 32+ boxes of 1-2 KB) were
     // slower than the per-thread cp.async tile (877 vs 819 ms per C5-family circuit at n=32)
@@ -322,28 +311,23 @@ bool tile_tensor_map(double2* amps, int n, PassParams& p, CUtensorMap* map) {
         tile &= ~(u64(1) << p.bits[p.m - 1 - iter]);
         ++iter;
     }
+    TmaDim L[16];
+    int rank = tma_layout(tile, n, L, tma_gap_dims());
+    if (rank > 5) return false;
     cuuint64_t gdim[5], gstride[4];
     cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
-    int rank = 1;
-    gdim[0] = 16;
-    box[0] = 16;
     std::uint8_t gpos[5] = {}, glen[5] = {};
-    for (int b = 3; b < n;) {
-        const bool in = tile >> b & 1;
-        int e = b;
-        while (e < n && bool(tile >> e & 1) == in) ++e;
-        for (int c = b; c < e;) {
-            const int len = in ? std::min(8, e - c) : e - c;
-            if (rank >= 5 || (!in && len > 31)) return false;
-            gdim[rank] = cuuint64_t(1) << len;
-            box[rank] = in ? cuuint32_t(1) << len : 1;
-            gstride[rank - 1] = cuuint64_t(16) << c;
-            gpos[rank] = std::uint8_t(in ? 0 : c);
-            glen[rank] = std::uint8_t(in ? 0 : len);
-            ++rank;
-            c += len;
+    for (int d = 0; d < rank; ++d) {
+        if (d == 0) {  // doubles: 16 per 8 amplitudes, then the gap bits above them
+            gdim[0] = cuuint64_t(2) << L[0].len;
+            box[0] = 16;
+        } else {
+            gdim[d] = cuuint64_t(1) << L[d].len;
+            box[d] = cuuint32_t(1) << L[d].inlen;
+            gstride[d - 1] = cuuint64_t(16) << L[d].pos;
         }
-        b = e;
+        gpos[d] = std::uint8_t(L[d].pos);
+        glen[d] = std::uint8_t(L[d].len > L[d].inlen || d == 0 ? L[d].len : 0);
     }
     if (rank < 2) {  // a 3-bit state: one more (unit) dim keeps the 2d..5d forms
         gdim[1] = 1;
