@@ -387,6 +387,43 @@ std::string affine_expr(const Affine& A, const char* var, unsigned regmask, int 
     return head + e;
 }
 
+// A +-1 diagonal whose phase bits are register bits and/or bits constant over the group
+// (c0 / c1: phase bit 0 / 1 is group-constant, at basis position p0 / p1).  sm holds, per value
+// cg of the constant bits, the G-bit mask of registers that flip.  The flips that do not depend
+// on the group (cg = 0) are returned for the round's pending mask `negacc`, which thereby stays a
+// compile-time constant (flip_signs1 then touches only the flagged registers); the
+// group-dependent rest is applied here, one conditional xor of the sign bit per affected
+// register (flip_cond) -- merging it into negacc made every later flush a run-time mask over all
+// registers (~5 integer instructions per register; 17% of a C4 pass's instructions).
+unsigned long long emit_signed(Out& o, unsigned long long sm, bool c0, bool c1, int dk, int p0, int p1, int G) {
+    const unsigned long long gmask = (1ull << G) - 1;
+    auto field = [&](int cg) { return (sm >> (G * cg)) & gmask; };
+    const unsigned long long m0 = field(0);
+    if (!c0 && !c1) return m0;
+    static const bool split = [] { const char* v = std::getenv("QCS_JIT_SPLIT_SIGNS"); return !v || std::atoi(v) != 0; }();
+    if (!split) {  // A/B: the group-dependent flips into negacc as well
+        o("      negacc ^= unsigned(0x%llxull >> (%d * (%s))) & 0x%llxu;\n", sm, G, const_bits(c0, c1, dk, p0, p1).c_str(), gmask);
+        return 0;
+    }
+    for (int a = 0; a <= (c0 ? 1 : 0); ++a)
+        for (int b = 0; b <= (c1 ? 1 : 0); ++b) {
+            if (!a && !b) continue;
+            const int cg = (a << (dk - 1)) | b;
+            const unsigned long long d = field(cg) ^ m0;
+            if (!d) continue;
+            auto term = [](int pos, int want) {  // 1u when basis bit `pos` of the group equals `want`
+                const std::string b = "(unsigned(g0 >> " + std::to_string(pos) + ") & 1u)";
+                return want ? b : "(" + b + " ^ 1u)";
+            };
+            std::string cond;
+            if (c0) cond = term(p0, a);
+            if (c1) cond = cond.empty() ? term(p1, b) : "(" + cond + " & " + term(p1, b) + ")";
+            o("      flip_cond<0x%llxu>(v, %s);\n", d, cond.c_str());
+        }
+    return m0;
+}
+
+
 // One register round: the interpreter's round loop (tile_kernels.cu) with every structural
 // field of the operations as a literal.  (16-amplitude rounds -- 4 register bits, 22% fewer
 // rounds for C4 -- were measured no faster at 2 resident tiles per SM and slower for C3.)
@@ -598,14 +635,13 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
                 one(op.smask, op.dreg[0] == 0xff, op.dk == 2 && op.dreg[1] == 0xff, op.dk, op.dpos[0], op.dpos[1]);
             }
         } else if (kind == TOP_DIAG && (kb & KF_SIGNED) && (kb & KF_BUNDLE)) {
-            o("      { unsigned acc = 0x%llxu;\n", (unsigned long long)(op.smask & gmask));
+            unsigned long long acc = op.smask & gmask;
             for (int i = 0; i < op.t; ++i) {
                 SignEntry e;
                 std::memcpy(&e, &P.pool[op.ref + i], sizeof(e));
-                o("        acc ^= unsigned(0x%llxull >> (%d * (%s))) & 0x%llxu;\n", (unsigned long long)e.smask, G,
-                  const_bits(e.cmask & 1u, e.cmask & 2u, e.dk, e.p0, e.p1).c_str(), gmask);
+                acc ^= emit_signed(o, e.smask, e.cmask & 1u, e.cmask & 2u, e.dk, e.p0, e.p1, G);
             }
-            o("        negacc ^= acc; }\n");
+            if (acc) o("      negacc ^= 0x%llxu;\n", acc);
         } else if (kind == TOP_DIAG && (kb & KF_SIGNED)) {
             const bool c0 = op.dreg[0] == 0xff, c1 = op.dk == 2 && op.dreg[1] == 0xff;
             unsigned long long sm = op.smask;  // byte cg: the registers that flip when the constant bits spell cg
@@ -622,8 +658,8 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
                         if (op.dskip >> g & 1) sm |= 1ull << (16 * cg + q);
                     }
             }
-            o("      negacc ^= unsigned(0x%llxull >> (%d * (%s))) & 0x%llxu;\n", sm, G,
-              const_bits(c0, c1, op.dk, op.dpos[0], op.dpos[1]).c_str(), gmask);
+            const unsigned long long acc = emit_signed(o, sm, c0, c1, op.dk, op.dpos[0], op.dpos[1], G);
+            if (acc) o("      negacc ^= 0x%llxu;\n", acc);
         } else if (kind == TOP_WHT) {
             for (int b = 0; b < W; ++b)
                 if (op.t >> b & 1) {
@@ -776,7 +812,7 @@ bool emit_register_round(Out& o, const PassParams& P, int ri, unsigned threads, 
         return true;
     }
     for (int q = 0; q < G; ++q) o("      sm[slb ^ %uu] = v[%d];\n", soff[q], q);
-    o("    }\n    __syncthreads();\n  }\n");
+    o("    }\n    QCS_SYNC();\n  }\n");
     return false;
 }
 
@@ -788,13 +824,13 @@ void emit_smem_round(Out& o, const PassParams& P, int ri, unsigned threads) {
         o("      if (!(o.gctrl_mask && (base & o.gctrl_mask) != o.gctrl_val)) {\n");
         o("        if (o.gcase == 2) smem_gate<2>(sm, o, %d, %uu); else smem_gate<3>(sm, o, %d, %uu);\n", P.m, threads,
           P.m, threads);
-        o("      }\n      __syncthreads(); }\n");
+        o("      }\n      QCS_SYNC(); }\n");
     }
     o("  }\n");
 }
 
 // one program (the main rounds or the missed-tile alternative), then the tile's write-back
-void emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threads) {
+bool emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threads, bool persist = false) {
     Affine map(P.m);
     bool direct = false;
     for (int ri = begin; ri < end; ++ri) {
@@ -805,10 +841,56 @@ void emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threa
             direct = emit_register_round(o, P, ri, threads, map, ri + 1 == end);
         }
     }
+    if (persist) {
+        if (direct) raise(QCS_ERR_SIM, "internal: a pipelined pass with direct stores");
+        return false;
+    }
     if (!direct) o("  tile_end(a, P, tmap, c);\n");
+    return direct;
 }
 
-std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
+// ---- persistent pipelined form (tile_device.cuh, "persistent pipelined passes")
+// Which passes take it: plain gate/diagonal passes (no sign steps, shared-memory rounds, skip or
+// support masks, tile lists, relabelled direct stores) whose tile moves as TMA boxes, with
+// enough tiles to fill the ring on every SM.  QCS_PERSIST: 0 off, 1 passes with 16-register
+// rounds (default: those run 2 CTAs per SM otherwise), 2 every eligible pass.
+int persist_knob() {
+    static const int v = [] { const char* e = std::getenv("QCS_PERSIST"); return e ? std::atoi(e) : 1; }();
+    return v;
+}
+constexpr unsigned kPersistThreads = 512, kPersistRing = 196608;  // two groups of 256; bytes of ring
+unsigned persist_slots(const PassParams& P) {
+    static const int cap = [] { const char* e = std::getenv("QCS_PERSIST_SLOTS"); return e ? std::atoi(e) : 4; }();
+    return std::min<unsigned>(unsigned(cap), kPersistRing / (16u << P.m));
+}
+int pass_state_bits(const PassParams& P) {
+    int n = P.m;
+    for (int i = 0; i < P.nruns; ++i) n += P.run_len[i];
+    return n;
+}
+bool has_direct_store(const PassParams& P) {
+    // the last round stores straight to HBM when a relabelling is live at it (emit_register_round)
+    for (int i = 0; i < P.nops; ++i)
+        if ((P.ops[i].kind & KF_KIND) == TOP_PERM) return true;
+    return false;
+}
+bool persist_wanted(const PassParams& P, unsigned F) {
+    const int knob = persist_knob();
+    if (knob <= 0 || P.m < 10 || P.m > 12) return false;
+    if ((F & (4u | 8u)) || P.alt_mode != ALT_NONE || P.list_cnt || P.init || P.zmask || P.smask) return false;
+    if (has_direct_store(P)) return false;
+    bool w4 = false;
+    for (int r = 0; r < P.nrounds; ++r) {
+        if (P.rounds[r].flags & RD_SMEM) return false;
+        w4 |= (P.rounds[r].flags & RD_W4) != 0;
+    }
+    if (knob == 1 && !w4) return false;
+    const int n = pass_state_bits(P);
+    if (n - P.m < 11) return false;  // >= 2048 tiles: several ring turns per SM
+    return tile_tma_iter(n, P) >= 0 && persist_slots(P) >= 3;
+}
+
+std::string pass_source(const PassParams& P, unsigned F, unsigned threads, bool persist) {
     Out o;
     static const int minb_env = [] { const char* v = std::getenv("QCS_JIT_MINB"); return v ? std::atoi(v) : 0; }();
     static const int w4_minb = [] { const char* v = std::getenv("QCS_W4_MINB"); return v ? std::atoi(v) : 2; }();
@@ -818,6 +900,33 @@ std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
     const int minb = minb_env > 0 ? minb_env : w4 ? w4_minb : (F & 8u) ? 2 : 3;
     o("#include \"tile_device.cuh\"\n");
     o("using namespace qcs;\nusing namespace qcs::tile;\n");
+    if (persist) {
+        const unsigned S = persist_slots(P);
+        o("#define QCS_SYNC() group_sync(grp)\n");
+        o("extern \"C\" __global__ void __launch_bounds__(%u, 1)\n", kPersistThreads);
+        o("qcs_pass(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,\n");
+        o("         const u64* __restrict__ flipped, const u64* __restrict__ tables, const __grid_constant__ TmapParam tmap) {\n");
+        o("  extern __shared__ __align__(1024) unsigned char smem_raw[];\n");
+        o("  PersistCtx c;\n");
+        o("  persist_begin<%uu>(P, tables, tmap, smem_raw, c);\n", S);
+        o("  const u64* const hi_tab = c.hi_tab;\n");
+        o("  const unsigned grp = threadIdx.x >> 8, t = threadIdx.x & 255u;\n");
+        o("  const unsigned sign_hit = 0;\n  (void)sign_hit; (void)hi_tab; (void)big; (void)flipped; (void)a;\n");
+        o("  unsigned slot = grp, use = 0;\n");
+        o("#pragma unroll 1\n");
+        o("  for (u64 tile = blockIdx.x + u64(grp) * gridDim.x; tile < c.ntiles; tile += 2ull * gridDim.x) {\n");
+        o("  double2* const sm = c.sm0 + (slot << %d);\n", P.m);
+        o("  const u64 base = tile_base_of(P, tile);\n");
+        o("  mbar_wait(c.full + 2u * slot + (use & 1u), (use >> 1) & 1u);\n");
+        emit_rounds(o, P, 0, P.nrounds, 256, true);
+        o("  persist_end<%uu>(P, tmap, c, grp, t, tile, base, sm, c.full + 2u * slot + ((use + 1u) & 1u));\n", S);
+        o("  slot += 2u;\n  if (slot >= %uu) { slot -= %uu; ++use; }\n", S, S);
+        o("  }\n");
+        o("  if (t == 0) persist_finish();\n");
+        o("}\n");
+        return o.s;
+    }
+    o("#define QCS_SYNC() __syncthreads()\n");
     o("extern \"C\" __global__ void __launch_bounds__(%u, %d)\n", threads, minb);
     o("qcs_pass(double2* __restrict__ a, const __grid_constant__ PassParams P, const TileOp* __restrict__ big,\n");
     o("         const u64* __restrict__ flipped, const u64* __restrict__ tables, const __grid_constant__ TmapParam tmap) {\n");
@@ -839,6 +948,9 @@ std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
     o("}\n");
     return o.s;
 }
+std::string pass_source(const PassParams& P, unsigned F, unsigned threads) {
+    return pass_source(P, F, threads, persist_wanted(P, F));
+}
 
 // FP64 instructions per tile of the pass's main program as its specialised kernel runs it
 // (per thread, summed over the tile's 2^m / 8 groups)
@@ -859,6 +971,8 @@ void nvrtc_check(nvrtcResult r, const char* what) {
 struct JitKernel {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kernel = nullptr;
+    bool persist = false;        // the persistent pipelined form: one CTA of 512 threads per SM
+    std::size_t persist_smem = 0;
     std::set<int> attr_devices;  // devices whose dynamic shared-memory limit is raised
     std::map<int, CUfunction> fn;  // per device: the kernel's function in that device's context
 };
@@ -1006,6 +1120,7 @@ JitKernel& load(const std::string& src, const std::vector<char>& cubin) {
     QCS_CUDA(cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     QCS_CUDA(cudaLibraryGetKernel(&k->kernel, k->lib, "qcs_pass"));
     ++g_compiles;
+    k->persist = src.find("persist_begin<") != std::string::npos;
     auto& ref = *k;
     g_cache.emplace(src, std::move(k));
     return ref;
@@ -1148,8 +1263,20 @@ bool launch_tile_pass_jit(double2* amps, const PassParams& p, unsigned F, const 
     {
         std::lock_guard<std::mutex> lk(g_mu);
         // a plan the caller keeps remembers its kernel (no source generation on reuse)
-        JitKernel& k = jit_slot && *jit_slot ? *static_cast<JitKernel*>(*jit_slot) : compile(pass_source(p, F, threads));
+        JitKernel& k = jit_slot && *jit_slot
+                           ? *static_cast<JitKernel*>(*jit_slot)
+                           : compile(pass_source(p, F, threads, p.tma_rank > 0 && persist_wanted(p, F)));
         if (jit_slot) *jit_slot = &k;
+        if (k.persist) {  // one CTA per SM, the ring of tile slots in its shared memory
+            if (p.tma_rank <= 0) raise(QCS_ERR_SIM, "internal: a pipelined pass kernel without a tensor map");
+            static int sms[64] = {};
+            if (dev < 64 && !sms[dev]) QCS_CUDA(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
+            const unsigned nsm = unsigned(dev < 64 && sms[dev] > 0 ? sms[dev] : 148);
+            tiles = std::min(tiles, nsm);
+            threads = kPersistThreads;
+            smem = 1024 + std::size_t(persist_slots(p)) * (std::size_t(16) << p.m) + (std::size_t(8) << (p.m - 3)) + 128;
+            smem_max = std::max(smem_max, smem);
+        }
         if (drv.ok) {
             auto it = k.fn.find(dev);
             if (it == k.fn.end()) {

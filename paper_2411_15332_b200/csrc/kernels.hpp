@@ -278,6 +278,9 @@ void set_jit_mode(int mode);
 // NVRTC only (no device): cubin bytes; verify_only: generate with the addressing proof, no compile
 std::size_t jit_compile_only(const struct PassParams& p, bool verify_only = false);
 void tile_pass_shape(const struct PassParams& p, unsigned& F, unsigned& threads);  // kernel variant, CTA size
+// host only: how many of the tile's top local bits its TMA boxes iterate (tile_tensor_map's
+// choice), or -1 when the tile does not move as TMA boxes
+int tile_tma_iter(int n, const struct PassParams& p);
 unsigned long long jit_compiles();   // pass kernels compiled so far
 #endif
 

@@ -276,7 +276,10 @@ void split_phases(std::vector<FOp>& ops) {
     ops.swap(out);
 }
 
-Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
+namespace {
+// One greedy plan.  strict_dims: the tile search counts tensor-map dims the round-1 way (a dim per
+// gap between tile runs as well) when it prefers tiles that move as one TMA box.
+Plan plan_ops_policy(int n, const std::vector<FOp>& ops, int max_bits, bool strict_dims) {
     Plan plan;
     const int M = std::min(max_bits, n);
     static const bool no_seed = knob("QCS_NO_TILE_SEARCH");  // A/B switch
@@ -353,7 +356,7 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
     // dims of the tile's TMA tensor map (tile_tensor_map): bits 0..2, then every run of tile bits
     // (split at 8 bits) and every run of other bits; > 5 falls back to per-thread cp.async tiles,
     // which cost the pass ~15% more instructions (address arithmetic per 16 bytes)
-    auto tma_dims = [&](u64 S) { return tma_layout(S, n, nullptr, tma_gap_dims()); };
+    auto tma_dims = [&](u64 S) { return tma_layout(S, n, nullptr, strict_dims || tma_gap_dims()); };
     static const double tma_weight = [] {
         const char* v = std::getenv("QCS_TILE_TMA_WEIGHT");
         return v ? std::atof(v) : 0.85;
@@ -409,6 +412,27 @@ Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
         remaining.swap(best.skipped);
     }
     return plan;
+}
+}  // namespace
+
+// The tile search is greedy (most gates per pass), so which tiles count as one TMA box steers
+// where the passes of a layered circuit cut it, and one more pass is one more sweep of the state.
+// Plan under both dim counts -- the layout the kernels use, and the stricter round-1 count --
+// and keep the plan with fewer passes (ties: fewer tiles that need more than 5 dims, then the
+// kernels' own count).  C4 n=32: 9 passes under the kernels' count alone, 8 under the strict one.
+Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
+    static const bool one_policy = knob("QCS_PLAN_ONE_POLICY") || knob("QCS_NO_TILE_SEARCH");  // A/B switch
+    Plan a = plan_ops_policy(n, ops, max_bits, false);
+    if (one_policy || tma_gap_dims() || a.passes.size() < 3) return a;
+    Plan b = plan_ops_policy(n, ops, max_bits, true);
+    auto non_tma = [&](const Plan& p) {
+        int c = 0;
+        for (const auto& q : p.passes) c += tma_layout(q.tile, n, nullptr, false) > 5;
+        return c;
+    };
+    if (b.passes.size() < a.passes.size()) return b;
+    if (b.passes.size() == a.passes.size() && non_tma(b) < non_tma(a)) return b;
+    return a;
 }
 
 // The program a pass runs on tiles that none of its sign steps' listed indices fall in: each
@@ -1094,7 +1118,16 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
                 if (f.kind == TOP_SIGN || (f.kind == TOP_GATE && f.K >= 2)) ok = false;
                 if (f.kind == TOP_GATE && f.K == 1 && f.nrows == 2 && f.nnz[0] == 1 && f.nnz[1] == 1 && virt_pass) ok = false;
             }
-            if (ok) RW = 4;
+            // worth it only for passes with arithmetic to spare: a pass of a few butterflies is
+            // HBM bound, and the 16-register kernels keep 2 tiles resident per SM instead of 3
+            // (C3 n=30: 11.1 ms with them, 9.9 ms without)
+            static const int w4_min_gates = [] { const char* v = std::getenv("QCS_W4_MIN_GATES"); return v ? std::atoi(v) : 16; }();
+            int work = 0;
+            for (int idx : lists[pi]) {
+                const FOp& f = ops[std::size_t(idx)];
+                work += (f.kind == TOP_GATE || f.kind == TOP_WHT) ? 1 : 0;
+            }
+            if (ok && work >= w4_min_gates) RW = 4;
         }
         const int RG = 1 << RW;  // registers per group
         // rounds of <= 3 register bits; gates on 2-3 targets get shared-memory rounds

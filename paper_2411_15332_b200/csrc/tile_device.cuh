@@ -408,6 +408,18 @@ constexpr unsigned long tile_smem(int m) {
     return 1024ul + (1ul << m) * 16 + ((1ul << (m - 3)) * 8 > 16 ? (1ul << (m - 3)) * 8 : 16ul) + 16;
 }
 
+// negate the registers in M (a literal) when cond (0 / 1, uniform over the group) is set: one xor
+// of the sign word per component
+template <unsigned M, int NR>
+__device__ __forceinline__ void flip_cond(double2 (&v)[NR], unsigned cond) {
+    const int hm = int(cond << 31);
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+        if ((M >> q) & 1u)
+            v[q] = make_double2(__hiloint2double(__double2hiint(v[q].x) ^ hm, __double2loint(v[q].x)),
+                                __hiloint2double(__double2hiint(v[q].y) ^ hm, __double2loint(v[q].y)));
+}
+
 // One group of 8 register amplitudes: apply and clear pending +-1 flips (bit q: negate register q)
 template <int NR>
 __device__ __forceinline__ void flip_signs1(double2 (&v)[NR], unsigned& negacc) {
@@ -571,6 +583,122 @@ __device__ __forceinline__ void tile_end(double2* a, const PassParams& P, const 
         for (unsigned j = t, k = 0; j < sz; j += bt, k += rs) __stcs(a + (gt | c.hi_tab[k]), c.sm[swz(j)]);
     }
 }
+
+
+// ---------------------------------------------------------------- persistent pipelined passes
+// One CTA per SM walks its share of the pass's tiles (tile = blockIdx.x + k * gridDim.x) through a
+// ring of S shared-memory slots.  Two groups of 256 threads compute alternate tiles (group k & 1
+// takes the CTA's k-th tile, in slot k % S; named barrier 1 + group), so while both groups work
+// the ring's other slots are being written back and refilled by TMA: the HBM round trip of a tile
+// hides behind the arithmetic of its neighbours instead of sitting between a CTA's launch and its
+// first round.  The thread that issues a tile's store waits until the store has read the slot,
+// then loads the CTA's (k + S)-th tile into it.  Each slot has TWO mbarriers, taken in turn by
+// its uses (barrier use & 1, parity (use >> 1) & 1): with an odd ring the uses of a slot
+// alternate between the groups, and a group that waits for use u + 1 on a single barrier whose
+// phase u is still incomplete (the other group's tile has not landed yet) would see the
+// "preceding" phase u - 1 as the one it asked for and run on a slot that is not its own.  With
+// two barriers the group that waits on one has itself consumed that barrier's previous phase.
+struct PersistCtx {
+    double2* sm0;              // slot 0 (1 KB aligned); slot s at sm0 + (s << m)
+    u64* hi_tab;               // the pass's run-offset table (as in TileCtx)
+    unsigned long long* full;  // 2 S mbarriers (slot s, use parity p: full[2 s + p]): the slot's tile has landed
+    u64 ntiles;
+};
+
+__device__ __forceinline__ u64 tile_base_of(const PassParams& P, u64 tl) {
+    u64 base = 0;
+    for (int i = 0; i < P.nruns; ++i) {
+        base |= (tl & ((u64(1) << P.run_len[i]) - 1)) << P.run_pos[i];
+        tl >>= P.run_len[i];
+    }
+    return base;
+}
+__device__ __forceinline__ void group_sync(unsigned grp) {
+    asm volatile("bar.sync %0, 256;\n" ::"r"(grp + 1u) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n.reg .pred done;\nWAITP_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+        "@!done bra WAITP_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+// one thread: the tile at basis offset `base` into `dst` (completes on `bar`)
+__device__ __forceinline__ void tile_load_async(const PassParams& P, const TmapParam& tmap, u64 base, double2* dst,
+                                                unsigned long long* bar) {
+    const unsigned sz = 1u << P.m;
+    mbar_expect_tx(bar, sz * 16u);
+    if (!P.tma_iter) {
+        int cc[5];
+        for (int d = 0; d < 5; ++d) cc[d] = tma_coord(P, base, d);
+        tma_load(dst, &tmap, cc, P.tma_rank, bar);
+    } else {
+        const unsigned nb = 1u << P.tma_iter, chunk = sz >> P.tma_iter;
+        for (unsigned i = 0; i < nb; ++i) {
+            int cc[5];
+            tma_box_coords(P, base, i, cc);
+            tma_load(dst + i * chunk, &tmap, cc, P.tma_rank, bar);
+        }
+    }
+}
+// one thread: the slot back to its tile; returns once the store has read the slot
+__device__ __forceinline__ void tile_store_read(const PassParams& P, const TmapParam& tmap, u64 base, const double2* src) {
+    const unsigned sz = 1u << P.m;
+    if (!P.tma_iter) {
+        int cc[5];
+        for (int d = 0; d < 5; ++d) cc[d] = tma_coord(P, base, d);
+        tma_store(&tmap, cc, P.tma_rank, src);
+    } else {
+        const unsigned nb = 1u << P.tma_iter, chunk = sz >> P.tma_iter;
+        for (unsigned i = 0; i < nb; ++i) {
+            int cc[5];
+            tma_box_coords(P, base, i, cc);
+            tma_store(&tmap, cc, P.tma_rank, src + i * chunk);
+        }
+    }
+    tma_store_commit_wait();
+}
+
+template <unsigned S>
+__device__ __forceinline__ void persist_begin(const PassParams& P, const u64* tables, const TmapParam& tmap,
+                                              unsigned char* smem_raw, PersistCtx& c) {
+    const unsigned sz = 1u << P.m, ngroups = sz >> 3;
+    const unsigned align_pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    c.sm0 = reinterpret_cast<double2*>(smem_raw + align_pad);
+    c.hi_tab = reinterpret_cast<u64*>(c.sm0 + S * sz);
+    c.full = reinterpret_cast<unsigned long long*>(c.hi_tab + (ngroups < 2 ? 2 : ngroups));
+    int out_bits = 0;
+    for (int i = 0; i < P.nruns; ++i) out_bits += P.run_len[i];
+    c.ntiles = u64(1) << out_bits;
+    const unsigned t = threadIdx.x, bt = blockDim.x;
+    for (unsigned j = 2 * t; j < ngroups; j += 2 * bt) cp_async16(c.hi_tab + j, tables + P.hi_off + j);
+    if (t == 0) {
+        for (unsigned s = 0; s < 2 * S; ++s) mbar_init(c.full + s);
+        for (unsigned s = 0; s < S; ++s) {
+            const u64 tile = blockIdx.x + u64(s) * gridDim.x;
+            if (tile < c.ntiles) tile_load_async(P, tmap, tile_base_of(P, tile), c.sm0 + s * sz, c.full + 2 * s);
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+}
+
+// after the group's last round on the CTA's k-th tile (in `sm`): write it back and refill the slot
+// (bar: the barrier of the slot's NEXT use)
+template <unsigned S>
+__device__ __forceinline__ void persist_end(const PassParams& P, const TmapParam& tmap, const PersistCtx& c, unsigned grp,
+                                            unsigned t, u64 tile, u64 base, double2* sm, unsigned long long* bar) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    group_sync(grp);
+    if (t == 0) {
+        tile_store_read(P, tmap, base, sm);
+        const u64 next = tile + u64(S) * gridDim.x;
+        if (next < c.ntiles) tile_load_async(P, tmap, tile_base_of(P, next), sm, bar);
+    }
+}
+// before the CTA exits: every store this thread issued has read its slot (persist_end waits per
+// store, so this only documents the invariant)
+__device__ __forceinline__ void persist_finish() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 
 }  // namespace tile
 }  // namespace qcs

@@ -295,22 +295,10 @@ bool tile_tensor_map(double2* amps, int n, PassParams& p, CUtensorMap* map) {
             cudaGetLastError();
     }
     if (!encode || n > 36 || p.m < 3) return false;
-    // the boxes cover the lowest m - iter local bits; the top `iter` ones are iterated (one box per
-    // value, contiguous in shared memory): the fewest iterated bits that bring the map to <= 5
-    // dims, with boxes of at least 64 amplitudes (1 KB)
-    auto dims = [&](u64 S) { return tma_layout(S, n, nullptr, tma_gap_dims()); };
-    static const bool no_iter = std::getenv("QCS_NO_TMA_ITER") != nullptr;  // A/B switch
-    // at most a few big boxes: many small ones (C5's scattered tiles: 32+ boxes of 1-2 KB) were
-    // slower than the per-thread cp.async tile (877 vs 819 ms per C5-family circuit at n=32)
-    static const int max_iter = [] { const char* v = std::getenv("QCS_TMA_MAX_ITER"); return v ? std::atoi(v) : 2; }();
-    int iter = 0;
+    const int iter = tile_tma_iter(n, p);
+    if (iter < 0) return false;
     u64 tile = 0;
-    for (int b = 0; b < p.m; ++b) tile |= u64(1) << p.bits[b];
-    while (dims(tile) > 5) {
-        if (no_iter || iter >= max_iter || p.m - iter - 1 < 6) return false;
-        tile &= ~(u64(1) << p.bits[p.m - 1 - iter]);
-        ++iter;
-    }
+    for (int b = 0; b < p.m - iter; ++b) tile |= u64(1) << p.bits[b];
     TmaDim L[16];
     int rank = tma_layout(tile, n, L, tma_gap_dims());
     if (rank > 5) return false;
@@ -351,6 +339,27 @@ bool tile_tensor_map(double2* amps, int n, PassParams& p, CUtensorMap* map) {
 }  // namespace
 
 int tile_max_bits() { return kMaxBits; }
+
+int tile_tma_iter(int n, const PassParams& p) {
+    if (!QCS_TILE_TMA || n > 36 || p.m < 3) return -1;
+    // the boxes cover the lowest m - iter local bits; the top `iter` ones are iterated (one box per
+    // value, contiguous in shared memory): the fewest iterated bits that bring the map to <= 5
+    // dims, with boxes of at least 64 amplitudes (1 KB)
+    auto dims = [&](u64 S) { return tma_layout(S, n, nullptr, tma_gap_dims()); };
+    static const bool no_iter = std::getenv("QCS_NO_TMA_ITER") != nullptr;  // A/B switch
+    // at most a few big boxes: many small ones (C5's scattered tiles: 32+ boxes of 1-2 KB) were
+    // slower than the per-thread cp.async tile (877 vs 819 ms per C5-family circuit at n=32)
+    static const int max_iter = [] { const char* v = std::getenv("QCS_TMA_MAX_ITER"); return v ? std::atoi(v) : 2; }();
+    int iter = 0;
+    u64 tile = 0;
+    for (int b = 0; b < p.m; ++b) tile |= u64(1) << p.bits[b];
+    while (dims(tile) > 5) {
+        if (no_iter || iter >= max_iter || p.m - iter - 1 < 6) return -1;
+        tile &= ~(u64(1) << p.bits[p.m - 1 - iter]);
+        ++iter;
+    }
+    return iter;
+}
 
 void tile_pass_shape(const PassParams& p, unsigned& f, unsigned& threads) {
     threads = unsigned(std::min(kThreads, std::max(32, 1 << (p.m - 3))));
