@@ -267,6 +267,14 @@ int qcs_plan_stats(int n, const qcs_step* steps, int num_steps, int engine, cons
  * Both forms compute bit-identical results; process-wide. */
 int qcs_set_jit_mode(int mode);
 int qcs_get_jit_mode(void);
+/* Which specialised pass kernels take the persistent pipelined form -- one CTA per SM walking its
+ * tiles through a ring of shared-memory slots, the HBM round trip of a tile hidden behind the
+ * arithmetic of its neighbours: 0 none, 1 passes with 16-amplitude register rounds (default), 2
+ * every eligible pass.  Initial value from QCS_PERSIST.  Same arithmetic in the same order as the
+ * one-tile-per-CTA form: bit-identical results; process-wide; plans already cached by a state
+ * keep their kernels.  B200-specific. */
+int qcs_set_pipeline_mode(int mode);
+int qcs_get_pipeline_mode(void);
 int qcs_plan_compile(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
                      int64_t* kernels, int64_t* cubin_bytes);
 /* Host-only addressing proof of that plan's specialised kernels (no compile): for every register

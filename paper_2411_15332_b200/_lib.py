@@ -101,6 +101,8 @@ SIGNATURES = {
                                  C.POINTER(qcs_plan_info)]),
     "qcs_set_jit_mode": (C.c_int, [C.c_int]),
     "qcs_get_jit_mode": (C.c_int, []),
+    "qcs_set_pipeline_mode": (C.c_int, [C.c_int]),
+    "qcs_get_pipeline_mode": (C.c_int, []),
     "qcs_plan_compile": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),
                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "qcs_plan_verify": (C.c_int, [C.c_int, C.POINTER(qcs_step), C.c_int, C.c_int, C.POINTER(qcs_sim_options),

@@ -476,6 +476,10 @@ int qcs_set_jit_mode(int mode) {
     return guarded([&] { qcs::set_jit_mode(mode); });
 }
 int qcs_get_jit_mode(void) { return qcs::jit_mode(); }
+int qcs_set_pipeline_mode(int mode) {
+    return guarded([&] { qcs::set_pipeline_mode(mode); });
+}
+int qcs_get_pipeline_mode(void) { return qcs::pipeline_mode(); }
 
 int qcs_plan_compile(int n, const qcs_step* steps, int num_steps, int engine, const qcs_sim_options* opts,
                      int64_t* kernels, int64_t* cubin_bytes) {

@@ -854,10 +854,8 @@ bool emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threa
 // support masks, tile lists, relabelled direct stores) whose tile moves as TMA boxes, with
 // enough tiles to fill the ring on every SM.  QCS_PERSIST: 0 off, 1 passes with 16-register
 // rounds (default: those run 2 CTAs per SM otherwise), 2 every eligible pass.
-int persist_knob() {
-    static const int v = [] { const char* e = std::getenv("QCS_PERSIST"); return e ? std::atoi(e) : 1; }();
-    return v;
-}
+std::atomic<int> g_persist{[] { const char* e = std::getenv("QCS_PERSIST"); return e ? std::atoi(e) : 1; }()};
+int persist_knob() { return g_persist.load(std::memory_order_relaxed); }
 constexpr unsigned kPersistThreads = 512, kPersistRing = 196608;  // two groups of 256; bytes of ring
 unsigned persist_slots(const PassParams& P) {
     static const int cap = [] { const char* e = std::getenv("QCS_PERSIST_SLOTS"); return e ? std::atoi(e) : 4; }();
@@ -1160,6 +1158,11 @@ std::atomic<int> g_mode{[] {
 }()};
 }  // namespace
 
+int pipeline_mode() { return persist_knob(); }
+void set_pipeline_mode(int mode) {
+    if (mode < 0 || mode > 2) raise(QCS_ERR_ARG, "pipeline mode must be 0, 1 or 2");
+    g_persist.store(mode);
+}
 int jit_mode() { return g_mode.load(std::memory_order_relaxed); }
 void set_jit_mode(int mode) {
     if (mode < 0 || mode > 3) raise(QCS_ERR_ARG, "jit mode must be 0, 1, 2 or 3");

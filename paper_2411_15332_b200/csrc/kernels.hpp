@@ -275,6 +275,9 @@ int jit_mode();                      // 0 off, 1 passes with enough work (defaul
 bool jit_pivot(int n, const struct PassParams& p);  // lower this pass's gates to the pivoted form
 bool jit_virtual(int n, int m, bool skip_pass);      // lower this pass's X-like gates to relabellings
 void set_jit_mode(int mode);
+// persistent pipelined pass kernels (jit.cpp): 0 off, 1 passes with 16-register rounds (default), 2 every eligible pass
+int pipeline_mode();
+void set_pipeline_mode(int mode);
 // NVRTC only (no device): cubin bytes; verify_only: generate with the addressing proof, no compile
 std::size_t jit_compile_only(const struct PassParams& p, bool verify_only = false);
 void tile_pass_shape(const struct PassParams& p, unsigned& F, unsigned& threads);  // kernel variant, CTA size

@@ -891,6 +891,10 @@ bool schedule_rounds(int n, const int* loc, int m, const std::vector<FOp>& ops, 
         }
         return gates;
     };
+    static const long bank_penalty = [] {
+        const char* v = std::getenv("QCS_BANK_PENALTY");  // in quarter gates
+        return long((v ? std::atof(v) : 0.0) * double(1L << 30));  // default off: C4 n=32 has 4 such rounds of 39, and avoiding them costs a round
+    }();
     while (int(order.size()) < N) {
         unsigned U = 0;  // bits with an unscheduled gate
         for (int i = 0; i < N; ++i)
@@ -915,6 +919,11 @@ bool schedule_rounds(int n, const int* loc, int m, const std::vector<FOp>& ops, 
             for (int i : pick) T |= 1u << bits[std::size_t(i)];
             long sc;
             closure(T, false, sc);
+            // register sets that hold local bits b and b + 3 (b < 3) leave no thread-index bit for
+            // bank-group bit b of the swizzled tile (position j ^ ((j >> 3) & 7)): every 16-byte
+            // access of the round is a 2-way bank conflict.  Cost: a fraction of a gate per pair.
+            for (int b = 0; b < 3; ++b)
+                if ((T >> b & 1u) && (T >> (b + 3) & 1u)) sc -= bank_penalty;
             if (sc > best) {
                 best = sc;
                 bestT = T;

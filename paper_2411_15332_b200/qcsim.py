@@ -683,6 +683,17 @@ def jit_mode() -> int:
     return int(L.lib().qcs_get_jit_mode())
 
 
+def set_pipeline_mode(mode: int) -> None:
+    """Which specialised pass kernels run in the persistent pipelined form (one CTA per SM, a ring
+    of TMA tile slots, two compute groups): 0 none, 1 passes with 16-amplitude register rounds
+    (default), 2 every eligible pass.  Bit-identical results.  B200-specific."""
+    _check(L.lib().qcs_set_pipeline_mode(int(mode)))
+
+
+def pipeline_mode() -> int:
+    return int(L.lib().qcs_get_pipeline_mode())
+
+
 def plan_compile(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOptions] = None) -> dict:
     """Generate and compile (NVRTC, host only) the specialised kernel of every tile pass of the
     plan of `c`.  B200-specific check/tool: {"kernels": passes compiled, "cubin_bytes": code size}."""

@@ -243,3 +243,47 @@ def test_default_mode_specialises_big_passes(Q, cfg):
     got, want = run_mode(Q, c, 1), run_mode(Q, c, 0)
     assert np.abs(got - want).max() <= TOL_AMP
     assert np.linalg.norm(got - want) <= TOL_L2
+
+
+# ---------------------------------------------------------------- persistent pipelined form
+def run_pipeline(Q, c, pmode):
+    old = Q.pipeline_mode()
+    Q.set_pipeline_mode(pmode)
+    try:
+        return Q.simulate(c, Q.Engine.rh_dax).final.download()  # a fresh state: a fresh plan cache
+    finally:
+        Q.set_pipeline_mode(old)
+
+
+def test_pipelined_sources_compile_and_address(Q, cfg):
+    """CPU: with every eligible pass in the persistent pipelined form (mode 2) the generated
+    sources still compile for sm_100a and pass the addressing proof; the plans are the same."""
+    old = Q.pipeline_mode()
+    try:
+        for mode in (0, 2):
+            Q.set_pipeline_mode(mode)
+            for c in (cfg.c4_circuit(24, 3), cfg.c3_circuit(24)):
+                st = Q.plan_stats(c)
+                assert Q.plan_compile(c)["kernels"] == st["tile_passes"]
+                assert Q.plan_verify(c) == st["tile_passes"]
+        with pytest.raises(ValueError):
+            Q.set_pipeline_mode(3)
+    finally:
+        Q.set_pipeline_mode(old)
+    assert Q.pipeline_mode() == old
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("family", ["c4", "c3", "random"])
+def test_pipelined_equals_one_tile_per_cta(Q, cfg, family):
+    """The persistent pipelined kernels (one CTA per SM, two compute groups over a ring of TMA
+    tile slots) run the same arithmetic in the same order as the one-tile-per-CTA kernels: the
+    states are bit-identical, for the default (16-register passes) and with every eligible pass
+    pipelined (8-register rounds, butterflies: short tiles, where a group that runs ahead of the
+    other's loads once read a slot that was not its own)."""
+    c = {"c4": lambda: cfg.c4_circuit(24, 4), "c3": lambda: cfg.c3_circuit(24),
+         "random": lambda: random_catalog_circuit(Q, 11, 23, 30)}[family]()
+    want = run_pipeline(Q, c, 0)
+    for pmode in (1, 2):
+        for rep in range(2):  # the first run is the cold one (compiles, first touch of the state)
+            assert bits_equal(run_pipeline(Q, c, pmode), want), (family, pmode, rep)
