@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -298,8 +300,19 @@ void plan_fused(int n, const std::vector<FOp>& ops, Lowered& low) {
 
 void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low) {
     if (n >= 3) {
-        lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
+        static const bool show = std::getenv("QCS_PLAN_TIME") != nullptr;  // host planning cost, per stage
+        const auto t0 = std::chrono::steady_clock::now();
+        Plan plan = plan_ops(n, ops, tile_max_bits());
+        const auto t1 = std::chrono::steady_clock::now();
+        lower_plan(n, ops, plan, low);
+        const auto t2 = std::chrono::steady_clock::now();
         jit_prepare(n, low.passes, low.pass_ops);
+        const auto t3 = std::chrono::steady_clock::now();
+        if (show)
+            std::fprintf(stderr, "plan_ops %.2f ms, lower_plan %.2f ms, jit_prepare %.2f ms\n",
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                         std::chrono::duration<double, std::milli>(t2 - t1).count(),
+                         std::chrono::duration<double, std::milli>(t3 - t2).count());
     } else {  // no 3-bit tile: one operation per pass
         for (std::size_t i = 0; i < ops.size(); ++i) {
             low.pass_ops.push_back({int(i)});
@@ -787,7 +800,17 @@ void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out, std:
         return;
     }
     Lowered low;
-    lower_plan(n, ops, plan_ops(n, ops, tile_max_bits()), low);
+    {
+        const auto t0 = std::chrono::steady_clock::now();
+        Plan plan = plan_ops(n, ops, tile_max_bits());
+        const auto t1 = std::chrono::steady_clock::now();
+        lower_plan(n, ops, plan, low);
+        const auto t2 = std::chrono::steady_clock::now();
+        if (std::getenv("QCS_PLAN_TIME"))
+            std::fprintf(stderr, "plan_ops %.2f ms, lower_plan %.2f ms\n",
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                         std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
     compute_reached(ops, low);
     apply_support(n, low, init);  // from |init> (opts->reset), as execute_fused runs the plan
     const bool dump = std::getenv("QCS_PLAN_DUMP") != nullptr;  // planner debugging: rounds and ops
