@@ -1125,7 +1125,8 @@ void lower_plan(int n, const std::vector<FOp>& ops_in, const Plan& plan, Lowered
             for (int idx : lists[pi]) {
                 const FOp& f = ops[std::size_t(idx)];
                 if (f.kind == TOP_SIGN || (f.kind == TOP_GATE && f.K >= 2)) ok = false;
-                if (f.kind == TOP_GATE && f.K == 1 && f.nrows == 2 && f.nnz[0] == 1 && f.nnz[1] == 1 && virt_pass) ok = false;
+                static const bool w4_perms = [] { const char* v = std::getenv("QCS_W4_PERMS"); return v && std::atoi(v) != 0; }();
+                if (f.kind == TOP_GATE && f.K == 1 && f.nrows == 2 && f.nnz[0] == 1 && f.nnz[1] == 1 && virt_pass && !w4_perms) ok = false;
             }
             // worth it only for passes with arithmetic to spare: a pass of a few butterflies is
             // HBM bound, and the 16-register kernels keep 2 tiles resident per SM instead of 3
