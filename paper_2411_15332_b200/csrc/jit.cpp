@@ -841,10 +841,7 @@ bool emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threa
             direct = emit_register_round(o, P, ri, threads, map, ri + 1 == end);
         }
     }
-    if (persist) {
-        if (direct) raise(QCS_ERR_SIM, "internal: a pipelined pass with direct stores");
-        return false;
-    }
+    if (persist) return direct;  // the caller emits the ring's write-back / refill
     if (!direct) o("  tile_end(a, P, tmap, c);\n");
     return direct;
 }
@@ -876,16 +873,19 @@ bool persist_wanted(const PassParams& P, unsigned F) {
     const int knob = persist_knob();
     if (knob <= 0 || P.m < 10 || P.m > 12) return false;
     if ((F & (4u | 8u)) || P.alt_mode != ALT_NONE || P.list_cnt || P.init || P.zmask || P.smask) return false;
-    if (has_direct_store(P)) return false;
     bool w4 = false;
     for (int r = 0; r < P.nrounds; ++r) {
         if (P.rounds[r].flags & RD_SMEM) return false;
         w4 |= (P.rounds[r].flags & RD_W4) != 0;
     }
-    if (knob == 1 && !w4) return false;
     const int n = pass_state_bits(P);
     if (n - P.m < 11) return false;  // >= 2048 tiles: several ring turns per SM
-    return tile_tma_iter(n, P) >= 0 && persist_slots(P) >= 3;
+    if (persist_slots(P) < 3) return false;
+    // the default: passes with 16-register rounds whose tile moves as TMA boxes and whose last
+    // round stores through shared memory; mode 2 adds 8-register passes, relabelled passes (direct
+    // stores) and tiles that load as per-thread cp.async copies
+    if (knob == 1) return w4 && !has_direct_store(P) && tile_tma_iter(n, P) >= 0;
+    return true;
 }
 
 std::string pass_source(const PassParams& P, unsigned F, unsigned threads, bool persist) {
@@ -906,7 +906,7 @@ std::string pass_source(const PassParams& P, unsigned F, unsigned threads, bool 
         o("         const u64* __restrict__ flipped, const u64* __restrict__ tables, const __grid_constant__ TmapParam tmap) {\n");
         o("  extern __shared__ __align__(1024) unsigned char smem_raw[];\n");
         o("  PersistCtx c;\n");
-        o("  persist_begin<%uu>(P, tables, tmap, smem_raw, c);\n", S);
+        o("  persist_begin<%uu>(a, P, tables, tmap, smem_raw, c);\n", S);
         o("  const u64* const hi_tab = c.hi_tab;\n");
         o("  const unsigned grp = threadIdx.x >> 8, t = threadIdx.x & 255u;\n");
         o("  const unsigned sign_hit = 0;\n  (void)sign_hit; (void)hi_tab; (void)big; (void)flipped; (void)a;\n");
@@ -916,11 +916,12 @@ std::string pass_source(const PassParams& P, unsigned F, unsigned threads, bool 
         o("  double2* const sm = c.sm0 + (slot << %d);\n", P.m);
         o("  const u64 base = tile_base_of(P, tile);\n");
         o("  mbar_wait(c.full + 2u * slot + (use & 1u), (use >> 1) & 1u);\n");
-        emit_rounds(o, P, 0, P.nrounds, 256, true);
-        o("  persist_end<%uu>(P, tmap, c, grp, t, tile, base, sm, c.full + 2u * slot + ((use + 1u) & 1u));\n", S);
+        const bool direct = emit_rounds(o, P, 0, P.nrounds, 256, true);
+        o("  persist_end<%uu, %s>(a, P, tmap, c, grp, t, tile, base, sm, c.full + 2u * slot + ((use + 1u) & 1u));\n", S,
+          direct ? "true" : "false");
         o("  slot += 2u;\n  if (slot >= %uu) { slot -= %uu; ++use; }\n", S, S);
         o("  }\n");
-        o("  if (t == 0) persist_finish();\n");
+        o("  persist_finish();\n");
         o("}\n");
         return o.s;
     }
@@ -1268,10 +1269,9 @@ bool launch_tile_pass_jit(double2* amps, const PassParams& p, unsigned F, const 
         // a plan the caller keeps remembers its kernel (no source generation on reuse)
         JitKernel& k = jit_slot && *jit_slot
                            ? *static_cast<JitKernel*>(*jit_slot)
-                           : compile(pass_source(p, F, threads, p.tma_rank > 0 && persist_wanted(p, F)));
+                           : compile(pass_source(p, F, threads, persist_wanted(p, F)));
         if (jit_slot) *jit_slot = &k;
         if (k.persist) {  // one CTA per SM, the ring of tile slots in its shared memory
-            if (p.tma_rank <= 0) raise(QCS_ERR_SIM, "internal: a pipelined pass kernel without a tensor map");
             static int sms[64] = {};
             if (dev < 64 && !sms[dev]) QCS_CUDA(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
             const unsigned nsm = unsigned(dev < 64 && sms[dev] > 0 ? sms[dev] : 148);

@@ -131,8 +131,9 @@ __device__ __forceinline__ void tma_box_coords(const PassParams& P, u64 base, un
         if (i >> k & 1) g |= u64(1) << P.bits[P.m - int(P.tma_iter) + k];
     for (int d = 0; d < 5; ++d) cc[d] = tma_coord(P, g, d);
 }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\nfence.mbarrier_init.release.cluster;\n" ::"r"(smem_u32(bar))
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count = 1u) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\nfence.mbarrier_init.release.cluster;\n" ::"r"(smem_u32(bar)),
+                 "r"(count)
                  : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
@@ -659,9 +660,20 @@ __device__ __forceinline__ void tile_store_read(const PassParams& P, const TmapP
     tma_store_commit_wait();
 }
 
+// all 256 threads of a group: the tile at `base` into `dst` as 16-byte cp.async copies (tiles whose
+// bit layout needs more than 5 tensor-map dims); each thread's arrival on `bar` (count 256)
+// fires when its copies have landed
+__device__ __forceinline__ void tile_load_coop(const PassParams& P, const double2* a, u64 base, double2* dst,
+                                               const u64* hi_tab, unsigned long long* bar, unsigned t) {
+    const unsigned sz = 1u << P.m;
+    const u64 gt = base | (t & 7u) | hi_tab[t >> 3];
+    for (unsigned j = t, k = 0; j < sz; j += 256u, k += 32u) cp_async16(dst + swz(j), a + (gt | hi_tab[k]));
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <unsigned S>
-__device__ __forceinline__ void persist_begin(const PassParams& P, const u64* tables, const TmapParam& tmap,
-                                              unsigned char* smem_raw, PersistCtx& c) {
+__device__ __forceinline__ void persist_begin(const double2* a, const PassParams& P, const u64* tables,
+                                              const TmapParam& tmap, unsigned char* smem_raw, PersistCtx& c) {
     const unsigned sz = 1u << P.m, ngroups = sz >> 3;
     const unsigned align_pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
     c.sm0 = reinterpret_cast<double2*>(smem_raw + align_pad);
@@ -672,33 +684,56 @@ __device__ __forceinline__ void persist_begin(const PassParams& P, const u64* ta
     c.ntiles = u64(1) << out_bits;
     const unsigned t = threadIdx.x, bt = blockDim.x;
     for (unsigned j = 2 * t; j < ngroups; j += 2 * bt) cp_async16(c.hi_tab + j, tables + P.hi_off + j);
-    if (t == 0) {
-        for (unsigned s = 0; s < 2 * S; ++s) mbar_init(c.full + s);
-        for (unsigned s = 0; s < S; ++s) {
-            const u64 tile = blockIdx.x + u64(s) * gridDim.x;
-            if (tile < c.ntiles) tile_load_async(P, tmap, tile_base_of(P, tile), c.sm0 + s * sz, c.full + 2 * s);
-        }
-    }
+    if (t == 0)
+        for (unsigned s = 0; s < 2 * S; ++s) mbar_init(c.full + s, P.tma_rank ? 1u : 256u);
     cp_async_wait_all();
     __syncthreads();
+    if (P.tma_rank) {
+        if (t == 0)
+            for (unsigned s = 0; s < S; ++s) {
+                const u64 tile = blockIdx.x + u64(s) * gridDim.x;
+                if (tile < c.ntiles) tile_load_async(P, tmap, tile_base_of(P, tile), c.sm0 + s * sz, c.full + 2 * s);
+            }
+    } else {  // the group that will compute slot s's first tile loads it
+        for (unsigned s = t >> 8; s < S; s += 2) {
+            const u64 tile = blockIdx.x + u64(s) * gridDim.x;
+            if (tile < c.ntiles)
+                tile_load_coop(P, a, tile_base_of(P, tile), c.sm0 + s * sz, c.hi_tab, c.full + 2 * s, t & 255u);
+        }
+    }
 }
 
 // after the group's last round on the CTA's k-th tile (in `sm`): write it back and refill the slot
-// (bar: the barrier of the slot's NEXT use)
-template <unsigned S>
-__device__ __forceinline__ void persist_end(const PassParams& P, const TmapParam& tmap, const PersistCtx& c, unsigned grp,
-                                            unsigned t, u64 tile, u64 base, double2* sm, unsigned long long* bar) {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    group_sync(grp);
-    if (t == 0) {
-        tile_store_read(P, tmap, base, sm);
-        const u64 next = tile + u64(S) * gridDim.x;
-        if (next < c.ntiles) tile_load_async(P, tmap, tile_base_of(P, next), sm, bar);
+// (bar: the barrier of the slot's NEXT use).  DIRECT: the last round stored its registers
+// straight to HBM (relabelled passes), so the slot is free once the group has passed its barrier.
+template <unsigned S, bool DIRECT>
+__device__ __forceinline__ void persist_end(double2* a, const PassParams& P, const TmapParam& tmap, const PersistCtx& c,
+                                            unsigned grp, unsigned t, u64 tile, u64 base, double2* sm,
+                                            unsigned long long* bar) {
+    const u64 next = tile + u64(S) * gridDim.x;
+    if (P.tma_rank) {
+        if (!DIRECT) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        group_sync(grp);
+        if (t == 0) {
+            if (!DIRECT) tile_store_read(P, tmap, base, sm);
+            if (next < c.ntiles) tile_load_async(P, tmap, tile_base_of(P, next), sm, bar);
+        }
+    } else {
+        if (!DIRECT) {  // (the last round ended with the group's barrier)
+            const unsigned sz = 1u << P.m;
+            const u64 gt = base | (t & 7u) | c.hi_tab[t >> 3];
+            for (unsigned j = t, k = 0; j < sz; j += 256u, k += 32u) __stcs(a + (gt | c.hi_tab[k]), sm[swz(j)]);
+        }
+        group_sync(grp);
+        if (next < c.ntiles) tile_load_coop(P, a, tile_base_of(P, next), sm, c.hi_tab, bar, t);
     }
 }
 // before the CTA exits: every store this thread issued has read its slot (persist_end waits per
-// store, so this only documents the invariant)
-__device__ __forceinline__ void persist_finish() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+// store, so this only documents the invariant), and no cp.async of its own is in flight
+__device__ __forceinline__ void persist_finish() {
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    cp_async_wait_all();
+}
 
 }  // namespace tile
 }  // namespace qcs
