@@ -367,6 +367,39 @@ def test_reductions(Q, oracle):
     assert abs(s.norm() - 1) < 1e-12
 
 
+@pytest.mark.parametrize("n", [1, 3, 5, 9, 13, 21])
+def test_topk_ties_and_sizes(Q, n):
+    """top-k against a stable sort (ties to the lower index, as std::max_element): states with
+    many equal probabilities (a uniform superposition with a few raised entries, basis states,
+    fewer than k nonzero entries), every k, from 2 amplitudes up to more than one batch per warp."""
+    dim = 1 << n
+    rng = np.random.default_rng(n)
+    cases = [np.full(dim, 1.0 / np.sqrt(dim), np.complex128)]
+    x = cases[0].copy()
+    for j in rng.choice(dim, min(dim, 5), replace=False):
+        x[j] *= 1.5
+    cases.append(x)
+    b = np.zeros(dim, np.complex128)
+    b[dim - 1] = 1.0
+    cases.append(b)
+    q = rng.integers(0, 4, dim).astype(np.float64) + 1j * rng.integers(0, 4, dim)  # heavy ties
+    cases.append(q.astype(np.complex128))
+    cases.append(random_state(n, 40 + n))
+    for x in cases:
+        s = Q.DeviceState.from_numpy(x)
+        p = x.real * x.real + x.imag * x.imag
+        order = np.argsort(-p, kind="stable")
+        for k in (1, 2, 7, 16):
+            idx, pr = s.topk(k)
+            m = min(k, dim)
+            assert [int(v) for v in idx[:m]] == [int(v) for v in order[:m]], (n, k)
+            assert list(pr[:m]) == [p[v] for v in order[:m]]
+        nrm, idx, pr = s.summary(16)
+        assert abs(nrm - np.sqrt(p.sum())) <= 1e-12 * max(1.0, np.sqrt(p.sum()))
+        m = min(16, dim)
+        assert [int(v) for v in idx[:m]] == [int(v) for v in order[:m]]
+
+
 @pytest.mark.slow
 def test_c2_full_size_properties(Q, cfg):
     """n = 28 (BASELINE C2 size): norm preservation and X/H involutions on the device."""
