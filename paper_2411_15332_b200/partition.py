@@ -411,10 +411,10 @@ class ShardedState:
         self.phys[qa], self.phys[qb] = pb, pa
 
     def _bring_local(self, need: List[int], protect: set, upcoming: List[set]) -> None:
-        """Remap the logical qubits `need` (global now) to local positions g..g+k-1.  A logical
-        qubit there that the waiting operations use (`protect`) first moves to a free local
-        position by a local Swap; the free position chosen is the one whose qubit is used
-        latest among `upcoming` (the remaining operations' qubit sets)."""
+        """Remap the logical qubits `need` (global now) to local positions g..g+k-1.  The local
+        qubits that become global in exchange are the ones used latest among `upcoming` (the
+        remaining operations' qubit sets) and not by the waiting operations (`protect`); each is
+        first brought to a top local position by a local Swap."""
         k = min(len(need), self.g, self.n - self.g)
         need = need[:k]
         free = [pp for pp in range(self.g + k, self.n) if self.phys.index(pp) not in protect]
@@ -422,23 +422,33 @@ class ShardedState:
         if len(free) < len(clash):
             raise RuntimeError("no free local qubit to make room for a remap")
         inv = {p: q for q, p in enumerate(self.phys)}
-        for i in range(k):
-            p = self.g + i
-            if inv[p] not in protect:
-                continue
-            taken = set(range(self.g, self.g + k))
-            cands = [pp for pp in range(self.g + k, self.n) if inv[pp] not in protect]
-            if not cands:
-                raise RuntimeError("no free local qubit to make room for a remap")
 
-            def next_use(pp):
-                q = inv[pp]
-                for t, qs in enumerate(upcoming):
-                    if q in qs:
-                        return t
-                return len(upcoming)
-            best = max(cands, key=next_use)
-            assert best not in taken
+        def next_use(pp):
+            q = inv[pp]
+            for t, qs in enumerate(upcoming):
+                if q in qs:
+                    return t
+            return len(upcoming)
+        # The k local qubits that trade places with the incoming ones become global: pick the
+        # ones used latest among the remaining operations (never again, if there are such --
+        # a layered circuit's cone leaves qubits far from the global ones finished), not whichever
+        # sit at the top local positions.  Evicting a qubit the next layer needs costs a remap
+        # per layer (C4 at n=32 on 2 ranks: 10 remaps, 5 shards on the wire, 18 passes); evicting
+        # finished ones costs one (0.5 shards, 11 passes).  A local Swap (fused into the pending
+        # batch) brings each chosen qubit to a top position first.
+        cands = [pp for pp in range(self.g, self.n) if inv[pp] not in protect]
+        victims = sorted(cands, key=lambda pp: (-next_use(pp), pp))[:k]
+        slots = [self.g + i for i in range(k)]
+        stay = [pp for pp in slots if pp in victims]          # already in place
+        move = [pp for pp in victims if pp not in slots]       # to be swapped up
+        for p in slots:
+            if p in stay:
+                continue
+            if not move:
+                if inv[p] in protect:
+                    raise RuntimeError("no free local qubit to make room for a remap")
+                continue
+            best = move.pop(0)
             self._local_swap(p, best)
             inv = {pp: q for q, pp in enumerate(self.phys)}
         self._remap([self.phys[q] for q in need])

@@ -99,6 +99,50 @@ def test_c4_one_batched_remap_per_layer(oracle, world, layers):
         assert s["bytes_sent"] <= s["remaps"] * shard * (world - 1) // world
 
 
+class _ScheduleOnlyBackend:
+    """No amplitudes: records the local batches the scheduler hands over."""
+
+    def __init__(self, n_local):
+        self.n = n_local
+        self.batches = []
+
+    def set_basis(self, index):
+        pass
+
+    def run(self, ops):
+        self.batches.append(len(ops))
+
+    def sync(self):
+        pass
+
+
+class _CountingTransport:
+    def swap_blocks(self, backend, k, pairs, chunk):
+        pass
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c4_n32_schedule_one_remap(world):
+    """BASELINE configs[3] sharded (host only, no amplitudes): the cone the scheduler runs before
+    its first exchange leaves the ring qubits far from the global ones finished, and the remap
+    evicts THOSE (latest next use), so the whole 10-layer circuit costs one remap -- (2^g - 1)/2^g
+    of a shard on the wire -- and two local batches.  (Evicting the top local qubits, which the
+    next layer needs, cost 10 remaps and 5 / 7 / 7.9 shards at 2 / 4 / 8 ranks.)"""
+    from paper_2411_15332_b200 import configs
+    from paper_2411_15332_b200.partition import ShardedState
+    c = configs.c4_circuit(32)
+    g = world.bit_length() - 1
+    be = _ScheduleOnlyBackend(c.n - g)
+    st = ShardedState(c.n, world, 0, be, _CountingTransport(), initial=c.initial)
+    st.run(circuit_ops(c))
+    st.flush()
+    s = st.exchange_stats()
+    shard = 16 << (c.n - g)
+    assert s["remaps"] == 1 and s["qubits"] == g
+    assert s["bytes_sent"] == shard * (world - 1) // world
+    assert len(be.batches) == 2 and sum(be.batches) <= 992 + 32 + g  # the gates (H^n as 32) + the local swaps
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("name", ["c4", "c5", "grover"])
 def test_threads_peer_remap_match_full_state(oracle, world, name):
