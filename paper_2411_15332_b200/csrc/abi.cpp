@@ -370,8 +370,13 @@ int qcs_topk(qcs_state* s, int k, uint64_t* indices, double* probabilities) {
         need(s, "state");
         need(indices, "indices");
         need(probabilities, "probabilities");
+        if (k < 1 || k > 16) qcs::raise(QCS_ERR_ARG, "top-k supports 1 <= k <= 16");
+        if (s->summary_k) qcs::raise(QCS_ERR_ARG, "a summary of this state is pending");
         qcs::DeviceGuard g(s->device);
-        qcs::topk(s->amps, uint64_t(1) << s->n, k, indices, probabilities, s->stream);
+        if (!s->summary_host) QCS_CUDA(cudaHostAlloc(&s->summary_host, qcs::topk_host_bytes(16), cudaHostAllocDefault));
+        qcs::topk_begin(s->amps, uint64_t(1) << s->n, k, false, s->summary_host, s->stream);
+        QCS_CUDA(cudaStreamSynchronize(s->stream));
+        qcs::topk_finish(s->summary_host, k, false, indices, probabilities, nullptr);
     });
 }
 
@@ -381,8 +386,15 @@ int qcs_summary(qcs_state* s, int k, double* norm, uint64_t* indices, double* pr
         need(norm, "norm");
         need(indices, "indices");
         need(probabilities, "probabilities");
+        if (k < 1 || k > 16) qcs::raise(QCS_ERR_ARG, "top-k supports 1 <= k <= 16");
+        if (s->summary_k) qcs::raise(QCS_ERR_ARG, "a summary of this state is already pending");
         qcs::DeviceGuard g(s->device);
-        qcs::topk(s->amps, uint64_t(1) << s->n, k, indices, probabilities, s->stream, norm);
+        // the block candidates land in the state's pinned buffer (a pageable destination makes the
+        // copy a staged, synchronous one: ~0.4 ms per call, more than a small circuit's passes)
+        if (!s->summary_host) QCS_CUDA(cudaHostAlloc(&s->summary_host, qcs::topk_host_bytes(16), cudaHostAllocDefault));
+        qcs::topk_begin(s->amps, uint64_t(1) << s->n, k, true, s->summary_host, s->stream);
+        QCS_CUDA(cudaStreamSynchronize(s->stream));
+        qcs::topk_finish(s->summary_host, k, true, indices, probabilities, norm);
     });
 }
 

@@ -265,6 +265,11 @@ __global__ void __launch_bounds__(256, 2) k_topk_partial(const double2* __restri
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     ArgMax* const wb = buf[w];
     const ArgMax none{-1.0, ~u64(0)};
+    if (u64(blockIdx.x) * blockDim.x >= dim) {  // small states: this block has no element
+        if (threadIdx.x < unsigned(k)) out[u64(blockIdx.x) * k + threadIdx.x] = none;
+        if (psum && threadIdx.x == 0) psum[blockIdx.x] = 0.0;
+        return;
+    }
     unsigned cnt = 0;   // warp-uniform
     ArgMax tau = none;  // warp-uniform
     double acc = 0.0;

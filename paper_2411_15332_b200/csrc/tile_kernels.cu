@@ -338,7 +338,15 @@ bool tile_tensor_map(double2* amps, int n, PassParams& p, CUtensorMap* map) {
 
 }  // namespace
 
-int tile_max_bits() { return kMaxBits; }
+int tile_max_bits() {
+    // QCS_TILE_MAX_BITS (<= the compiled limit): smaller tiles for experiments (planner A/B)
+    static const int bits = [] {
+        const char* v = std::getenv("QCS_TILE_MAX_BITS");
+        const int b = v ? std::atoi(v) : kMaxBits;
+        return b >= 6 && b <= kMaxBits ? b : kMaxBits;
+    }();
+    return bits;
+}
 
 int tile_tma_iter(int n, const PassParams& p) {
     if (!QCS_TILE_TMA || n > 36 || p.m < 3) return -1;

@@ -10,7 +10,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 st = Q.DeviceState(n)
 st.randomize(7)
 st.sync()
-for name, fn in (("norm", st.norm), ("argmax", st.argmax), ("summary(16)", lambda: st.summary(16)), ("topk(16)", lambda: st.topk(16))):
+for name, fn in (("norm", st.norm), ("argmax", st.argmax), ("summary(16)", lambda: st.summary(16)), ("topk(16)", lambda: st.topk(16)),
+                 ("sample(16)", lambda: st.sample(16, 5)), ("sample(4096)", lambda: st.sample(4096, 5))):
     fn()
     t0 = time.perf_counter()
     for _ in range(3):
