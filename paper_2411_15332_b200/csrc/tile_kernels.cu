@@ -323,8 +323,18 @@ bool tile_tensor_map(double2* amps, int n, PassParams& p, CUtensorMap* map) {
         gstride[0] = 128;
         rank = 2;
     }
+    // L2 promotion 128 B: a 256-byte promotion on a tile whose contiguous runs are 128 bytes fetches
+    // the neighbouring tile's 128 bytes as well and counts on that tile's own load hitting them in
+    // L2; under the persistent kernels' looser tile order that cost 3-9% extra DRAM traffic on the
+    // HBM-bound C4 passes (C4 n=32: 241.0 ms with 256 B, 239.0 ms with 128 B or none; C3 / C5
+    // unchanged; tools/gpu_r02av.sh).  QCS_TMA_L2PROMO = 0 / 128 / 256 overrides.
+    static const int promo_env = [] { const char* v = std::getenv("QCS_TMA_L2PROMO"); return v ? std::atoi(v) : -1; }();
+    const int promo = promo_env >= 0 ? promo_env : 128;
+    const CUtensorMapL2promotion l2p = promo == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                       : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                      : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     if (encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(rank), amps, gdim, gstride, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2p,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     p.tma_rank = rank;
