@@ -279,7 +279,7 @@ void split_phases(std::vector<FOp>& ops) {
 namespace {
 // One greedy plan.  strict_dims: the tile search counts tensor-map dims the round-1 way (a dim per
 // gap between tile runs as well) when it prefers tiles that move as one TMA box.
-Plan plan_ops_policy(int n, const std::vector<FOp>& ops, int max_bits, bool strict_dims) {
+Plan plan_ops_policy(int n, const std::vector<FOp>& ops, int max_bits, bool strict_dims, std::size_t max_starts) {
     Plan plan;
     const int M = std::min(max_bits, n);
     static const bool no_seed = knob("QCS_NO_TILE_SEARCH");  // A/B switch
@@ -377,7 +377,7 @@ Plan plan_ops_policy(int n, const std::vector<FOp>& ops, int max_bits, bool stri
             u64 low = 0;
             for (int b = 0; b < std::min(3, n); ++b) low |= u64(1) << b;
             std::vector<std::size_t> starts;
-            for (std::size_t p = 0; p < remaining.size() && starts.size() < 48; ++p)
+            for (std::size_t p = 0; p < remaining.size() && starts.size() < max_starts; ++p)
                 if (!elementwise(ops[std::size_t(remaining[p])])) starts.push_back(p);
             for (std::size_t st : starts) {
                 u64 seed = low;
@@ -422,17 +422,29 @@ Plan plan_ops_policy(int n, const std::vector<FOp>& ops, int max_bits, bool stri
 // kernels' own count).  C4 n=32: 9 passes under the kernels' count alone, 8 under the strict one.
 Plan plan_ops(int n, const std::vector<FOp>& ops, int max_bits) {
     static const bool one_policy = knob("QCS_PLAN_ONE_POLICY") || knob("QCS_NO_TILE_SEARCH");  // A/B switch
-    Plan a = plan_ops_policy(n, ops, max_bits, false);
-    if (one_policy || tma_gap_dims() || a.passes.size() < 3) return a;
-    Plan b = plan_ops_policy(n, ops, max_bits, true);
+    static const std::size_t seeds = [] { const char* v = std::getenv("QCS_TILE_SEEDS"); return std::size_t(v ? std::atoi(v) : 48); }();
+    static const std::size_t deep_seeds = [] { const char* v = std::getenv("QCS_TILE_DEEP_SEEDS"); return std::size_t(v ? std::atoi(v) : 400); }();
+    Plan best = plan_ops_policy(n, ops, max_bits, false, seeds);
+    if (one_policy || tma_gap_dims() || best.passes.size() < 3) return best;
     auto non_tma = [&](const Plan& p) {
         int c = 0;
         for (const auto& q : p.passes) c += tma_layout(q.tile, n, nullptr, false) > 5;
         return c;
     };
-    if (b.passes.size() < a.passes.size()) return b;
-    if (b.passes.size() == a.passes.size() && non_tma(b) < non_tma(a)) return b;
-    return a;
+    auto consider = [&](Plan&& b) {
+        if (b.passes.size() < best.passes.size() ||
+            (b.passes.size() == best.passes.size() && non_tma(b) < non_tma(best)))
+            best = std::move(b);
+    };
+    consider(plan_ops_policy(n, ops, max_bits, true, seeds));
+    // Plans of many passes over big states (the C5 family: scattered CNOT pairs) also try a wider
+    // seed window: a pass saved is ~30 ms at n=32, the wider search ~15 ms of planning (C5 family
+    // n=32: 25 -> 23 passes; C4's 8-pass plans are left alone -- the wider window finds 9).
+    if (n >= 26 && best.passes.size() >= 12 && deep_seeds > seeds) {
+        consider(plan_ops_policy(n, ops, max_bits, false, deep_seeds));
+        consider(plan_ops_policy(n, ops, max_bits, true, deep_seeds));
+    }
+    return best;
 }
 
 // The program a pass runs on tiles that none of its sign steps' listed indices fall in: each
