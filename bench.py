@@ -427,7 +427,7 @@ def run_single(args):
 
     # e2e: fresh angles every step (plan-cache miss, same kernel structure), host-side circuit in,
     # render_report's numbers out (norm, argmax, top-16) into host memory
-    e2e_steps = max(2, args.steps)
+    e2e_steps = max(8, args.steps)  # its own count (reported in e2e.steps): amortises the pipeline's fill and drain
     circuits = [builders[w](seed + 1000 + i) for i in range(e2e_steps)] if w != "c3" else [c] * e2e_steps
     h2d = sum(circuit_bytes(ci) for ci in circuits) // e2e_steps
     Q.simulate(circuits[0], Q.Engine.rh_dax, state=state)  # not timed: the first fresh-angle plan

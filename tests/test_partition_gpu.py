@@ -124,3 +124,26 @@ def test_split_gate_bit_exact():
         got = gather([o[0] for o in outs], [o[1] for o in outs])
         assert all(o[0].splits == 1 and o[0].swaps == 0 for o in outs), gate.name
         assert bits_equal(got, want), gate.name
+
+
+def test_nccl_transport_self_exchange():
+    """The NCCL transport (DistTransport.swap_blocks / .exchange on CUDA tensors) run for real at
+    world size 1, the partner being the rank itself (tools/nccl_self_exchange.py): the chunked,
+    double-buffered send/recv path a multi-GPU run takes, which needs no second GPU to execute.
+    In a subprocess with a time limit (a process group per test process; an NCCL build that
+    cannot send to self would hang rather than fail)."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    try:
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "nccl_self_exchange.py"), str(port)],
+                             capture_output=True, text=True, timeout=240, cwd=ROOT)
+    except subprocess.TimeoutExpired:
+        pytest.skip("NCCL send/recv to self did not complete on this box")
+    assert out.returncode == 0 and "nccl self exchange ok" in out.stdout, out.stderr[-2000:]
