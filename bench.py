@@ -65,11 +65,12 @@ def dist_env():
 class Dist:
     """torch.distributed plumbing for N > 1 (barrier + max over ranks); inert at N = 1."""
 
-    def __init__(self, world, local_rank, backend="nccl"):
+    def __init__(self, world, local_rank, backend="nccl", force=False):
         self.world = world
         self.backend = backend
         self.init_lines = []
-        if world > 1:
+        self.active = world > 1 or force  # force: a process group at world size 1 (--sharded on one GPU)
+        if self.active:
             import torch
             import torch.distributed as dist
             if backend == "nccl":
@@ -85,11 +86,11 @@ class Dist:
             self.torch = torch
 
     def barrier(self):
-        if self.world > 1:
+        if self.active:
             self.dist.barrier()
 
     def max(self, v: float) -> float:
-        if self.world == 1:
+        if not self.active:
             return v
         dev = "cuda" if self.backend == "nccl" else "cpu"
         t = self.torch.tensor([v], dtype=self.torch.float64, device=dev)
@@ -97,7 +98,7 @@ class Dist:
         return float(t.item())
 
     def close(self):
-        if self.world > 1:
+        if self.active:
             self.dist.destroy_process_group()
 
 
@@ -582,7 +583,7 @@ def run_sharded(args, rank, world, local_rank):
     from paper_2411_15332_b200 import configs
     from paper_2411_15332_b200.partition import DistTransport, ShardedState, circuit_ops
     dry = args.dry_run
-    dist = Dist(world, local_rank, "gloo" if dry else "nccl")
+    dist = Dist(world, local_rank, "gloo" if dry else "nccl", force=True)
     w = args.workload if args.workload in ("c4", "c5", "c3") else "c4"
     n = args.n_circuit or {"c3": 30, "c4": 32, "c5": 35}[w]
     c = {"c3": lambda: configs.c3_circuit(n), "c4": lambda: configs.c4_circuit(n),
@@ -646,6 +647,8 @@ def run_sharded(args, rank, world, local_rank):
     norms = []
     for _ in range(args.steps):
         step()
+        if not dry:
+            backend._materialise()  # (a shard still at its deferred reset)
         norms.append(float(torch.linalg.vector_norm(backend.tensor).item()) if not dry else 0.0)
     e2e_ms = dist.max(1e3 * (time.perf_counter() - t0))
     if not dry:
@@ -714,6 +717,10 @@ def main():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--peer", action="store_true",
                     help="N > 1: remaps through the peer-memory swap kernel (torch symmetric memory) instead of NCCL")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded arm (the N > 1 code path: NCCL process group, DeviceBackend over a torch "
+                         "tensor, ShardedState scheduler, exchange accounting) even at one rank, e.g. under "
+                         "torchrun --nproc-per-node 1: checks that path on a one-GPU box")
     ap.add_argument("--dry-run", action="store_true",
                     help="N > 1 on a CPU host (gloo): exchanges only, no compute -- tests the launcher path")
     args = ap.parse_args()
@@ -727,7 +734,7 @@ def main():
         return bench_modes.rh_signs(args)
     if args.workload == "c2":
         return run_c2(args, rank, world, local_rank)
-    if world > 1:
+    if world > 1 or args.sharded:
         return run_sharded(args, rank, world, local_rank)
     return run_single(args)
 

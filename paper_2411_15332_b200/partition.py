@@ -77,26 +77,50 @@ class DeviceBackend:
         self.device = device
         if symmetric:  # peer-mappable (torch symmetric memory): SymmetricTransport rendezvous
             import torch.distributed._symmetric_memory as symm_mem
-            self.tensor = symm_mem.empty(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}")
-            self.tensor.zero_()
+            self._tensor = symm_mem.empty(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}")
+            self._tensor.zero_()
         else:
-            self.tensor = torch.zeros(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}")
+            self._tensor = torch.zeros(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}")
         stream = torch.cuda.current_stream(device).cuda_stream
         import ctypes as C
         h = C.c_void_p()
-        Q._check(Q.L.lib().qcs_state_wrap(n_local, device, C.c_void_p(self.tensor.data_ptr()), C.c_void_p(stream),
+        Q._check(Q.L.lib().qcs_state_wrap(n_local, device, C.c_void_p(self._tensor.data_ptr()), C.c_void_p(stream),
                                           C.byref(h)))
         self.state = Q.DeviceState(n_local, 0, device, _handle=h)
 
+    @property
+    def tensor(self):
+        """The shard as a torch tensor, for readers and writers outside this class: a deferred
+        reset is written first, and the shard's content is no longer taken as known."""
+        self._materialise()
+        self.known = None
+        return self._tensor
+
     def set_basis(self, index: Optional[int]) -> None:
-        self.tensor.zero_()
-        if index is not None:
-            self.tensor[index] = 1.0
+        # what the shard holds, until something else writes it: the next batch starts from it.
+        # The memory is written only when someone needs it (_materialise): a batch that starts
+        # from a basis state folds the reset into its first pass and never reads the old content.
+        self.known = "zero" if index is None else int(index)
+        self.stale = True
+
+    def _materialise(self) -> None:
+        if getattr(self, "stale", False):
+            self.stale = False
+            self._tensor.zero_()
+            if isinstance(self.known, int):
+                self._tensor[self.known] = 1.0
 
     def run(self, ops) -> None:
         """Apply a batch of local operations with one fused qcs_simulate call.  A run of
-        Hadamards covering every local qubit becomes the RH step (butterflies, one scale)."""
+        Hadamards covering every local qubit becomes the RH step (butterflies, one scale).
+        A shard known to be a basis state runs the batch with the reset folded in (the passes
+        skip the tiles outside the support reached so far, as the single-GPU simulate does); a
+        shard known to be all zeros stays all zeros under these linear operations: nothing runs."""
         Q = self.Q
+        known, self.known = getattr(self, "known", None), None
+        if known == "zero":
+            self.known = "zero"
+            return
         steps = []
         hs = []
 
@@ -122,33 +146,47 @@ class DeviceBackend:
         if hs:
             flush_h()
         if steps:
-            Q.run(Q.Circuit(self.n, steps), self.state, Q.Engine.rh_dax)
+            if isinstance(known, int):
+                self.stale = False  # the run writes |known> itself
+            else:
+                self._materialise()
+            Q.run(Q.Circuit(self.n, steps), self.state, Q.Engine.rh_dax,
+                  reset_index=known if isinstance(known, int) else None)
+        else:
+            self.known = known
 
     def apply_split(self, peer, self_bit: int, sel_bits: Sequence[int], blocks: np.ndarray, skip: int) -> None:
         """A gate on a global qubit, fused with the exchange: `peer` is the partner shard
         (a tensor in this device's address space)."""
+        self._materialise()
+        self.known = None
         self.state.apply_split(peer.data_ptr(), self_bit, sel_bits, blocks, skip)
 
     def swap_peer(self, offset: int, peer_block, count: int) -> None:
         """Swap this shard's [offset, offset+count) with `peer_block` (qcs_swap_peer)."""
         Q = self.Q
         import ctypes as C
+        self._materialise()
+        self.known = None
         Q._check(Q.L.lib().qcs_swap_peer(self.state.handle, offset, C.c_void_p(peer_block.data_ptr()), count))
 
     def block(self, k: int, j: int, start: int, count: int):
         """Elements [start, start+count) of block j of 2^k (by the top k local bits)."""
         b = (1 << (self.n - k)) * j + start
-        return self.tensor[b: b + count]
+        self._materialise()
+        self.known = None  # a view the transports write through
+        return self._tensor[b: b + count]
 
     def empty(self, count: int):
-        return self.torch.empty(count, dtype=self.torch.complex128, device=self.tensor.device)
+        return self.torch.empty(count, dtype=self.torch.complex128, device=self._tensor.device)
 
     def sync(self) -> None:
+        self._materialise()
         self.torch.cuda.synchronize(self.device)
 
     def numpy(self) -> np.ndarray:
         self.sync()
-        return self.tensor.cpu().numpy()
+        return self._tensor.cpu().numpy()
 
 
 class DistTransport:
@@ -238,6 +276,8 @@ def swap_blocks_peer(transport, backend, k: int, pairs, rank: int) -> None:
     block pair and the higher rank the second half (qcs_swap_peer), between two barriers."""
     size = 1 << (backend.n - k)
     h = size // 2
+    if hasattr(backend, "_materialise"):
+        backend._materialise()  # a deferred reset is written before the partners may read the shard
     transport.barrier()  # every partner's earlier work on its shard is done
     for peer, mine, theirs in pairs:
         lo, cnt = (0, h) if rank < peer else (h, size - h)
@@ -583,6 +623,8 @@ class ShardedState:
         # every rank takes part in both barriers (they are world-wide); a rank pair whose blocks
         # are all the identity (a global control that is off) launches nothing
         self.flush()
+        if hasattr(self.backend, "_materialise"):
+            self.backend._materialise()  # a deferred reset is written before the partner reads the shard
         self.transport.barrier()  # the partner's earlier work on its shard is done
         if skip != (1 << nb) - 1:
             self.backend.apply_split(self.transport.peer_buffer(self.rank ^ (1 << (self.g - 1 - phys[ig]))),

@@ -626,15 +626,19 @@ def simulate(c: Circuit, engine: Engine = Engine.rh_dax, opts: Optional[SimOptio
     return SimReport(state, steps, sum(s.sign_count for s in steps) & mask, sum(s.madd_count for s in steps) & mask)
 
 
-def run(c: Circuit, state: DeviceState, engine: Engine = Engine.rh_dax, opts: Optional[SimOptions] = None
-        ) -> List[StepReport]:
+def run(c: Circuit, state: DeviceState, engine: Engine = Engine.rh_dax, opts: Optional[SimOptions] = None,
+        reset_index: Optional[int] = None) -> List[StepReport]:
     """Apply the circuit's steps to `state` as it is (no reset to |initial>): the in-place form
-    of simulate used by the partitioner between exchanges."""
+    of simulate used by the partitioner between exchanges.  reset_index: the state is to start
+    from the basis state |reset_index> (qcs_sim_options.reset: folded into the first pass, and
+    the passes skip the tiles outside the support reached so far)."""
     opts = opts or SimOptions()
     if state.n != c.n:
         raise DimensionError("state qubit count mismatch")
     arr, keep = _steps(c.steps)
     o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)))
+    if reset_index is not None:
+        o = L.qcs_sim_options(int(opts.sign_method), int(opts.block_size), int(bool(opts.fuse)), 1, int(reset_index))
     rep = (L.qcs_step_report * max(1, len(c.steps)))()
     _check(L.lib().qcs_simulate(state.handle, arr, len(c.steps), int(engine), C.byref(o), rep))
     return _reports(rep, len(c.steps))

@@ -147,3 +147,53 @@ def test_nccl_transport_self_exchange():
     except subprocess.TimeoutExpired:
         pytest.skip("NCCL send/recv to self did not complete on this box")
     assert out.returncode == 0 and "nccl self exchange ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_world1_sharded_equals_simulate_and_defers_the_reset():
+    """One rank: the sharded path hands the whole circuit to the fused engine with the reset
+    folded in (the shard is known to be |initial>, its memory untouched until the run writes it),
+    so the result is bit for bit simulate's; a reader of the shard's tensor in between sees the
+    basis state (the deferred reset is written first)."""
+    from conftest import bits_equal
+    from paper_2411_15332_b200 import configs
+    from paper_2411_15332_b200 import qcsim as Q
+    from paper_2411_15332_b200.partition import DeviceBackend, ShardedState
+    c = configs.c4_circuit(n=18, layers=3)
+    want = Q.simulate(c, Q.Engine.rh_dax).final.download()
+    be = DeviceBackend(c.n)
+    st = ShardedState(c.n, 1, 0, be, None, initial=c.initial)
+    assert be.known == c.initial and be.stale
+    st.run(circuit_ops(c))
+    st.flush()
+    assert be.known is None and not be.stale
+    assert bits_equal(st.local_numpy(), want)
+    st.reset(5)
+    assert be.stale
+    t = be.tensor  # an outside reader: the reset is materialised, the content no longer assumed
+    assert not be.stale and be.known is None
+    assert complex(t[5].item()) == 1.0 and float(t.abs().sum().item()) == 1.0
+
+
+def test_bench_sharded_arm_on_one_gpu():
+    """bench.py --sharded under torchrun with one rank: the N > 1 code path (NCCL process group,
+    DeviceBackend, ShardedState, exchange accounting, the JSON line) runs on one B200."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "1", "--sharded",
+           "--n-circuit", "22", "--steps", "2", "--warmup", "1", "--no-clocks"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["scaling"] == "strong" and d["gpu_launches"] > 0
+    assert any("NCCL" in s for s in d["comm_init"]) and d["exchange"]["remaps_per_step"] == 0
