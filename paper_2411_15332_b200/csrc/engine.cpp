@@ -328,13 +328,12 @@ void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low) {
         const auto t1 = std::chrono::steady_clock::now();
         lower_plan(n, ops, plan, low);
         const auto t2 = std::chrono::steady_clock::now();
-        jit_prepare(n, low.passes, low.pass_ops);
-        const auto t3 = std::chrono::steady_clock::now();
         if (show)
-            std::fprintf(stderr, "plan_ops %.2f ms, lower_plan %.2f ms, jit_prepare %.2f ms\n",
+            std::fprintf(stderr, "plan_ops %.2f ms, lower_plan %.2f ms\n",
                          std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                         std::chrono::duration<double, std::milli>(t2 - t1).count(),
-                         std::chrono::duration<double, std::milli>(t3 - t2).count());
+                         std::chrono::duration<double, std::milli>(t2 - t1).count());
+        // (the pass kernels are compiled in execute_fused, once the support masks that decide
+        // their form are known)
     } else {  // no 3-bit tile: one operation per pass
         for (std::size_t i = 0; i < ops.size(); ++i) {
             low.pass_ops.push_back({int(i)});
@@ -441,7 +440,11 @@ void execute_fused(qcs_state* s, const std::vector<FOp>& ops, Lowered& low, std:
     const std::int64_t init_index = init ? *init : -1;
     if (!apply_support(n, low, init_index)) fill_basis(s->amps, u64(1) << n, u64(init_index), s->stream);
     if (init) *init = -1;
+    // compile the plan's missing pass kernels in parallel before its first launch (a kept plan's
+    // later runs know their kernels and skip the source generation)
+    const bool first_run = !jit || jit->size() != low.passes.size();
     if (jit && jit->size() != low.passes.size()) jit->assign(low.passes.size(), nullptr);
+    if (first_run && n >= 3) jit_prepare(n, low.passes, low.pass_ops);
     for (std::size_t i = 0; i < low.passes.size(); ++i) {
         const auto& po = low.pass_ops[i];
         if (po.size() == 1) run_single(s, ops[std::size_t(po[0])], flips_dev + low.single_flip_off[i], low.single_flip_cnt[i]);

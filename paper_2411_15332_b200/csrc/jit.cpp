@@ -848,9 +848,11 @@ bool emit_rounds(Out& o, const PassParams& P, int begin, int end, unsigned threa
 
 // ---- persistent pipelined form (tile_device.cuh, "persistent pipelined passes")
 // Which passes take it: plain gate/diagonal passes (no sign steps, shared-memory rounds, skip or
-// support masks, tile lists, relabelled direct stores) whose tile moves as TMA boxes, with
-// enough tiles to fill the ring on every SM.  QCS_PERSIST: 0 off, 1 passes with 16-register
-// rounds (default: those run 2 CTAs per SM otherwise), 2 every eligible pass.
+// support masks, tile lists) with enough tiles to fill the ring on every SM.  QCS_PERSIST /
+// qcs_set_pipeline_mode: 0 off; 1 (default) passes with 16-register rounds whose tile moves as
+// TMA boxes and is stored through shared memory (those run 2 CTAs per SM otherwise); 2 every
+// eligible pass, including relabelled passes (direct stores) and cp.async-loaded tiles --
+// measured slower for passes of 8-register rounds (profiles/r02_ab_round_scheduler.txt).
 std::atomic<int> g_persist{[] { const char* e = std::getenv("QCS_PERSIST"); return e ? std::atoi(e) : 1; }()};
 int persist_knob() { return g_persist.load(std::memory_order_relaxed); }
 constexpr unsigned kPersistThreads = 512, kPersistRing = 196608;  // two groups of 256; bytes of ring
