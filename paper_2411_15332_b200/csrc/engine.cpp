@@ -297,7 +297,7 @@ void run_single(qcs_state* s, const FOp& f, const u64* flips_dev, u64 flip_cnt) 
     }
 }
 
-void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low);
+void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low, std::int64_t init = -1);
 
 // support: from a basis state, an amplitude can only become nonzero by flipping bits that
 // non-diagonal operations target (gates, butterflies); diagonals and scales never do
@@ -315,16 +315,129 @@ void compute_reached(const std::vector<FOp>& ops, Lowered& low) {
     }
 }
 
-void plan_fused(int n, const std::vector<FOp>& ops, Lowered& low) {
-    plan_fused_passes(n, ops, low);
+void plan_fused(int n, const std::vector<FOp>& ops, Lowered& low, std::int64_t init = -1) {
+    plan_fused_passes(n, ops, low, init);
     compute_reached(ops, low);
 }
 
-void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low) {
+// Deferred qubits.  From a basis state, the amplitudes stay confined to the sub-cube spanned by
+// the qubits that non-diagonal operations have targeted so far, and the passes skip every tile
+// outside it (apply_support).  So the operations that can run before ANY non-diagonal operation
+// on a set D of qubits -- everything outside D's light cone; operations on disjoint qubits and
+// diagonal ones commute -- cost 2^-|D| of a sweep each when they run FIRST.  split_deferred
+// partitions the list (order kept inside both parts); the two parts are planned separately so
+// that no early pass pulls a gate on D in.
+void split_deferred(const std::vector<FOp>& ops, u64 D, std::vector<int>& first, std::vector<int>& second) {
+    u64 blocked_nd = 0, blocked_d = 0;
+    for (std::size_t i = 0; i < ops.size(); ++i) {
+        const FOp& f = ops[i];
+        u64 targets = 0;
+        if (!f.diagonal)
+            for (int k = 0; k < f.K; ++k) targets |= u64(1) << f.tpos[k];
+        const bool reaches = !f.diagonal && (f.kind == TOP_SIGN || (targets & D));
+        const bool conflict = (f.touch & blocked_nd) || (!f.diagonal && (f.touch & blocked_d));
+        if (reaches || conflict) {
+            second.push_back(int(i));
+            (f.diagonal ? blocked_d : blocked_nd) |= f.touch;
+        } else {
+            first.push_back(int(i));
+        }
+    }
+}
+
+Plan plan_with_deferral(int n, const std::vector<FOp>& ops, int k) {
+    const u64 D = ((u64(1) << k) - 1) << (n - k);  // the k highest basis bits (reference qubits 0..k-1)
+    std::vector<int> first, second;
+    split_deferred(ops, D, first, second);
+    if (first.empty() || second.empty()) return plan_ops(n, ops, tile_max_bits());
+    Plan out;
+    for (const std::vector<int>* part : {&first, &second}) {
+        std::vector<FOp> sub;
+        sub.reserve(part->size());
+        for (int i : *part) sub.push_back(ops[std::size_t(i)]);
+        Plan p = plan_ops(n, sub, tile_max_bits());
+        for (auto& pass : p.passes) {
+            for (int& idx : pass.ops) idx = (*part)[std::size_t(idx)];
+            out.passes.push_back(std::move(pass));
+        }
+    }
+    return out;
+}
+
+// Estimated time of a plan run from a basis state (seconds): per pass, the larger of its FP64 time
+// and its HBM time over the tiles that compute / load / store under the support masks
+// apply_support will set (tiles outside the reached sub-cube are skipped), plus the launch and the
+// scheduling of skipped tiles.  A model for choosing between plans, not a prediction: gates count
+// 2.2 FP64 instructions per amplitude, other operations 0.4; the pipes run at the fractions the
+// C4 passes reach (FP64 0.75 of 148 x 64 lanes at 1.8 GHz, HBM 0.8 of 6.5 TB/s).
+double plan_cost_from_basis(int n, const std::vector<FOp>& ops, const Plan& plan) {
+    const u64 full = n >= 64 ? ~u64(0) : (u64(1) << n) - 1;
+    const std::size_t np = plan.passes.size();
+    std::vector<u64> zmask(np + 1, 0);
+    u64 reached = 0;
+    for (std::size_t i = 0; i < np; ++i) {
+        zmask[i] = full & ~plan.passes[i].tile & ~reached;
+        for (int idx : plan.passes[i].ops) {
+            const FOp& f = ops[std::size_t(idx)];
+            if (f.diagonal) continue;
+            if (f.kind == TOP_SIGN) reached = full;
+            for (int k = 0; k < f.K; ++k) reached |= u64(1) << f.tpos[k];
+        }
+    }
+    double total = 0.0;
+    for (std::size_t i = 0; i < np; ++i) {
+        const PlannedPass& p = plan.passes[i];
+        const int m = __builtin_popcountll(p.tile);
+        const double tiles = std::ldexp(1.0, n - m), amps = std::ldexp(1.0, n);
+        const double active = std::ldexp(1.0, -__builtin_popcountll(zmask[i]));
+        const double written = i + 1 < np ? std::ldexp(1.0, -__builtin_popcountll(zmask[i + 1] & ~p.tile)) : 1.0;
+        double fp64_per_amp = 0.0;
+        for (int idx : p.ops) {
+            const FOp& f = ops[std::size_t(idx)];
+            fp64_per_amp += (f.kind == TOP_GATE || f.kind == TOP_WHT) ? 2.2 : 0.4;
+        }
+        const double t_fp64 = fp64_per_amp * amps * active / (0.75 * 148.0 * 64.0 * 1.8e9);
+        const double t_hbm = 16.0 * amps * ((i == 0 ? 0.0 : active) + std::max(written, active)) / (0.8 * 6.5e12);
+        total += std::max(t_fp64, t_hbm) + 5e-6 + tiles * 1.4e-9;
+    }
+    return total;
+}
+
+// The plan of a circuit: plan_ops, or -- from a basis state, when the model says so -- the plan
+// with 1..3 deferred qubits.  QCS_DEFER: -1 (default) choose by the model, 0 off, k forced.
+Plan choose_plan(int n, const std::vector<FOp>& ops, std::int64_t init, bool show) {
+    static const int defer_env = [] { const char* v = std::getenv("QCS_DEFER"); return v ? std::atoi(v) : -1; }();
+    if (init >= 0 && defer_env > 0) return plan_with_deferral(n, ops, std::min(defer_env, n - 4));
+    Plan plan = plan_ops(n, ops, tile_max_bits());
+    if (!(init >= 0 && defer_env < 0 && n >= 20 && plan.passes.size() >= 3)) return plan;
+    double best = plan_cost_from_basis(n, ops, plan);
+    int gates = 0;
+    for (const FOp& f : ops) gates += !f.diagonal;
+    for (int k = 1; k <= 3 && k <= n - 13; ++k) {
+        // worth planning only when a good part of the circuit lies outside the light cone of the
+        // deferred qubits (layered nearest-neighbour circuits; not random pairings, whose cones
+        // cover everything after a few layers)
+        std::vector<int> first, second;
+        split_deferred(ops, ((u64(1) << k) - 1) << (n - k), first, second);
+        int early = 0;
+        for (int i : first) early += !ops[std::size_t(i)].diagonal;
+        if (second.empty() || early * 10 < gates * 4) break;
+        Plan cand = plan_with_deferral(n, ops, k);
+        const double c = plan_cost_from_basis(n, ops, cand);
+        if (show) std::fprintf(stderr, "defer %d: model %.1f ms (best so far %.1f ms)\n", k, 1e3 * c, 1e3 * best);
+        if (c < 0.97 * best) {
+            best = c;
+            plan = std::move(cand);
+        }
+    }
+    return plan;
+}
+
+void plan_fused_passes(int n, const std::vector<FOp>& ops, Lowered& low, std::int64_t init) {
     if (n >= 3) {
         static const bool show = std::getenv("QCS_PLAN_TIME") != nullptr;  // host planning cost, per stage
         const auto t0 = std::chrono::steady_clock::now();
-        Plan plan = plan_ops(n, ops, tile_max_bits());
+        Plan plan = choose_plan(n, ops, init, show);
         const auto t1 = std::chrono::steady_clock::now();
         lower_plan(n, ops, plan, low);
         const auto t2 = std::chrono::steady_clock::now();
@@ -456,7 +569,7 @@ void execute_fused(qcs_state* s, const std::vector<FOp>& ops, Lowered& low, std:
 void run_fused(qcs_state* s, const std::vector<FOp>& ops, std::int64_t* init = nullptr) {
     if (ops.empty()) return;
     Lowered low;
-    plan_fused(s->n, ops, low);
+    plan_fused(s->n, ops, low, init ? *init : -1);
     s->plan_loaded = 0;
     execute_fused(s, ops, low, init);
 }
@@ -807,7 +920,7 @@ void simulate(qcs_state* s, const qcs_step* steps, int nsteps, int engine, const
             cp->key = std::move(key);
             cp->ops = std::move(ops);
             cp->reports = std::move(reps);
-            plan_fused(n, cp->ops, cp->low);
+            plan_fused(n, cp->ops, cp->low, init);
             CachedPlan& e = s->plan_cache->insert(std::move(cp));
             execute_fused(s, e.ops, e.low, &init, &e.jit, e.id);
         }
@@ -825,17 +938,7 @@ void add_plan_stats(int n, const std::vector<FOp>& ops, qcs_plan_info* out, std:
         return;
     }
     Lowered low;
-    {
-        const auto t0 = std::chrono::steady_clock::now();
-        Plan plan = plan_ops(n, ops, tile_max_bits());
-        const auto t1 = std::chrono::steady_clock::now();
-        lower_plan(n, ops, plan, low);
-        const auto t2 = std::chrono::steady_clock::now();
-        if (std::getenv("QCS_PLAN_TIME"))
-            std::fprintf(stderr, "plan_ops %.2f ms, lower_plan %.2f ms\n",
-                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                         std::chrono::duration<double, std::milli>(t2 - t1).count());
-    }
+    plan_fused_passes(n, ops, low, init);  // the plan execute_fused would run
     compute_reached(ops, low);
     apply_support(n, low, init);  // from |init> (opts->reset), as execute_fused runs the plan
     const bool dump = std::getenv("QCS_PLAN_DUMP") != nullptr;  // planner debugging: rounds and ops
