@@ -251,6 +251,8 @@ struct PassParams {           // <= 32 KB: the kernel parameter limit
                                 // (outside the support the circuit has reached): nothing to load
     std::uint64_t smask, sval;  // tiles whose base bits under smask differ from sval are skipped: zero
                                 // and read as zero by the next pass (its zmask), nothing to write
+    std::uint64_t base_or;      // OR-ed into every tile's base: a launch that enumerates only the
+                                // tiles smask keeps (its runs leave the smask bits out) sets sval here
     RoundDesc rounds[kPassMaxOps];
     RegOp ops[kPassMaxOps];
     double2 pool[kPassPool];

@@ -471,6 +471,7 @@ __device__ __forceinline__ bool tile_begin(double2* a, const PassParams& P, cons
             tl >>= P.run_len[i];
         }
     }
+    base |= P.base_or;
     c.base = base;
     // zero, and the next pass reads it as zero: nothing to do (before any asynchronous copy)
     if (P.smask && (base & P.smask) != P.sval) return false;
@@ -612,7 +613,7 @@ __device__ __forceinline__ u64 tile_base_of(const PassParams& P, u64 tl) {
         base |= (tl & ((u64(1) << P.run_len[i]) - 1)) << P.run_pos[i];
         tl >>= P.run_len[i];
     }
-    return base;
+    return base | P.base_or;
 }
 __device__ __forceinline__ void group_sync(unsigned grp) {
     asm volatile("bar.sync %0, 256;\n" ::"r"(grp + 1u) : "memory");

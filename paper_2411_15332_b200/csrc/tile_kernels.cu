@@ -392,6 +392,14 @@ void tile_pass_shape(const PassParams& p, unsigned& f, unsigned& threads) {
     }
 }
 
+namespace {
+inline u64 tile_bits(const PassParams& p) {
+    u64 t = 0;
+    for (int b = 0; b < p.m; ++b) t |= u64(1) << p.bits[b];
+    return t;
+}
+}  // namespace
+
 void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev, const std::uint64_t* flipped_dev,
                       const std::uint64_t* tables_dev, cudaStream_t st, void** jit_slot) {
     if (p.m < 3 || p.m > kMaxBits || p.m > n) raise(QCS_ERR_ARG, "tile bits out of range");
@@ -410,8 +418,39 @@ void launch_tile_pass(double2* amps, int n, PassParams& p, const TileOp* big_dev
     const double read_frac = p.init ? 0.0 : p.zmask ? std::ldexp(1.0, -__builtin_popcountll(p.zmask)) : 1.0;
     const double active = p.smask ? std::ldexp(1.0, -__builtin_popcountll(p.smask)) : 1.0;  // not skipped
     TimedLaunch tl("tile_pass", 16.0 * active * (1.0 + read_frac) * double(tiles) * double(1u << p.m), st);
-    if (launch_tile_pass_jit(amps, p, f, big_dev, flipped_dev, tables_dev, tmap, unsigned(tiles), unsigned(threads), smem,
-                             tile_smem(kMaxBits), st, jit_slot)) {
+    // A pass that skips most of its tiles (smask: the tiles outside the support stay zero and
+    // unwritten) launches only the ones it keeps: the runs that turn a block index into a tile
+    // base leave the smask bits out, and sval is OR-ed in (base_or).  Launching all 2^(n-m) CTAs
+    // to have most return at once cost ~1.4 ms per pass at n=32 (a million empty CTAs).
+    static const bool no_compact = std::getenv("QCS_NO_COMPACT_LAUNCH") != nullptr;  // A/B switch
+    if (p.smask && !p.list_cnt && !no_compact) {
+        static thread_local PassParams q;
+        q = p;
+        q.nruns = 0;
+        int kept = 0;
+        for (int b = 0; b < n;) {
+            auto out = [&](int x) { return x < n && !(tile_bits(p) >> x & 1) && !(p.smask >> x & 1); };
+            if (!out(b)) {
+                ++b;
+                continue;
+            }
+            int e = b;
+            while (out(e)) ++e;
+            q.run_pos[q.nruns] = std::uint8_t(b);
+            q.run_len[q.nruns++] = std::uint8_t(e - b);
+            kept += e - b;
+            b = e;
+        }
+        q.base_or = p.sval & p.smask;
+        const u64 few = u64(1) << kept;
+        if (launch_tile_pass_jit(amps, q, f, big_dev, flipped_dev, tables_dev, tmap, unsigned(few), unsigned(threads), smem,
+                                 tile_smem(kMaxBits), st, jit_slot)) {
+            check_launch("qcs_pass");
+            return;
+        }
+        // (the interpreter kernels below take the full grid and skip in tile_begin)
+    } else if (launch_tile_pass_jit(amps, p, f, big_dev, flipped_dev, tables_dev, tmap, unsigned(tiles), unsigned(threads), smem,
+                                    tile_smem(kMaxBits), st, jit_slot)) {
         check_launch("qcs_pass");
         return;
     }
