@@ -131,3 +131,30 @@ def test_state_distance_small(Q):
     mx, l2 = a.distance(b)
     assert abs(mx - 1e-3) < 1e-15 and abs(l2 - 1e-3) < 1e-15
     assert a.distance(a) == (0.0, 0.0)
+
+
+@pytest.mark.parametrize("initial", [0, (1 << 23) - 1, (0b101 << 21) | 0x1234])
+def test_deferred_qubits_from_any_basis_state(Q, cfg, initial):
+    """n = 24 (the planner defers the top qubits of a layered nearest-neighbour circuit run from a
+    basis state: the operations outside their light cone run first, on the sub-cube the state is
+    still confined to).  The fused result must equal the per-gate kernels' -- which run the steps
+    in circuit order on the whole state -- within the 1e-12 bar, whatever the basis state's bits
+    on the deferred qubits; and with fewer layers than the ring is long the plan does defer
+    (fewer FP64 instructions per amplitude than gates would cost on the whole state)."""
+    n = 24
+    c = cfg.c4_circuit(n, layers=6)
+    c.initial = initial
+    st = Q.plan_stats(c)
+    gates = sum(len(s.placements) for s in c.steps if int(s.kind) == 0 and not s.is_hadamard_all(n))
+    assert st["fp64_ops"] / float(1 << n) < 0.9 * (2.0 * 6 * n), (st, gates)  # RY alone would cost 2 per qubit-layer
+    a = Q.DeviceState(n)
+    b = Q.DeviceState(n)
+    try:
+        Q.simulate(c, Q.Engine.rh_dax, state=a)
+        assert abs(a.norm() - 1.0) <= 1e-12
+        per_gate(Q, c, b)
+        mx, l2 = a.distance(b)
+        assert mx <= TOL_AMP and l2 <= TOL_L2, (initial, mx, l2)
+    finally:
+        a.close()
+        b.close()
