@@ -16,7 +16,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 namespace qcs {
 
@@ -424,11 +426,44 @@ double plan_cost_from_basis(int n, const std::vector<FOp>& ops, const Plan& plan
 
 // The plan of a circuit: plan_ops, or -- from a basis state, when the model says so -- the plan
 // with 1..3 deferred qubits.  QCS_DEFER: -1 (default) choose by the model, 0 off, k forced.
+// The model's choice depends on the circuit's structure only (which operations touch which qubits,
+// which are diagonal), not on its angles: a variational loop that sends the same circuit with
+// fresh angles pays for the candidate plans once (structure hash -> k; process-wide, bounded).
+std::uint64_t structure_hash(int n, const std::vector<FOp>& ops) {
+    std::uint64_t h = 1469598103934665603ull ^ std::uint64_t(n);
+    auto mix = [&](std::uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+    for (const FOp& f : ops) {
+        mix(std::uint64_t(f.kind) | (std::uint64_t(f.diagonal) << 8) | (std::uint64_t(f.K) << 16) | (std::uint64_t(f.dk) << 24));
+        mix(f.touch);
+        mix(f.ctrl_mask);
+        for (int k = 0; k < f.K; ++k) mix(std::uint64_t(f.tpos[k]) + 0x9e37u);
+    }
+    return h;
+}
+std::mutex g_defer_mu;
+std::unordered_map<std::uint64_t, int> g_defer_choice;
+
 Plan choose_plan(int n, const std::vector<FOp>& ops, std::int64_t init, bool show) {
     static const int defer_env = [] { const char* v = std::getenv("QCS_DEFER"); return v ? std::atoi(v) : -1; }();
     if (init >= 0 && defer_env > 0) return plan_with_deferral(n, ops, std::min(defer_env, n - 4));
+    if (!(init >= 0 && defer_env < 0 && n >= 20)) return plan_ops(n, ops, tile_max_bits());
+    const std::uint64_t key = structure_hash(n, ops);
+    {
+        std::lock_guard<std::mutex> lk(g_defer_mu);
+        auto it = g_defer_choice.find(key);
+        if (it != g_defer_choice.end())
+            return it->second > 0 ? plan_with_deferral(n, ops, it->second) : plan_ops(n, ops, tile_max_bits());
+    }
+    auto remember = [&](int k) {
+        std::lock_guard<std::mutex> lk(g_defer_mu);
+        if (g_defer_choice.size() >= 4096) g_defer_choice.clear();
+        g_defer_choice[key] = k;
+    };
     Plan plan = plan_ops(n, ops, tile_max_bits());
-    if (!(init >= 0 && defer_env < 0 && n >= 20 && plan.passes.size() >= 3)) return plan;
+    if (plan.passes.size() < 3) {
+        remember(0);
+        return plan;
+    }
     double best = plan_cost_from_basis(n, ops, plan);
     int gates = 0, best_k = 0;
     for (const FOp& f : ops) gates += !f.diagonal;
@@ -452,7 +487,7 @@ Plan choose_plan(int n, const std::vector<FOp>& ops, std::int64_t init, bool sho
     }
     // (nested levels -- a wider set deferred first, e.g. {4, 2} or {6, 2} -- model within 3% of the
     // single level for C4 and cost two more plans: not searched; plan_with_levels takes them)
-    (void)best_k;
+    remember(best_k);
     return plan;
 }
 
