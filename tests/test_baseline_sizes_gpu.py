@@ -158,3 +158,43 @@ def test_deferred_qubits_from_any_basis_state(Q, cfg, initial):
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_deferred_qubits_random_chain_circuits(Q, seed):
+    """Random layered circuits on a chain at n = 21..23: any one-qubit catalog gate on every qubit
+    per layer (X-like, diagonal, dense, complex), then random diagonal couplings on
+    nearest-neighbour pairs (a few of them long-range), from a random basis state.  Few layers
+    against the chain's length, so the planner defers the top qubits; fused vs the per-gate
+    kernels within 1e-12."""
+    rng = np.random.default_rng(4200 + seed)
+    n = int(rng.integers(21, 24))
+    one = [i for i in Q.gate_catalog() if i.arity == 1]
+    diag2 = ["Controlled-Z", "CPhase", "RZZ", "CRZ", "CU1"]
+    steps = [Q.hadamard_all(n)] if seed % 2 == 0 else []
+    for _ in range(int(rng.integers(3, 6))):
+        pl = []
+        for q in range(n):
+            info = one[int(rng.integers(0, len(one)))]
+            pl.append(Q.Placement(Q.gate_catalog_lookup(info.name, list(rng.uniform(0, 2 * np.pi, info.param_count))), q))
+        steps.append(Q.CircuitStep.of_gates(pl))
+        for start in (0, 1):
+            for q in range(start, n - 1, 2):
+                name = diag2[int(rng.integers(0, len(diag2)))]
+                info = next(i for i in Q.gate_catalog() if i.name == name)
+                g = Q.gate_catalog_lookup(name, list(rng.uniform(0, 2 * np.pi, info.param_count)))
+                far = int(rng.integers(0, n)) if rng.random() < 0.05 else q + 1
+                if far == q:
+                    far = q + 1
+                steps.append(Q.CircuitStep.of_gates([Q.Placement(g, qubits=[q, far])]))
+    c = Q.Circuit(n, steps, int(rng.integers(0, 1 << n)))
+    a = Q.DeviceState(n)
+    b = Q.DeviceState(n)
+    try:
+        Q.simulate(c, Q.Engine.rh_dax, state=a)
+        per_gate(Q, c, b)
+        mx, l2 = a.distance(b)
+        assert mx <= TOL_AMP and l2 <= TOL_L2, (seed, n, mx, l2)
+    finally:
+        a.close()
+        b.close()
